@@ -1,0 +1,140 @@
+/*
+ * f2lin_gpu.h — C-ABI drop-in surface of the B200 GF(2) PLS engine.
+ *
+ * Every entry point below replaces one entry point of the reference C++ API
+ * (`f2lin`, /root/reference/proj/include/f2lin/*.hpp); the cited file:line is
+ * the interface it stands in for.  Argument meaning and error behaviour mirror
+ * the reference: each `std::invalid_argument` becomes F2_INVALID_ARGUMENT, each
+ * `std::out_of_range` becomes F2_OUT_OF_RANGE, and outputs are written only on
+ * the paths where the reference would have written them.
+ *
+ * Conventions
+ *  - A matrix lives in HBM (`f2_matrix`), bit-packed row-major in 64-bit words,
+ *    bit j of a row in word j/64 at position j%64 (bitmat.hpp:3-6).  Device rows
+ *    are padded to a multiple of 16 words (128 B); padding bits are zero.
+ *  - Host word arrays passed to upload/download and to the *_host entry points
+ *    use any row stride >= ceil(ncols/64) words (the reference uses exactly that).
+ *  - Permutations are LAPACK-style transposition vectors of uint64_t, the width
+ *    of the reference's std::size_t (perm.hpp:3-7).
+ *  - Windows are half-open row/column bounds (MatrixWindow, bitmat.hpp:239-250).
+ *  - Calls are synchronous on return and stream-ordered on the library's stream.
+ *  - There is no CPU fallback: without a CUDA device every compute entry point
+ *    returns F2_NO_DEVICE.
+ */
+#ifndef F2LIN_GPU_H
+#define F2LIN_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum f2_status {
+    F2_OK = 0,
+    F2_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    F2_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference      */
+    F2_CUDA_ERROR = 3,
+    F2_NO_DEVICE = 4,
+    F2_OUT_OF_MEMORY = 5
+};
+
+/* enum class Algorithm — pls.hpp:18 */
+enum f2_algorithm { F2_ALG_GAUSS = 0, F2_ALG_M4RI = 1, F2_ALG_MMPF = 2, F2_ALG_PLS = 3, F2_ALG_HYBRID = 4 };
+
+/* struct EliminationConfig — pls.hpp:26-35 (0 = automatic, as in the reference) */
+typedef struct f2_elim_config {
+    unsigned k;
+    uint64_t cutoff_bytes;
+    double hybrid_threshold;
+    int algorithm;
+} f2_elim_config;
+
+/* MatrixWindow bounds — bitmat.hpp:239-250 (r_start, c_start, r_end, c_end) */
+typedef struct f2_window {
+    size_t r0, c0, r1, c1;
+} f2_window;
+
+/* class BitMatrix — bitmat.hpp:90-234, resident in HBM */
+typedef struct f2_matrix f2_matrix;
+
+/* ---- library / device ------------------------------------------------- */
+const char* f2_last_error(void);
+int f2_device_count(void);
+int f2_set_device(int device);
+
+/* ---- BitMatrix lifecycle (bitmat.hpp:94-140) ---------------------------- */
+int f2_matrix_create(size_t nrows, size_t ncols, f2_matrix** out);      /* BitMatrix(m,n), zeroed   */
+void f2_matrix_destroy(f2_matrix* a);                                    /* ~BitMatrix               */
+size_t f2_matrix_nrows(const f2_matrix* a);                              /* nrows()  bitmat.hpp:142  */
+size_t f2_matrix_ncols(const f2_matrix* a);                              /* ncols()  bitmat.hpp:143  */
+size_t f2_matrix_stride(const f2_matrix* a);                             /* device row stride, words */
+uint64_t* f2_matrix_device_ptr(f2_matrix* a);                            /* raw HBM words            */
+int f2_matrix_upload(f2_matrix* a, const uint64_t* host, size_t host_stride_words);
+int f2_matrix_download(const f2_matrix* a, uint64_t* host, size_t host_stride_words);
+int f2_matrix_copy(f2_matrix* dst, const f2_matrix* src);               /* BitMatrix copy (deep)    */
+int f2_matrix_clear(f2_matrix* a);                                       /* clear()  bitmat.hpp:207  */
+/* BitMatrix::randomize — bitmat.hpp:196, bitmat.cpp:136-154: same SplitMix64
+ * stream, bit for bit, generated on the device (counter-based). */
+int f2_matrix_randomize(f2_matrix* a, double density, uint64_t seed);
+/* order-sensitive fingerprint over the reference packing (tests/oracle_lib.digest) */
+int f2_matrix_digest(const f2_matrix* a, uint64_t* out);
+
+/* pinned host memory for the end-to-end path */
+void* f2_host_alloc(size_t bytes);
+void f2_host_free(void* p);
+
+/* ---- PLS decomposition ------------------------------------------------- */
+/* std::size_t mmpf_pls(MatrixWindow a, span<size_t> p, span<size_t> q, unsigned k=0)
+ *   — mmpf.hpp:35-36, mmpf.cpp:81-121.  p has w.r1-w.r0 entries, q has w.c1-w.c0. */
+int f2_mmpf_pls(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen,
+                unsigned k, uint64_t* rank);
+/* std::size_t pls_recursive(MatrixWindow, span p, span q, const EliminationConfig&)
+ *   — pls.hpp:42-43, pls.cpp:105-113.  cfg may be NULL (= {}). */
+int f2_pls_recursive(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen,
+                     const f2_elim_config* cfg, uint64_t* rank);
+/* Host-buffer variants (the call a caller holding a host BitMatrix makes):
+ * upload, decompose, download in one call.  `words` is updated in place. */
+int f2_mmpf_pls_host(uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
+                     uint64_t* q, unsigned k, uint64_t* rank);
+int f2_pls_recursive_host(uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
+                          uint64_t* q, const f2_elim_config* cfg, uint64_t* rank);
+
+/* std::size_t default_cutoff_bytes() — pls.cpp:37-53 (host CPU L2, F2_L2_BYTES) */
+uint64_t f2_default_cutoff_bytes(void);
+/* detail::auto_table_bits — mul.cpp:9-14 */
+unsigned f2_auto_table_bits(size_t dim);
+
+/* ---- multiply / triangular solve --------------------------------------- */
+/* void addmul(MatrixWindow c, MatrixWindow a, MatrixWindow b, unsigned k=0) — mul.hpp:20, mul.cpp:102-107 */
+int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix* b, f2_window wb,
+              unsigned k);
+/* BitMatrix mul_m4rm(const BitMatrix&, const BitMatrix&, unsigned k=0) — mul.hpp:17, mul.cpp:90-100.
+ * *out is created by the call. */
+int f2_mul_m4rm(const f2_matrix* a, const f2_matrix* b, unsigned k, f2_matrix** out);
+/* void trsm_lower_left_unit(MatrixWindow l, MatrixWindow b) — mul.hpp:24, mul.cpp:109-131 */
+int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window wb);
+/* void compress_columns(BitMatrix&, rank, const Permutation& q) — perm.hpp:61, perm.cpp:55-60 */
+int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t qlen);
+/* Permutation::apply_rows / apply_rows_inverse — perm.hpp:42-45, perm.cpp:29-38 */
+int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int inverse);
+
+/* ---- instrumentation (bench.py roofline) -------------------------------- */
+/* When enabled, the library brackets every launch of kernel family `kind`
+ * with CUDA events on its own stream and accumulates launches, device ms and
+ * the launch's algorithmic work (bytes for the table-apply, bit-ops for the
+ * multiply).  kind: 0 = table-apply/M4RM multiply, 1 = leaf pivot search,
+ * 2 = pivot-row TRSM, 3 = everything else. */
+int f2_stats_enable(int enable);
+int f2_stats_get(int kind, uint64_t* launches, double* ms, double* bytes, double* bitops);
+int f2_stats_reset(void);
+/* kernel launches issued by the last compute call (all families) */
+uint64_t f2_last_launch_count(void);
+/* engine tuning (panel width in bits for pls_recursive; 0 = default) */
+int f2_set_panel_bits(unsigned bits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* F2LIN_GPU_H */

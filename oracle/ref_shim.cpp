@@ -1,0 +1,153 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// C-ABI shim over the *unmodified* reference library sources compiled from
+// /root/reference/proj/src (see oracle/Makefile).  It lets the parity tests and
+// bench.py's `--impl reference` arm drive the reference's own entry points:
+//   mmpf_pls            (proj/include/f2lin/mmpf.hpp:35-37, proj/src/mmpf.cpp:118-133)
+//   pls_recursive       (proj/include/f2lin/pls.hpp:42-47, proj/src/pls.cpp:105-126)
+//   gauss_pls           (proj/src/gauss.cpp:26-55)
+//   rref_from_pls       (proj/src/pls.cpp:128-161)
+//   mul_m4rm / addmul   (proj/src/mul.cpp:90-107)
+//   trsm_*_left_unit    (proj/src/mul.cpp:109-157)
+//   BitMatrix::randomize(proj/src/bitmat.cpp:136-154)
+// Host arrays use the reference's packing: row-major, stride = ceil(ncols/64)
+// 64-bit words, LSB = lowest column (bitmat.hpp:3-6).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <vector>
+
+#include <f2lin/gauss.hpp>
+#include <f2lin/mmpf.hpp>
+#include <f2lin/mul.hpp>
+#include <f2lin/perm.hpp>
+#include <f2lin/pls.hpp>
+
+using namespace f2lin;
+
+namespace {
+
+BitMatrix load(const uint64_t* w, size_t m, size_t n) {
+    BitMatrix a(m, n);
+    size_t s = a.stride();
+    for (size_t i = 0; i < m; ++i) std::memcpy(a.row(i), w + i * s, s * 8);
+    return a;
+}
+
+void store(const BitMatrix& a, uint64_t* w) {
+    size_t s = a.stride();
+    for (size_t i = 0; i < a.nrows(); ++i) std::memcpy(w + i * s, a.row(i), s * 8);
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (const std::out_of_range&) {
+        return 2;
+    } catch (...) {
+        return 9;
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int ref_randomize(uint64_t* w, size_t m, size_t n, double density, uint64_t seed) {
+    return guard([&] {
+        BitMatrix a(m, n);
+        a.randomize(density, seed);
+        store(a, w);
+    });
+}
+
+int ref_mmpf_pls(uint64_t* w, size_t m, size_t n, unsigned k, uint64_t* p, uint64_t* q,
+                 uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        Permutation P, Q;
+        *rank = mmpf_pls(a, P, Q, k);
+        store(a, w);
+        for (size_t i = 0; i < m; ++i) p[i] = P[i];
+        for (size_t i = 0; i < n; ++i) q[i] = Q[i];
+    });
+}
+
+int ref_pls_recursive(uint64_t* w, size_t m, size_t n, unsigned k, uint64_t cutoff, uint64_t* p,
+                      uint64_t* q, uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        Permutation P, Q;
+        EliminationConfig cfg;
+        cfg.k = k;
+        cfg.cutoff_bytes = cutoff;
+        *rank = pls_recursive(a, P, Q, cfg);
+        store(a, w);
+        for (size_t i = 0; i < m; ++i) p[i] = P[i];
+        for (size_t i = 0; i < n; ++i) q[i] = Q[i];
+    });
+}
+
+int ref_gauss_pls(uint64_t* w, size_t m, size_t n, uint64_t* p, uint64_t* q, uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        Permutation P, Q;
+        *rank = gauss_pls(a, P, Q);
+        store(a, w);
+        for (size_t i = 0; i < m; ++i) p[i] = P[i];
+        for (size_t i = 0; i < n; ++i) q[i] = Q[i];
+    });
+}
+
+int ref_rref_from_pls(uint64_t* w, size_t m, size_t n, uint64_t rank, const uint64_t* q,
+                      size_t qlen) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        std::vector<size_t> qv(q, q + qlen);
+        rref_from_pls(a.view(), rank, std::span<const size_t>(qv));
+        store(a, w);
+    });
+}
+
+int ref_mul_m4rm(const uint64_t* a, size_t m, size_t s, const uint64_t* b, size_t n, unsigned k,
+                 uint64_t* c) {
+    return guard([&] {
+        BitMatrix A = load(a, m, s), B = load(b, s, n);
+        store(mul_m4rm(A, B, k), c);
+    });
+}
+
+int ref_mul_naive(const uint64_t* a, size_t m, size_t s, const uint64_t* b, size_t n,
+                  uint64_t* c) {
+    return guard([&] {
+        BitMatrix A = load(a, m, s), B = load(b, s, n);
+        store(mul_naive(A, B), c);
+    });
+}
+
+int ref_trsm_lower_left_unit(const uint64_t* l, size_t r, uint64_t* b, size_t n) {
+    return guard([&] {
+        BitMatrix L = load(l, r, r), B = load(b, r, n);
+        trsm_lower_left_unit(L.view(), B.view());
+        store(B, b);
+    });
+}
+
+int ref_trsm_upper_left_unit(const uint64_t* u, size_t r, uint64_t* b, size_t n) {
+    return guard([&] {
+        BitMatrix U = load(u, r, r), B = load(b, r, n);
+        trsm_upper_left_unit(U.view(), B.view());
+        store(B, b);
+    });
+}
+
+size_t ref_default_cutoff_bytes() { return default_cutoff_bytes(); }
+
+unsigned ref_auto_table_bits(size_t dim) { return detail::auto_table_bits(dim); }
+
+} // extern "C"

@@ -1,0 +1,887 @@
+// Host side of the B200 GF(2) PLS engine and its C ABI (include/f2lin_gpu.h).
+//
+// The engine is a blocked right-looking PLS.  The matrix is walked in panels of
+// W columns (64 for the MMPF entry point, 1024 by default for the recursive
+// entry point); each panel is walked in 64-column leaves.  Per leaf:
+//   k_leaf_pivot     exact pivot search (gauss.cpp:33-44 rule)          1 CTA
+//   k_row_moves      the leaf's transpositions applied to whole rows     (perm.cpp:8-16)
+//   k_leaf_finalize  elimination of the leaf word -> L coefficients      (gauss.cpp:47-49)
+//   k_pivot_trsm     leaf pivot rows solved over the rest of the panel   (mul.cpp:109-131)
+//   k_table_apply    Gray-table update of the rest of the panel          (m4ri.cpp:28-38)
+// Per panel:
+//   k_pivot_trsm     panel pivot rows solved over the trailing columns
+//   k_table_apply    Schur complement C ^= L21 * U12 (M4RM, mul.cpp:21-68)
+// and finally k_compress (compress_columns, perm.cpp:18-21) when Q != identity.
+// Every row offset and pivot count lives in device memory (PlsState), so the
+// launch sequence is fixed by (m, n, W) alone and the host never waits on the
+// GPU until the end of the call.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <unistd.h>
+
+#include "../../include/f2lin_gpu.h"
+#include "f2gpu.cuh"
+#include "kernels.cuh"
+
+using namespace f2g;
+
+struct f2_matrix {
+    size_t m = 0, n = 0, stride = 0;
+    uint64_t* d = nullptr;
+    int device = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;  // one compute call at a time per process (shared stream + workspace)
+
+struct Ctx {
+    bool init = false;
+    int device = -1;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    // engine workspace
+    PlsState* st = nullptr;
+    int64_t* P = nullptr;
+    int64_t* Qp = nullptr;
+    size_t cap_m = 0, cap_q = 0;
+    int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
+    size_t h_r_cap = 0;
+    unsigned long long* d_digest = nullptr;
+    // stats
+    bool stats = false;
+    uint64_t launches = 0;
+    struct Family {
+        uint64_t n = 0;
+        double ms = 0, bytes = 0, bitops = 0;
+    } fam[4];
+    unsigned panel_bits = 1024;
+};
+Ctx g;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? F2_OUT_OF_MEMORY : F2_CUDA_ERROR;
+}
+
+#define CK(x)                                          \
+    do {                                               \
+        cudaError_t e_ = (x);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+    } while (0)
+
+int ensure_init() {
+    if (g.init) return F2_OK;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(F2_NO_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    }
+    if (g.device < 0) g.device = 0;
+    CK(cudaSetDevice(g.device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, g.device));
+    if (prop.major < 10) return fail(F2_NO_DEVICE, "kernels are built for sm_100a (B200)");
+    g.nsm = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&g.st, sizeof(PlsState)));
+    CK(cudaMalloc(&g.d_digest, sizeof(unsigned long long)));
+    setup_leaf_kernels();
+    setup_trsm_kernels();
+    setup_m4rm_kernels();
+    setup_misc_kernels();
+    CK(cudaGetLastError());
+    g.init = true;
+    return F2_OK;
+}
+
+int ensure_workspace(size_t m, size_t nq, size_t npanels) {
+    if (m > g.cap_m) {
+        if (g.P) cudaFree(g.P);
+        CK(cudaMalloc(&g.P, sizeof(int64_t) * std::max<size_t>(m, 1)));
+        g.cap_m = m;
+    }
+    if (nq > g.cap_q) {
+        if (g.Qp) cudaFree(g.Qp);
+        CK(cudaMalloc(&g.Qp, sizeof(int64_t) * std::max<size_t>(nq, 1)));
+        g.cap_q = nq;
+    }
+    if (npanels > g.h_r_cap) {
+        if (g.h_r) cudaFreeHost(g.h_r);
+        CK(cudaMallocHost(&g.h_r, sizeof(int64_t) * npanels));
+        g.h_r_cap = npanels;
+    }
+    return F2_OK;
+}
+
+size_t stride_for(size_t ncols) {
+    size_t w = (ncols + 63) / 64;
+    return (w + 15) / 16 * 16;
+}
+
+Mat mat_of(const f2_matrix* a) {
+    return Mat{a->d, static_cast<int64_t>(a->m), static_cast<int64_t>(a->n), static_cast<int64_t>(a->stride)};
+}
+
+int alloc_matrix(size_t m, size_t n, f2_matrix** out) {
+    f2_matrix* a = new f2_matrix;
+    a->m = m;
+    a->n = n;
+    a->stride = stride_for(n);
+    a->device = g.device;
+    size_t bytes = std::max<size_t>(m * a->stride * 8, 8);
+    cudaError_t e = cudaMalloc(&a->d, bytes);
+    if (e != cudaSuccess) {
+        delete a;
+        return cuda_fail(e, "cudaMalloc(matrix)");
+    }
+    e = cudaMemsetAsync(a->d, 0, bytes, g.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(matrix)");
+    *out = a;
+    return F2_OK;
+}
+
+// ---- stats ------------------------------------------------------------------
+struct Timed {
+    int fam;
+    cudaEvent_t e0, e1;
+    double bytes, bitops;
+};
+std::vector<Timed> g_timed;
+
+struct LaunchTimer {
+    int fam;
+    double bytes, bitops;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    LaunchTimer(int f, double by, double bo) : fam(f), bytes(by), bitops(bo) {
+        ++g.launches;
+        if (g.stats) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, g.stream);
+        }
+    }
+    ~LaunchTimer() {
+        if (g.stats) {
+            cudaEventRecord(e1, g.stream);
+            g_timed.push_back({fam, e0, e1, bytes, bitops});
+        }
+    }
+};
+
+void collect_stats() {
+    if (g_timed.empty()) return;
+    cudaStreamSynchronize(g.stream);
+    for (auto& t : g_timed) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t.e0, t.e1);
+        auto& f = g.fam[t.fam];
+        f.n += 1;
+        f.ms += ms;
+        f.bytes += t.bytes;
+        f.bitops += t.bitops;
+        cudaEventDestroy(t.e0);
+        cudaEventDestroy(t.e1);
+    }
+    g_timed.clear();
+}
+
+// ---- Q of pls_recursive -------------------------------------------------------
+// pls_recursive_impl's Q bookkeeping (proj/src/pls.cpp:63-103) replayed from the
+// pivot columns: leaf rule :71, cut :74-75, merge :96-98.  The recursion's P,
+// packed matrix and Q[0..rank) equal the Gaussian ones; only the tail depends on
+// the recursion shape, and only through (m, n, cutoff, pivot columns).
+void replay_q(size_t m, size_t n, uint64_t cutoff, const int64_t* piv, size_t npiv, uint64_t* q) {
+    for (size_t j = 0; j < n; ++j) q[j] = j;
+    if (m == 0 || n == 0) return;
+    if (n <= 64 || static_cast<uint64_t>(m) * ((n + 7) / 8) <= cutoff) {
+        for (size_t t = 0; t < npiv; ++t) q[t] = static_cast<uint64_t>(piv[t]);
+        return;
+    }
+    size_t n0 = ((n / 2 + 63) / 64) * 64;
+    if (n0 >= n) n0 = n / 2;
+    size_t r0 = 0;
+    while (r0 < npiv && static_cast<size_t>(piv[r0]) < n0) ++r0;
+    replay_q(m, n0, cutoff, piv, r0, q);
+    const size_t r1 = npiv - r0;
+    std::vector<int64_t> sub(r1);
+    for (size_t t = 0; t < r1; ++t) sub[t] = piv[r0 + t] - static_cast<int64_t>(n0);
+    replay_q(m - r0, n - n0, cutoff, sub.data(), r1, q + n0);
+    for (size_t i = n0; i < n; ++i) q[i] += n0;
+    for (size_t t = 0; t < r1; ++t) q[r0 + t] = q[n0 + t];
+}
+
+// ---- the engine -------------------------------------------------------------
+struct EngineOut {
+    int64_t rank = 0;
+    std::vector<int64_t> P;   // P[0..rank)
+    std::vector<int64_t> Qp;  // pivot columns
+};
+
+int run_engine(const Mat& A, unsigned W, EngineOut& out) {
+    const int64_t m = A.m, n = A.n;
+    out.rank = 0;
+    out.P.clear();
+    out.Qp.clear();
+    if (m == 0 || n == 0) return F2_OK;
+    const int64_t nw = (n + 63) / 64;
+    const int64_t npanels = (n + W - 1) / W;
+    int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels));
+    if (rc) return rc;
+    cudaStream_t s = g.stream;
+    CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), s));
+    std::vector<cudaEvent_t> evs;
+    evs.reserve(npanels);
+    int64_t checked = 0;
+    bool stop = false;
+
+    for (int64_t pi = 0; pi < npanels && !stop; ++pi) {
+        const int64_t c = pi * W;
+        const int64_t cw = std::min<int64_t>(W, n - c);
+        const int nleaves = static_cast<int>((cw + 63) / 64);
+        const int64_t pw0 = c / 64, pw1 = pw0 + nleaves;
+        for (int j = 0; j < nleaves; ++j) {
+            const int64_t wl = pw0 + j;
+            const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
+            {
+                LaunchTimer t(1, 0, 0);
+                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp);
+            }
+            {
+                LaunchTimer t(3, 0, 0);
+                launch_row_moves(s, A, nw, g.st);
+            }
+            {
+                LaunchTimer t(3, 0, 0);
+                launch_leaf_finalize(s, A, wl, g.st, g.nsm);
+            }
+            if (wl + 1 < pw1) {
+                {
+                    LaunchTimer t(2, 0, 0);
+                    launch_pivot_trsm(s, A, wl, 1, wl + 1, pw1, g.st, PivotSet{0, 0, 0}, nullptr);
+                }
+                TableApply ta{};
+                ta.C = A;
+                ta.c_r1 = m;
+                ta.cw0 = wl + 1;
+                ta.cw1 = pw1;
+                ta.A = A;
+                ta.aw0 = wl;
+                ta.kw = 1;
+                ta.kbits = lw;
+                ta.B = A;
+                ta.bw0 = wl + 1;
+                ta.brow = g.st->brow + 64 * j;
+                ta.row_mode = ROWS_AFTER_LEAF;
+                ta.st = g.st;
+                LaunchTimer t(3, 0, 0);
+                launch_table_apply(s, ta, g.nsm);
+            }
+        }
+        if (pw1 < nw) {
+            {
+                LaunchTimer t(2, 0, 0);
+                launch_pivot_trsm(s, A, pw0, nleaves, pw1, nw, g.st, PivotSet{1, 0, 0}, nullptr);
+            }
+            TableApply ta{};
+            ta.C = A;
+            ta.c_r1 = m;
+            ta.cw0 = pw1;
+            ta.cw1 = nw;
+            ta.A = A;
+            ta.aw0 = pw0;
+            ta.kw = nleaves;
+            ta.kbits = cw;
+            ta.B = A;
+            ta.bw0 = pw1;
+            ta.brow = g.st->brow;
+            ta.row_mode = ROWS_AFTER_PANEL;
+            ta.st = g.st;
+            // work is data dependent; filled in from the pivots after the call
+            LaunchTimer t(0, static_cast<double>(pi), -1.0);
+            launch_table_apply(s, ta, g.nsm);
+        }
+        // early exit once every row is a pivot: snapshot r without blocking
+        CK(cudaMemcpyAsync(g.h_r + pi, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, s));
+        evs.push_back(ev);
+        while (checked < static_cast<int64_t>(evs.size()) && cudaEventQuery(evs[checked]) == cudaSuccess) {
+            if (g.h_r[checked] >= m) stop = true;
+            ++checked;
+        }
+    }
+    CK(cudaGetLastError());
+    int64_t r = 0;
+    CK(cudaMemcpyAsync(&r, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (auto ev : evs) cudaEventDestroy(ev);
+    out.rank = r;
+    out.P.resize(r);
+    out.Qp.resize(r);
+    if (r) {
+        CK(cudaMemcpy(out.P.data(), g.P, sizeof(int64_t) * r, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(out.Qp.data(), g.Qp, sizeof(int64_t) * r, cudaMemcpyDeviceToHost));
+    }
+    bool ident = true;
+    for (int64_t t = 0; t < r && ident; ++t) ident = out.Qp[t] == t;
+    if (!ident) {
+        LaunchTimer t(3, 0, 0);
+        launch_compress(s, A, r, g.Qp, g.nsm);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    // resolve the data-dependent work of the timed Schur launches
+    if (g.stats) {
+        for (auto& tm : g_timed) {
+            if (tm.fam != 0 || tm.bitops >= 0) continue;
+            const int64_t pi = static_cast<int64_t>(tm.bytes);
+            const int64_t c = pi * W, cw = std::min<int64_t>(W, n - c);
+            int64_t before = 0, in = 0;
+            for (int64_t t2 = 0; t2 < r; ++t2) {
+                if (out.Qp[t2] < c) ++before;
+                else if (out.Qp[t2] < c + cw) ++in;
+            }
+            const double rows = static_cast<double>(m - before - in);
+            const double tcols = static_cast<double>(n - c - cw);
+            const double tbytes = 8.0 * static_cast<double>(nw - (c + cw) / 64);
+            tm.bitops = in ? 2.0 * rows * in * tcols : 0.0;
+            // algorithmic HBM bytes: C read+write, the coefficient words, the B rows
+            tm.bytes = in ? rows * (2.0 * tbytes + 8.0 * ((cw + 63) / 64)) + in * tbytes : 0.0;
+        }
+        collect_stats();
+    }
+    return F2_OK;
+}
+
+bool window_ok(const f2_matrix* a, const f2_window& w) {
+    return w.r0 <= w.r1 && w.c0 <= w.c1 && w.r1 <= a->m && w.c1 <= a->n;
+}
+
+bool full_window(const f2_matrix* a, const f2_window& w) {
+    return w.r0 == 0 && w.c0 == 0 && w.r1 == a->m && w.c1 == a->n;
+}
+
+// Run the engine on a window: in place for the whole matrix, otherwise on an
+// aligned copy that is written back bit-exactly inside the window bounds.
+int pls_on_window(f2_matrix* a, const f2_window& w, unsigned W, EngineOut& out) {
+    if (full_window(a, w)) return run_engine(mat_of(a), W, out);
+    f2_matrix* tmp = nullptr;
+    int rc = alloc_matrix(w.r1 - w.r0, w.c1 - w.c0, &tmp);
+    if (rc) return rc;
+    Mat t = mat_of(tmp);
+    launch_extract(g.stream, mat_of(a), static_cast<int64_t>(w.r0), static_cast<int64_t>(w.c0), t);
+    rc = run_engine(t, W, out);
+    if (!rc) {
+        launch_insert(g.stream, mat_of(a), static_cast<int64_t>(w.r0), static_cast<int64_t>(w.c0), t);
+        cudaError_t e = cudaStreamSynchronize(g.stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "window insert");
+    }
+    cudaFree(tmp->d);
+    delete tmp;
+    return rc;
+}
+
+void fill_pq(const EngineOut& o, uint64_t* p, size_t m, uint64_t* q, size_t n, bool recursive, uint64_t cutoff) {
+    for (size_t i = 0; i < m; ++i) p[i] = i;
+    for (int64_t t = 0; t < o.rank; ++t) p[t] = static_cast<uint64_t>(o.P[t]);
+    if (recursive) {
+        replay_q(m, n, cutoff, o.Qp.data(), static_cast<size_t>(o.rank), q);
+    } else {
+        for (size_t j = 0; j < n; ++j) q[j] = j;
+        for (int64_t t = 0; t < o.rank; ++t) q[t] = static_cast<uint64_t>(o.Qp[t]);
+    }
+}
+
+uint64_t default_cutoff() {
+    const uint64_t four_mib = uint64_t{4} << 20;
+    uint64_t l2 = 0;
+    if (const char* env = std::getenv("F2_L2_BYTES")) {
+        char* end = nullptr;
+        unsigned long long v = std::strtoull(env, &end, 10);
+        if (end && *end == '\0' && v > 0) l2 = v;
+    }
+#if defined(_SC_LEVEL2_CACHE_SIZE)
+    if (l2 == 0) {
+        long v = sysconf(_SC_LEVEL2_CACHE_SIZE);
+        if (v > 0) l2 = static_cast<uint64_t>(v);
+    }
+#endif
+    if (l2 == 0) return four_mib;
+    return std::min(l2, four_mib);
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+const char* f2_last_error(void) { return g_err.c_str(); }
+
+int f2_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int f2_set_device(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g.init && device != g.device) return fail(F2_INVALID_ARGUMENT, "device already initialised");
+    g.device = device;
+    return ensure_init();
+}
+
+int f2_matrix_create(size_t nrows, size_t ncols, f2_matrix** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!out) return fail(F2_INVALID_ARGUMENT, "out is NULL");
+    int rc = ensure_init();
+    if (rc) return rc;
+    rc = alloc_matrix(nrows, ncols, out);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+void f2_matrix_destroy(f2_matrix* a) {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (a->d) cudaFree(a->d);
+    delete a;
+}
+
+size_t f2_matrix_nrows(const f2_matrix* a) { return a ? a->m : 0; }
+size_t f2_matrix_ncols(const f2_matrix* a) { return a ? a->n : 0; }
+size_t f2_matrix_stride(const f2_matrix* a) { return a ? a->stride : 0; }
+uint64_t* f2_matrix_device_ptr(f2_matrix* a) { return a ? a->d : nullptr; }
+
+int f2_matrix_upload(f2_matrix* a, const uint64_t* host, size_t host_stride_words) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!host && a->m)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const size_t nw = (a->n + 63) / 64;
+    if (host_stride_words < nw) return fail(F2_INVALID_ARGUMENT, "host stride shorter than a row");
+    if (a->m == 0 || nw == 0) return F2_OK;
+    CK(cudaMemcpy2DAsync(a->d, a->stride * 8, host, host_stride_words * 8, nw * 8, a->m, cudaMemcpyHostToDevice,
+                         g.stream));
+    // padding bits of the last word must be zero (bitmat.hpp:3-6)
+    if (a->n % 64) {
+        // cheap: extract onto itself masks the tail word
+        Mat t = mat_of(a);
+        launch_extract(g.stream, t, 0, 0, t);
+    }
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_matrix_download(const f2_matrix* a, uint64_t* host, size_t host_stride_words) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!host && a->m)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const size_t nw = (a->n + 63) / 64;
+    if (host_stride_words < nw) return fail(F2_INVALID_ARGUMENT, "host stride shorter than a row");
+    if (a->m == 0 || nw == 0) return F2_OK;
+    CK(cudaMemcpy2DAsync(host, host_stride_words * 8, a->d, a->stride * 8, nw * 8, a->m, cudaMemcpyDeviceToHost,
+                         g.stream));
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_matrix_copy(f2_matrix* dst, const f2_matrix* src) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!dst || !src) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (dst->m != src->m || dst->n != src->n) return fail(F2_INVALID_ARGUMENT, "shape mismatch");
+    if (src->m) CK(cudaMemcpyAsync(dst->d, src->d, src->m * src->stride * 8, cudaMemcpyDeviceToDevice, g.stream));
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_matrix_clear(f2_matrix* a) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (a->m) CK(cudaMemsetAsync(a->d, 0, a->m * a->stride * 8, g.stream));
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_matrix_randomize(f2_matrix* a, double density, uint64_t seed) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!(density >= 0.0 && density <= 1.0))
+        return fail(F2_INVALID_ARGUMENT, "randomize: density must be in [0, 1]");
+    const uint64_t thr = static_cast<uint64_t>(std::llround(density * 9007199254740992.0));
+    LaunchTimer t(3, 0, 0);
+    launch_randomize(g.stream, mat_of(a), thr, seed);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_matrix_digest(const f2_matrix* a, uint64_t* out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || !out) return fail(F2_INVALID_ARGUMENT, "null argument");
+    launch_digest(g.stream, mat_of(a), g.d_digest);
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, g.d_digest, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
+    CK(cudaStreamSynchronize(g.stream));
+    *out = h;
+    return F2_OK;
+}
+
+void* f2_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void f2_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+uint64_t f2_default_cutoff_bytes(void) { return default_cutoff(); }
+
+unsigned f2_auto_table_bits(size_t dim) {
+    if (dim < 2) return 1;
+    unsigned lg = 0;
+    while ((dim >> (lg + 1)) != 0) ++lg;
+    if (lg <= 3) return 1;
+    return lg - 2 > 8 ? 8 : lg - 2;
+}
+
+int f2_set_panel_bits(unsigned bits) {
+    if (bits == 0) bits = 1024;
+    if (bits % 64 || bits > static_cast<unsigned>(kMaxPanelBits))
+        return fail(F2_INVALID_ARGUMENT, "panel bits must be a multiple of 64 and <= 2048");
+    g.panel_bits = bits;
+    return F2_OK;
+}
+
+// mmpf_pls (mmpf.cpp:81-121): size check :85-86 before touching P/Q; P/Q
+// identity-filled :87-88; empty -> 0 :89; k > 8 rejected after the fill :90.
+int f2_mmpf_pls(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen, unsigned k,
+                uint64_t* rank) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || !rank || (!p && plen) || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
+    if (plen != m || qlen != n) return fail(F2_INVALID_ARGUMENT, "mmpf_pls: permutation size mismatch");
+    for (size_t i = 0; i < m; ++i) p[i] = i;
+    for (size_t j = 0; j < n; ++j) q[j] = j;
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        return F2_OK;
+    }
+    if (k > 8) return fail(F2_INVALID_ARGUMENT, "mmpf_pls: k must be in 0..8");
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    EngineOut o;
+    rc = pls_on_window(a, w, 64, o);
+    if (rc) return rc;
+    fill_pq(o, p, m, q, n, false, 0);
+    *rank = static_cast<uint64_t>(o.rank);
+    return F2_OK;
+}
+
+// pls_recursive (pls.cpp:105-113): validate(cfg) :57-61, size check :110-111.
+int f2_pls_recursive(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen,
+                     const f2_elim_config* cfg, uint64_t* rank) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    f2_elim_config c0{0, 0, 0.15, F2_ALG_PLS};
+    const f2_elim_config& cfg_ = cfg ? *cfg : c0;
+    if (!a || !rank || (!p && plen) || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const uint64_t cutoff = cfg_.cutoff_bytes ? cfg_.cutoff_bytes : default_cutoff();
+    if (cutoff == 0) return fail(F2_INVALID_ARGUMENT, "cutoff_bytes must be positive");
+    if (!(cfg_.hybrid_threshold >= 0.0 && cfg_.hybrid_threshold <= 1.0))
+        return fail(F2_INVALID_ARGUMENT, "hybrid_threshold must be in [0, 1]");
+    if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
+    if (plen != m || qlen != n) return fail(F2_INVALID_ARGUMENT, "pls_recursive: permutation size mismatch");
+    for (size_t i = 0; i < m; ++i) p[i] = i;
+    for (size_t j = 0; j < n; ++j) q[j] = j;
+    if (m == 0 || n == 0) {
+        *rank = 0;
+        return F2_OK;
+    }
+    // the reference's first leaf is mmpf_pls(.., cfg.k), which rejects k > 8
+    if (cfg_.k > 8) return fail(F2_INVALID_ARGUMENT, "mmpf_pls: k must be in 0..8");
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    EngineOut o;
+    rc = pls_on_window(a, w, g.panel_bits, o);
+    if (rc) return rc;
+    fill_pq(o, p, m, q, n, true, cutoff);
+    *rank = static_cast<uint64_t>(o.rank);
+    return F2_OK;
+}
+
+static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
+                    uint64_t* q, const f2_elim_config* cfg, unsigned k, uint64_t* rank) {
+    f2_matrix* a = nullptr;
+    int rc = f2_matrix_create(nrows, ncols, &a);
+    if (rc) return rc;
+    rc = f2_matrix_upload(a, words, stride_words);
+    if (!rc) {
+        f2_window w{0, 0, nrows, ncols};
+        rc = recursive ? f2_pls_recursive(a, w, p, nrows, q, ncols, cfg, rank)
+                       : f2_mmpf_pls(a, w, p, nrows, q, ncols, k, rank);
+    }
+    if (!rc) rc = f2_matrix_download(a, words, stride_words);
+    f2_matrix_destroy(a);
+    return rc;
+}
+
+int f2_mmpf_pls_host(uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p, uint64_t* q,
+                     unsigned k, uint64_t* rank) {
+    return pls_host(false, words, nrows, ncols, stride_words, p, q, nullptr, k, rank);
+}
+
+int f2_pls_recursive_host(uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
+                          uint64_t* q, const f2_elim_config* cfg, uint64_t* rank) {
+    return pls_host(true, words, nrows, ncols, stride_words, p, q, cfg, 0, rank);
+}
+
+int f2_stats_enable(int enable) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g.stats = enable != 0;
+    return F2_OK;
+}
+
+int f2_stats_get(int kind, uint64_t* launches, double* ms, double* bytes, double* bitops) {
+    if (kind < 0 || kind > 3) return fail(F2_INVALID_ARGUMENT, "kind out of range");
+    const auto& f = g.fam[kind];
+    if (launches) *launches = f.n;
+    if (ms) *ms = f.ms;
+    if (bytes) *bytes = f.bytes;
+    if (bitops) *bitops = f.bitops;
+    return F2_OK;
+}
+
+int f2_stats_reset(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& f : g.fam) f = Ctx::Family{};
+    return F2_OK;
+}
+
+uint64_t f2_last_launch_count(void) { return g.launches; }
+
+}  // extern "C"
+
+// ---- multiply / triangular solve / permutations ------------------------------
+namespace {
+
+bool overlaps(const f2_matrix* x, const f2_window& a, const f2_matrix* y, const f2_window& b) {
+    if (x != y) return false;
+    const bool rows = a.r0 < b.r1 && b.r0 < a.r1;
+    const bool cols = a.c0 < b.c1 && b.c0 < a.c1;
+    return rows && cols && a.r0 < a.r1 && b.r0 < b.r1 && a.c0 < a.c1 && b.c0 < b.c1;
+}
+
+struct TmpMat {
+    f2_matrix* m = nullptr;
+    ~TmpMat() {
+        if (m) {
+            cudaFree(m->d);
+            delete m;
+        }
+    }
+};
+
+int extract_tmp(const f2_matrix* a, const f2_window& w, TmpMat& t) {
+    int rc = alloc_matrix(w.r1 - w.r0, w.c1 - w.c0, &t.m);
+    if (rc) return rc;
+    launch_extract(g.stream, mat_of(a), static_cast<int64_t>(w.r0), static_cast<int64_t>(w.c0), mat_of(t.m));
+    return F2_OK;
+}
+
+// C(p x q) ^= A(p x s) * B(s x q); A and B aligned at (0,0), C at (cr0, word cw0)
+void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0, int64_t aw0, int64_t s,
+               const Mat& B, int64_t br0, int64_t bw0, int64_t p, int64_t q) {
+    TableApply ta{};
+    ta.C = C;
+    ta.c_r0 = cr0;
+    ta.c_r1 = cr0 + p;
+    ta.cw0 = cw0;
+    ta.cw1 = cw0 + (q + 63) / 64;
+    ta.A = A;
+    ta.a_r0 = ar0;
+    ta.aw0 = aw0;
+    ta.kw = static_cast<int>((s + 63) / 64);
+    ta.kbits = s;
+    ta.B = B;
+    ta.b_r0 = br0;
+    ta.bw0 = bw0;
+    ta.brow = nullptr;
+    ta.row_mode = ROWS_STATIC;
+    ta.st = nullptr;
+    LaunchTimer t(0, 0.0, 2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
+    launch_table_apply(g.stream, ta, g.nsm);
+}
+
+// B <- L^{-1} B for L = Lm rows/cols [o, o+r) (o % 64 == 0) and B = Bm rows [o, o+r)
+void trsm_rec(const Mat& Lm, const Mat& Bm, int64_t o, int64_t r) {
+    if (r <= 1) return;
+    const int64_t nwb = (Bm.n + 63) / 64;
+    if (r <= kMaxPanelBits) {
+        Mat lsub{Lm.w + o * Lm.stride + o / 64, r, r, Lm.stride};
+        LaunchTimer t(2, 0, 0);
+        launch_pivot_trsm(g.stream, Bm, 0, static_cast<int>((r + 63) / 64), 0, nwb, nullptr, PivotSet{2, o, r}, &lsub);
+        return;
+    }
+    int64_t h = (r / 2 + 63) / 64 * 64;
+    if (h >= r) h = r / 2;
+    trsm_rec(Lm, Bm, o, h);
+    // B1 ^= L10 * B0
+    table_mul(Bm, o + h, 0, Lm, o + h, o / 64, h, Bm, o, 0, r - h, Bm.n);
+    trsm_rec(Lm, Bm, o + h, r - h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix* b, f2_window wb, unsigned k) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    (void)k;  // table width is an implementation choice; the product is exact for any k
+    if (!a || !b || !c) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(a, wa) || !window_ok(b, wb) || !window_ok(c, wc))
+        return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t p = wa.r1 - wa.r0, s = wa.c1 - wa.c0, q = wb.c1 - wb.c0;
+    if (p != wc.r1 - wc.r0 || s != wb.r1 - wb.r0 || q != wc.c1 - wc.c0)
+        return fail(F2_INVALID_ARGUMENT, "addmul: dimension mismatch");
+    if (overlaps(c, wc, a, wa) || overlaps(c, wc, b, wb)) return fail(F2_INVALID_ARGUMENT, "addmul: C aliases an input");
+    if (p == 0 || s == 0 || q == 0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    TmpMat at, bt;
+    if ((rc = extract_tmp(a, wa, at)) || (rc = extract_tmp(b, wb, bt))) return rc;
+    if (wc.c0 % 64 == 0) {
+        table_mul(mat_of(c), static_cast<int64_t>(wc.r0), static_cast<int64_t>(wc.c0 / 64), mat_of(at.m), 0, 0,
+                  static_cast<int64_t>(s), mat_of(bt.m), 0, 0, static_cast<int64_t>(p), static_cast<int64_t>(q));
+    } else {
+        TmpMat ct;
+        if ((rc = extract_tmp(c, wc, ct))) return rc;
+        table_mul(mat_of(ct.m), 0, 0, mat_of(at.m), 0, 0, static_cast<int64_t>(s), mat_of(bt.m), 0, 0,
+                  static_cast<int64_t>(p), static_cast<int64_t>(q));
+        launch_insert(g.stream, mat_of(c), static_cast<int64_t>(wc.r0), static_cast<int64_t>(wc.c0), mat_of(ct.m));
+        CK(cudaStreamSynchronize(g.stream));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    if (g.stats) collect_stats();
+    return F2_OK;
+}
+
+int f2_mul_m4rm(const f2_matrix* a, const f2_matrix* b, unsigned k, f2_matrix** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || !b || !out) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (a->n != b->m) return fail(F2_INVALID_ARGUMENT, "mul_m4rm: dimension mismatch");
+    if (k > 8) return fail(F2_INVALID_ARGUMENT, "mul_m4rm: k must be in 0..8");
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    if ((rc = alloc_matrix(a->m, b->n, out))) return rc;
+    if (a->m && b->n && a->n)
+        table_mul(mat_of(*out), 0, 0, mat_of(a), 0, 0, static_cast<int64_t>(a->n), mat_of(b), 0, 0,
+                  static_cast<int64_t>(a->m), static_cast<int64_t>(b->n));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    if (g.stats) collect_stats();
+    return F2_OK;
+}
+
+int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window wb) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!l || !b) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(l, wl) || !window_ok(b, wb)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t r = wl.r1 - wl.r0;
+    if (r != wl.c1 - wl.c0) return fail(F2_INVALID_ARGUMENT, "trsm: L must be square");
+    if (r != wb.r1 - wb.r0) return fail(F2_INVALID_ARGUMENT, "trsm: dimension mismatch");
+    if (r <= 1 || wb.c1 == wb.c0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    TmpMat lt, bt;
+    if ((rc = extract_tmp(l, wl, lt)) || (rc = extract_tmp(b, wb, bt))) return rc;
+    trsm_rec(mat_of(lt.m), mat_of(bt.m), 0, static_cast<int64_t>(r));
+    launch_insert(g.stream, mat_of(b), static_cast<int64_t>(wb.r0), static_cast<int64_t>(wb.c0), mat_of(bt.m));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    if (g.stats) collect_stats();
+    return F2_OK;
+}
+
+int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t qlen) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (rank > a->m || rank > qlen) return fail(F2_INVALID_ARGUMENT, "compress_columns: rank out of range");
+    for (uint64_t j = 0; j < rank; ++j)
+        if (q[j] >= a->n || j >= a->n) return fail(F2_INVALID_ARGUMENT, "compress_columns: column out of range");
+    if (rank == 0) return F2_OK;
+    if (a->stride * 8 > 200 * 1024) return fail(F2_INVALID_ARGUMENT, "compress_columns: row wider than 1.6M bits");
+    int rc = ensure_init();
+    if (rc) return rc;
+    int64_t* dq = nullptr;
+    CK(cudaMalloc(&dq, sizeof(int64_t) * rank));
+    std::vector<int64_t> hq(q, q + rank);
+    CK(cudaMemcpyAsync(dq, hq.data(), sizeof(int64_t) * rank, cudaMemcpyHostToDevice, g.stream));
+    launch_col_swaps(g.stream, mat_of(a), static_cast<int64_t>(rank), dq, g.nsm);
+    cudaError_t e = cudaStreamSynchronize(g.stream);
+    cudaFree(dq);
+    if (e != cudaSuccess) return cuda_fail(e, "compress_columns");
+    return F2_OK;
+}
+
+int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int inverse) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!p && plen)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t m = w.r1 - w.r0;
+    if (plen > m) return fail(F2_INVALID_ARGUMENT, "apply_rows: permutation longer than rows");
+    for (size_t i = 0; i < plen; ++i)
+        if (p[i] >= m) return fail(F2_INVALID_ARGUMENT, "apply_rows: entry out of range");
+    if (m == 0 || w.c1 == w.c0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    std::vector<int64_t> idx(m);
+    for (size_t i = 0; i < m; ++i) idx[i] = static_cast<int64_t>(i);
+    if (!inverse) {
+        for (size_t i = 0; i < plen; ++i) std::swap(idx[i], idx[p[i]]);
+    } else {
+        for (size_t i = plen; i-- > 0;) std::swap(idx[i], idx[p[i]]);
+    }
+    TmpMat t1, t2;
+    if ((rc = extract_tmp(a, w, t1))) return rc;
+    if ((rc = alloc_matrix(m, w.c1 - w.c0, &t2.m))) return rc;
+    int64_t* dmap = nullptr;
+    CK(cudaMalloc(&dmap, sizeof(int64_t) * m));
+    CK(cudaMemcpyAsync(dmap, idx.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, g.stream));
+    launch_gather_rows(g.stream, mat_of(t2.m), mat_of(t1.m), dmap, static_cast<int64_t>(m),
+                       static_cast<int64_t>(t1.m->stride));
+    launch_insert(g.stream, mat_of(a), static_cast<int64_t>(w.r0), static_cast<int64_t>(w.c0), mat_of(t2.m));
+    cudaError_t e = cudaStreamSynchronize(g.stream);
+    cudaFree(dmap);
+    if (e != cudaSuccess) return cuda_fail(e, "apply_rows");
+    return F2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// Shared device-side definitions of the B200 GF(2) PLS engine.
+//
+// Layout in HBM: a matrix is row-major, 64-bit words, bit j of a row in word
+// j/64 at bit j%64 (the reference packing, proj/include/f2lin/bitmat.hpp:3-6),
+// with the row stride padded to a multiple of 16 words (128 B) so every row
+// starts on a 128-byte line.  Padding bits and padding words are zero and every
+// kernel keeps them zero.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace f2g {
+
+constexpr int kMaxPanelBits = 2048;          // widest outer panel W
+constexpr int kWinSlots = 4;                 // leaf search window: 32 lanes x 4 slots
+constexpr int kWin = 32 * kWinSlots;         // 128 candidate positions in registers
+constexpr int kMaxSwaps = kWin + 64;         // window slots + outside positions
+constexpr int kOmapSlots = 128;              // open-addressing map for outside swaps
+
+struct Mat {
+    uint64_t* w;
+    int64_t m, n, stride;  // rows, columns (bits), row stride (words)
+};
+
+// Device-resident elimination state.  Every kernel of the engine reads its
+// row offsets and pivot counts from here, so the host enqueues a fixed,
+// data-independent launch sequence and never synchronises mid-factorisation.
+struct PlsState {
+    int64_t r;         // next pivot position (= pivots found so far)
+    int64_t leaf_r;    // r at the start of the current leaf
+    int64_t leaf_kb;   // pivots found by the current leaf
+    int64_t panel_r;   // r at the start of the current panel
+    int64_t panel_kb;  // pivots found so far in the current panel
+    int32_t nswap;     // row moves produced by the current leaf
+    int32_t pad0;
+    uint64_t leaf_mask;                 // pivot columns within the leaf word
+    uint64_t ustrict[64];               // leaf pivot words, bits <= pivot cleared
+    int32_t q[64];                      // leaf pivot bit positions (0..63)
+    int64_t swap_dst[kMaxSwaps];        // position that receives ...
+    int64_t swap_src[kMaxSwaps];        // ... the pre-leaf content of this physical row
+    int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
+    int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
+};
+
+// How a table-apply launch finds its C/A rows (device-side offsets).
+enum RowMode : int { ROWS_STATIC = 0, ROWS_AFTER_LEAF = 1, ROWS_AFTER_PANEL = 2 };
+
+}  // namespace f2g

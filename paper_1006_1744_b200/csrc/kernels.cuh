@@ -1,0 +1,57 @@
+// Host-side launchers of the engine's kernels (one per .cu translation unit).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "f2gpu.cuh"
+
+namespace f2g {
+
+// leaf.cu
+void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
+                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp);
+void launch_row_moves(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st);
+void launch_leaf_finalize(cudaStream_t s, const Mat& A, int64_t wl, const PlsState* st, int nsm);
+void setup_leaf_kernels();
+
+// trsm.cu — forward substitution of pivot rows by 8-column groups with
+// Gray tables (the M4RI-style TRSM of mul.cpp:109-131, blocked for SMEM).
+struct PivotSet {
+    int mode;              // 0: leaf (st->q, leaf_r, leaf_kb); 1: panel (st->panel_q, panel_r, panel_kb);
+                           // 2: static identity pivots (q_t = t, r0, kb given)
+    int64_t r0, kb;        // used by mode 2
+};
+void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_words, int64_t tw0,
+                       int64_t tw1, const PlsState* st, PivotSet ps, const Mat* L);
+void setup_trsm_kernels();
+
+// m4rm.cu — C ^= A * B by 8-bit Gray tables in SMEM (M4RM, mul.cpp:21-68),
+// also the MMPF table-apply (m4ri.cpp:28-38) when K = one 64-bit word.
+struct TableApply {
+    Mat C;                 // rows [c_r0, c_r1), words [cw0, cw1)
+    int64_t c_r0, c_r1, cw0, cw1;
+    Mat A;                 // coefficient rows: A row = a_r0 + (i - c_r0), words [aw0, aw0+kw)
+    int64_t a_r0, aw0;
+    int kw;                // coefficient words (K = 64*kw bits, padded with zero bits)
+    int64_t kbits;         // valid K bits
+    Mat B;                 // B row for raw bit j: brow ? brow[j] : b_r0 + j; B word = bw0 + (cw - cw0)
+    int64_t b_r0, bw0;
+    const int64_t* brow;
+    int row_mode;          // RowMode: static / after leaf / after panel (c_r0 = a_r0 from state)
+    const PlsState* st;
+};
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm);
+void setup_m4rm_kernels();
+
+// misc.cu
+void launch_randomize(cudaStream_t s, const Mat& A, uint64_t threshold, uint64_t seed);
+void launch_digest(cudaStream_t s, const Mat& A, unsigned long long* out);
+void launch_extract(cudaStream_t s, const Mat& src, int64_t r0, int64_t c0, const Mat& dst);
+void launch_insert(cudaStream_t s, const Mat& dst, int64_t r0, int64_t c0, const Mat& src);
+void launch_compress(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp, int nsm);
+void launch_gather_rows(cudaStream_t s, const Mat& dst, const Mat& src, const int64_t* rowmap, int64_t nrows,
+                        int64_t nwords);
+void launch_col_swaps(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* q, int nsm);
+void setup_misc_kernels();
+
+}  // namespace f2g

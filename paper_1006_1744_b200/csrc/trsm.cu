@@ -1,0 +1,139 @@
+// Pivot-row triangular solve over GF(2).
+//
+// X_t = B_t xor sum_{l<t} L[t][l] X_l for the kb pivot rows of a leaf/panel
+// (or an explicit unit-lower L), i.e. B <- L^{-1} B as trsm_lower_left_unit
+// does (proj/src/mul.cpp:109-131; the diagonal is implicit and everything on
+// or above it ignored).  L is read in "raw" form: row t's coefficient for
+// pivot l sits at the pivot's raw column q_l of its coefficient words, which
+// is how the packed layout stores L before compress_columns (gauss.cpp:47-53).
+//
+// Blocking: each CTA owns TW target words of all kb rows in SMEM and walks the
+// raw columns 8 at a time.  For each group it solves the (<= 8) pivots inside
+// the group, builds the 256-entry Gray table of their combinations, and adds
+// one table row into every later pivot row (one lookup per row per group).
+#include <cstdint>
+
+#include "f2gpu.cuh"
+#include "kernels.cuh"
+
+namespace f2g {
+
+namespace {
+
+constexpr int kTW = 4;           // target words per CTA
+constexpr int kMaxRows = kMaxPanelBits;
+
+struct TrsmCtx {
+    int64_t kb, r0;
+    const int32_t* q;  // nullptr => identity pivots
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(256)
+k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, const PlsState* st,
+             PivotSet ps, Mat L) {
+    extern __shared__ uint64_t smem[];
+    uint64_t* X = smem;                          // [kMaxRows][kTW]
+    uint64_t* T = X + kMaxRows * kTW;            // [256][kTW]
+    int32_t* sq = reinterpret_cast<int32_t*>(T + 256 * kTW);  // [kMaxRows]
+    int32_t* gstart = sq + kMaxRows;             // [kMaxPanelBits/8 + 1]
+
+    int64_t kb, r0;
+    const int32_t* qsrc = nullptr;
+    if (ps.mode == 0) {
+        kb = st->leaf_kb;
+        r0 = st->leaf_r;
+        qsrc = st->q;
+    } else if (ps.mode == 1) {
+        kb = st->panel_kb;
+        r0 = st->panel_r;
+        qsrc = st->panel_q;
+    } else {
+        kb = ps.kb;
+        r0 = ps.r0;
+    }
+    if (kb <= 1) return;
+    const int64_t tb = tw0 + static_cast<int64_t>(blockIdx.x) * kTW;
+    if (tb >= tw1) return;
+    const int ntw = static_cast<int>(tw1 - tb < kTW ? tw1 - tb : kTW);
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int nk = static_cast<int>(kb);
+
+    for (int t = tid; t < nk; t += nth) sq[t] = qsrc ? qsrc[t] : t;
+    for (int i = tid; i < nk * kTW; i += nth) {
+        int t = i / kTW, j = i % kTW;
+        X[i] = j < ntw ? A.w[(r0 + t) * A.stride + tb + j] : 0ull;
+    }
+    __syncthreads();
+    const int ngroups = coef_words * 8;
+    for (int g = tid; g <= ngroups; g += nth) {
+        int lo = 0, hi = nk;  // first t with sq[t] >= 8g
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (sq[mid] < 8 * g) lo = mid + 1;
+            else hi = mid;
+        }
+        gstart[g] = lo;
+    }
+    __syncthreads();
+
+    auto coef_byte = [&](int t, int g) -> unsigned {
+        const uint64_t w = ps.mode == 2 ? L.w[static_cast<int64_t>(t) * L.stride + (g >> 3)]
+                                        : A.w[(r0 + t) * A.stride + coef_w0 + (g >> 3)];
+        return static_cast<unsigned>((w >> (8 * (g & 7))) & 0xffu);
+    };
+
+    for (int g = 0; g < ngroups; ++g) {
+        const int t0 = gstart[g], t1 = gstart[g + 1];
+        if (t0 == t1) continue;
+        if (t1 - t0 > 1 && tid < kTW) {
+            const int j = tid;
+            for (int t = t0 + 1; t < t1; ++t) {
+                unsigned cb = coef_byte(t, g) & ((1u << (sq[t] - 8 * g)) - 1u);
+                uint64_t v = X[t * kTW + j];
+                for (int l = t0; l < t; ++l)
+                    if ((cb >> (sq[l] - 8 * g)) & 1u) v ^= X[l * kTW + j];
+                X[t * kTW + j] = v;
+            }
+        }
+        if (t1 >= nk) break;
+        __syncthreads();
+        for (int i = tid; i < 256 * kTW; i += nth) {
+            const int e = i / kTW, j = i % kTW;
+            uint64_t v = 0;
+            for (int l = t0; l < t1; ++l)
+                if ((e >> (sq[l] - 8 * g)) & 1) v ^= X[l * kTW + j];
+            T[i] = v;
+        }
+        __syncthreads();
+        for (int i = tid; i < (nk - t1) * kTW; i += nth) {
+            const int t = t1 + i / kTW, j = i % kTW;
+            X[t * kTW + j] ^= T[coef_byte(t, g) * kTW + j];
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int i = tid; i < nk * kTW; i += nth) {
+        int t = i / kTW, j = i % kTW;
+        if (j < ntw) A.w[(r0 + t) * A.stride + tb + j] = X[i];
+    }
+}
+
+static size_t trsm_smem() {
+    return sizeof(uint64_t) * (kMaxRows * kTW + 256 * kTW) + sizeof(int32_t) * (kMaxRows + kMaxPanelBits / 8 + 8);
+}
+
+void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_words, int64_t tw0,
+                       int64_t tw1, const PlsState* st, PivotSet ps, const Mat* L) {
+    if (tw1 <= tw0) return;
+    const int grid = static_cast<int>((tw1 - tw0 + kTW - 1) / kTW);
+    Mat l = L ? *L : Mat{nullptr, 0, 0, 0};
+    k_pivot_trsm<<<grid, 256, trsm_smem(), s>>>(A, coef_w0, coef_words, tw0, tw1, st, ps, l);
+}
+
+void setup_trsm_kernels() {
+    cudaFuncSetAttribute(k_pivot_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trsm_smem()));
+}
+
+}  // namespace f2g

@@ -1,0 +1,56 @@
+"""GPU: the five BASELINE.json configurations at full size against digests of the
+reference's own outputs (tests/golden/configs.json, made by make_golden.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import digest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden", "configs.json")
+
+
+def golden():
+    if not os.path.exists(GOLD):
+        return {}
+    return json.load(open(GOLD))
+
+
+def make_input(f2, oracle, cfg):
+    if cfg["kind"] == "dense":
+        a = f2.DeviceMatrix(cfg["m"], cfg["n"])
+        a.randomize(0.5, cfg["seed"])
+        return a
+    if cfg["kind"] == "xy":
+        x = f2.DeviceMatrix(cfg["m"], cfg["inner"])
+        x.randomize(0.5, cfg["seed_x"])
+        y = f2.DeviceMatrix(cfg["inner"], cfg["n"])
+        y.randomize(0.5, cfg["seed_y"])
+        return f2.mul_m4rm(x, y)
+    if cfg["kind"] == "fixed_weight":
+        return f2.DeviceMatrix.from_host(oracle.fixed_weight(cfg["m"], cfg["n"], cfg["weight"], cfg["seed"]), cfg["n"])
+    raise ValueError(cfg["kind"])
+
+
+@pytest.mark.parametrize("name", ["c1_dense_4096", "c2_dense_16384", "c4_xy_32768", "c5_sparse_16384x131072",
+                                  "c3_dense_65536"])
+def test_config_against_reference_digests(f2, oracle, name):
+    g = golden().get(name)
+    if g is None:
+        pytest.skip(f"{name} not in golden/configs.json yet")
+    a0 = make_input(f2, oracle, g)
+    assert a0.digest() == int(g["input_digest"]), "input differs from the reference's generator"
+    for path in g["paths"]:
+        ref = g[path]
+        a = a0.clone()
+        if path == "mmpf":
+            res = f2.mmpf_pls(a)
+        else:
+            res = f2.pls_recursive(a, f2.EliminationConfig(cutoff_bytes=int(g["cutoff_bytes"])))
+        assert res.rank == ref["rank"], path
+        assert digest(res.P) == int(ref["p_digest"]), path
+        assert digest(res.Q) == int(ref["q_digest"]), path
+        assert a.digest() == int(ref["packed_digest"]), path
