@@ -13,12 +13,13 @@
 // is zero in every row the kernel touches and maps to no B row), so no compaction
 // pass exists and the L bits are never rewritten.
 //
-// CTA tile: 512 rows x 1024 bits of C, accumulated in registers over all of K.
-// Per 8-bit chunk of K the CTA builds a 256 x 1024-bit table in SMEM (double
-// buffered, 32 KB each) from 8 B rows staged by cp.async four chunks ahead, then
-// every row does one 16-byte LDS per thread (8 lanes cover one 128-byte table
-// row: conflict-free).  SMEM bandwidth bounds it: 512 lookups + 256 table rows per
-// chunk and CTA.
+// CTA tile: 1024 rows x 512 bits of C (16 warps), accumulated in registers over
+// all of K.  Per 8-bit chunk of K the CTA builds a 256 x 512-bit table in SMEM
+// (double buffered, 16 KB each) from 8 B rows staged by cp.async three chunks
+// ahead; every row then does one 16-byte LDS per thread (4 lanes cover one 64-byte
+// table row, 8 rows per warp instruction: conflict-free).  The coefficient words
+// of the tile's rows are staged in SMEM one K-word ahead.  SMEM bandwidth bounds
+// it: per chunk 1024 lookups x 64 B + 256 table rows x 64 B.
 #include <cstdint>
 
 #include "f2gpu.cuh"
@@ -28,11 +29,21 @@ namespace f2g {
 
 namespace {
 
-constexpr int kRPT = 16;                 // rows per thread
-constexpr int kThreads = 256;
-constexpr int kTM = (kThreads / 32) * 4 * kRPT;  // 512 rows per CTA
-constexpr int kTNW = 16;                 // 64-bit words per tile row (1024 bits)
-constexpr int kStages = 4;               // B-row ring depth
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRPT = 8;                          // rows per thread
+constexpr int kTNW = 8;                          // 64-bit words per tile row (512 bits)
+constexpr int kTM = kWarps * 8 * kRPT;           // 1024 rows per CTA (8 rows per warp instruction)
+constexpr int kStages = 4;                       // B-row ring depth
+constexpr int kMaxMap = kMaxPanelBits;           // K bits held in the SMEM row map
+
+// shared memory carve-up (bytes)
+constexpr size_t kOffT = 0;                                   // [2][256][kTNW] u64   32 KB
+constexpr size_t kOffRing = kOffT + 2 * 256 * kTNW * 8;        // [kStages][8][kTNW]    2 KB
+constexpr size_t kOffA = kOffRing + kStages * 8 * kTNW * 8;    // [2][kTM] u64          16 KB
+constexpr size_t kOffMap = kOffA + 2 * kTM * 8;                // [kMaxMap] i32         8 KB
+constexpr size_t kOffLive = kOffMap + kMaxMap * 4;             // [kMaxMap/8/32] u32
+constexpr size_t kSmem = kOffLive + (kMaxMap / 8 / 32) * 4;
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
     const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -43,17 +54,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__device__ __forceinline__ int64_t bmap(const TableApply& p, int64_t j) {
-    if (j >= p.kbits) return -1;
-    return p.brow ? p.brow[j] : p.b_r0 + j;
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
 }
+__device__ __forceinline__ void sts128(void* p, uint4 v) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
 
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
-    extern __shared__ __align__(16) uint4 sm4[];
-    uint4* Tbuf = sm4;                                                   // [2][256][8]
-    uint64_t* ring = reinterpret_cast<uint64_t*>(sm4 + 2 * 256 * 8);   // [kStages][8][kTNW]
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* Tb = reinterpret_cast<uint64_t*>(smem + kOffT);
+    uint64_t* ring = reinterpret_cast<uint64_t*>(smem + kOffRing);
+    uint64_t* abuf = reinterpret_cast<uint64_t*>(smem + kOffA);
+    int32_t* bmap = reinterpret_cast<int32_t*>(smem + kOffMap);
+    uint32_t* livebits = reinterpret_cast<uint32_t*>(smem + kOffLive);
 
     int64_t c_r0 = p.c_r0, a_r0 = p.a_r0;
     if (p.row_mode == ROWS_AFTER_LEAF) {
@@ -66,110 +87,123 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     const int64_t row_base = c_r0 + static_cast<int64_t>(blockIdx.y) * kTM;
     if (row_base >= p.c_r1) return;
     const int64_t tile_w0 = p.cw0 + static_cast<int64_t>(blockIdx.x) * kTNW;
+    const int64_t arow_base = a_r0 + (row_base - c_r0);
+    const int64_t nrows = p.c_r1 - row_base < kTM ? p.c_r1 - row_base : kTM;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rg = lane >> 3, wp = lane & 7;
+    const int rq = lane >> 2, wp = lane & 3;
     const int64_t cwa = tile_w0 + 2 * wp, cwb = cwa + 1;
     const bool va = cwa < p.cw1, vb = cwb < p.cw1;
+    const int nch = static_cast<int>((p.kbits + 7) / 8);
+    const bool mapped = p.brow != nullptr;
 
-    uint64_t acc0[kRPT], acc1[kRPT];
-    uint64_t aw[kRPT], an[kRPT];
-    const int64_t nch = (p.kbits + 7) / 8;
-
-#pragma unroll
-    for (int i = 0; i < kRPT; ++i) {
-        const int64_t row = row_base + warp * 64 + rg + 4 * i;
-        const bool rv = row < p.c_r1;
-        const uint64_t* cr = p.C.w + row * p.C.stride;
-        acc0[i] = (rv && va) ? cr[cwa] : 0ull;
-        acc1[i] = (rv && vb) ? cr[cwb] : 0ull;
-        an[i] = rv ? p.A.w[(a_r0 + (row - c_r0)) * p.A.stride + p.aw0] : 0ull;
-        aw[i] = 0;
+    // B row map and live-chunk mask for the whole K range
+    if (mapped) {
+        for (int j = tid; j < nch * 8; j += kThreads) {
+            int64_t r = j < p.kbits ? p.brow[j] : -1;
+            bmap[j] = static_cast<int32_t>(r);
+        }
+        __syncthreads();
+        for (int w = tid; w < (nch + 31) / 32; w += kThreads) {
+            uint32_t bits = 0;
+            for (int b = 0; b < 32 && w * 32 + b < nch; ++b) {
+                const int c = w * 32 + b;
+                bool any = false;
+                for (int k = 0; k < 8; ++k) any |= bmap[c * 8 + k] >= 0;
+                bits |= static_cast<uint32_t>(any) << b;
+            }
+            livebits[w] = bits;
+        }
     }
 
-    // stage B rows of chunk c into ring slot c % kStages (threads 0..127, one word each)
-    auto issue = [&](int64_t c) {
+    auto brow_of = [&](int j) -> int64_t {
+        if (mapped) return bmap[j];
+        return j < p.kbits ? p.b_r0 + j : -1;
+    };
+    auto live = [&](int c) -> bool { return mapped ? ((livebits[c >> 5] >> (c & 31)) & 1u) : c < nch; };
+
+    // B rows of chunk c -> ring stage c % kStages (threads 0..63, one word each)
+    auto issue_b = [&](int c) {
         if (tid < 8 * kTNW) {
-            const int b = tid >> 4, k = tid & 15;
-            const int64_t br = bmap(p, c * 8 + b);
+            const int b = tid >> 3, k = tid & 7;
+            const int64_t br = brow_of(c * 8 + b);
             const int64_t wcol = tile_w0 + k;
             const bool ok = br >= 0 && wcol < p.cw1;
             const uint64_t* src = ok ? p.B.w + br * p.B.stride + (p.bw0 + (wcol - p.cw0)) : p.B.w;
             cp_async8(ring + ((c % kStages) * 8 + b) * kTNW + k, src, ok);
         }
     };
-    auto live = [&](int64_t c) {
-        bool any = false;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) any |= bmap(p, c * 8 + b) >= 0;
-        return any;
+    // coefficient word g of every row of the tile -> abuf[g & 1]
+    auto issue_a = [&](int g) {
+        for (int r = tid; r < kTM; r += kThreads) {
+            const bool ok = r < nrows;
+            const uint64_t* src = ok ? p.A.w + (arow_base + r) * p.A.stride + p.aw0 + g : p.A.w;
+            cp_async8(abuf + (g & 1) * kTM + r, src, ok);
+        }
     };
-    // 256-entry table of chunk c into buffer buf: entry e = xor of B rows b with bit b of e
-    auto build = [&](int buf, int64_t c) {
-        const uint64_t* rs = ring + (c % kStages) * 8 * kTNW;
-        const int el = tid >> 3;  // low 5 bits of the entry
-        uint64_t v0[8], v1[8];
+    // 256-entry table of chunk c: entry e = xor of B rows b with bit b of e (LSB first)
+    auto build = [&](int c) {
+        const uint64_t* rs = ring + (c % kStages) * 8 * kTNW + 2 * wp;
+        uint4 v[8];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            v0[b] = rs[b * kTNW + 2 * wp];
-            v1[b] = rs[b * kTNW + 2 * wp + 1];
-        }
-        uint64_t l0 = 0, l1 = 0;
+        for (int b = 0; b < 8; ++b) v[b] = lds128(rs + b * kTNW);
+        const int el = tid >> 2;  // low 7 bits of the entry
+        uint4 lo = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int b = 0; b < 5; ++b)
-            if ((el >> b) & 1) {
-                l0 ^= v0[b];
-                l1 ^= v1[b];
-            }
-        uint64_t h0 = 0, h1 = 0;
-        uint4* tb = Tbuf + buf * 256 * 8;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k) {
-                const int b = 5 + ((k & 1) ? 0 : ((k & 2) ? 1 : 2));  // 5 + ctz(k), folded
-                h0 ^= v0[b];
-                h1 ^= v1[b];
-            }
-            const int eh = k ^ (k >> 1);
-            const uint64_t x0 = l0 ^ h0, x1 = l1 ^ h1;
-            tb[(eh * 32 + el) * 8 + wp] = make_uint4(static_cast<unsigned>(x0), static_cast<unsigned>(x0 >> 32),
-                                                     static_cast<unsigned>(x1), static_cast<unsigned>(x1 >> 32));
-        }
+        for (int b = 0; b < 7; ++b)
+            if ((el >> b) & 1) lo = xor4(lo, v[b]);
+        uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
+        sts128(tb + el * kTNW, lo);
+        sts128(tb + (el + 128) * kTNW, xor4(lo, v[7]));
     };
 
-    for (int64_t c = 0; c < 3; ++c) {
-        if (c < nch) issue(c);
+    uint64_t acc0[kRPT], acc1[kRPT];
+#pragma unroll
+    for (int i = 0; i < kRPT; ++i) {
+        const int64_t row = row_base + warp * 64 + rq + 8 * i;
+        const bool rv = row < p.c_r1;
+        const uint64_t* cr = p.C.w + row * p.C.stride;
+        acc0[i] = (rv && va) ? cr[cwa] : 0ull;
+        acc1[i] = (rv && vb) ? cr[cwb] : 0ull;
+    }
+
+    issue_a(0);
+    for (int c = 0; c < 3; ++c) {
+        if (c < nch) issue_b(c);
         cp_async_commit();
     }
     cp_async_wait<2>();
     __syncthreads();
-    if (nch > 0 && live(0)) build(0, 0);
+    if (nch > 0 && live(0)) build(0);
 
-    for (int64_t c = 0; c < nch; ++c) {
-        if (c + 3 < nch) issue(c + 3);
-        cp_async_commit();
-        if ((c & 7) == 0) {
-            const int64_t g1 = (c >> 3) + 1;
+    uint64_t aw[kRPT];
+    const int ngroups = (nch + 7) / 8;
+    for (int g = 0; g < ngroups; ++g) {
 #pragma unroll
-            for (int i = 0; i < kRPT; ++i) {
-                aw[i] = an[i];
-                const int64_t row = row_base + warp * 64 + rg + 4 * i;
-                if (g1 < p.kw && row < p.c_r1)
-                    an[i] = p.A.w[(a_r0 + (row - c_r0)) * p.A.stride + p.aw0 + g1];
-            }
-        }
-        cp_async_wait<2>();
-        __syncthreads();
-        if (c + 1 < nch && live(c + 1)) build(static_cast<int>((c + 1) & 1), c + 1);
-        if (live(c)) {
-            const uint4* tb = Tbuf + (c & 1) * 256 * 8 + wp;
-            const int sh = 8 * static_cast<int>(c & 7);
+        for (int j = 0; j < 8; ++j) {
+            const int c = g * 8 + j;
+            if (c < nch) {
+                if (c + 3 < nch) issue_b(c + 3);
+                if (j == 0 && g + 1 < p.kw && g + 1 < ngroups) issue_a(g + 1);
+                cp_async_commit();
+                cp_async_wait<2>();
+                __syncthreads();
+                if (j == 0) {
+                    const uint64_t* ab = abuf + (g & 1) * kTM + warp * 64 + rq;
 #pragma unroll
-            for (int i = 0; i < kRPT; ++i) {
-                const unsigned idx = static_cast<unsigned>(aw[i] >> sh) & 0xffu;
-                const uint4 v = tb[idx * 8];
-                acc0[i] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
-                acc1[i] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
+                    for (int i = 0; i < kRPT; ++i) aw[i] = ab[8 * i];
+                }
+                if (c + 1 < nch && live(c + 1)) build(c + 1);
+                if (live(c)) {
+                    const uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
+#pragma unroll
+                    for (int i = 0; i < kRPT; ++i) {
+                        const unsigned idx = static_cast<unsigned>(aw[i] >> (8 * j)) & 0xffu;
+                        const uint4 t = lds128(tb + idx * kTNW);
+                        acc0[i] ^= static_cast<uint64_t>(t.x) | (static_cast<uint64_t>(t.y) << 32);
+                        acc1[i] ^= static_cast<uint64_t>(t.z) | (static_cast<uint64_t>(t.w) << 32);
+                    }
+                }
             }
         }
     }
@@ -177,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
 
 #pragma unroll
     for (int i = 0; i < kRPT; ++i) {
-        const int64_t row = row_base + warp * 64 + rg + 4 * i;
+        const int64_t row = row_base + warp * 64 + rq + 8 * i;
         if (row < p.c_r1) {
             uint64_t* cr = p.C.w + row * p.C.stride;
             if (va) cr[cwa] = acc0[i];
@@ -186,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     }
 }
 
-static size_t table_apply_smem() { return sizeof(uint4) * 2 * 256 * 8 + sizeof(uint64_t) * kStages * 8 * kTNW; }
+static size_t table_apply_smem() { return kSmem; }
 
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm) {
     (void)nsm;
