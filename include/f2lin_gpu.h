@@ -131,6 +131,8 @@ int f2_stats_get(int kind, uint64_t* launches, double* ms, double* bytes, double
 int f2_stats_reset(void);
 /* kernel launches issued by the last compute call (all families) */
 uint64_t f2_last_launch_count(void);
+/* phase clocks of the last leaf (only builds compiled with -DF2_LEAF_PROFILE fill them) */
+int f2_debug_clocks(long long* out, int n);
 /* engine tuning (panel width in bits for pls_recursive; 0 = default) */
 int f2_set_panel_bits(unsigned bits);
 

@@ -3,12 +3,13 @@
 // The engine is a blocked right-looking PLS.  The matrix is walked in panels of
 // W columns (64 for the MMPF entry point, 1024 by default for the recursive
 // entry point); each panel is walked in 64-column leaves.  Per leaf:
-//   k_leaf_pivot     exact pivot search (gauss.cpp:33-44 rule)          1 CTA
-//   k_row_moves      the leaf's transpositions applied to whole rows     (perm.cpp:8-16)
-//   k_leaf_finalize  elimination of the leaf word -> L coefficients      (gauss.cpp:47-49)
-//   k_pivot_trsm     leaf pivot rows solved over the rest of the panel   (mul.cpp:109-131)
-//   k_table_apply    Gray-table update of the rest of the panel          (m4ri.cpp:28-38)
+//   k_leaf_pivot     exact pivot search (gauss.cpp:33-44 rule), 1 CTA; the row
+//                    transpositions only re-map the panel's virtual row order
+//   k_leaf_update    leaf word -> L coefficients (gauss.cpp:47-49), leaf pivot rows
+//                    solved over the rest of the panel (mul.cpp:109-131), Gray-table
+//                    update of the rest of the panel (m4ri.cpp:28-38)
 // Per panel:
+//   k_perm_save/put  the panel's transpositions applied to whole rows (perm.cpp:8-16)
 //   k_pivot_trsm     panel pivot rows solved over the trailing columns
 //   k_table_apply    Schur complement C ^= L21 * U12 (M4RM, mul.cpp:21-68)
 // and finally k_compress (compress_columns, perm.cpp:18-21) when Q != identity.
@@ -52,7 +53,9 @@ struct Ctx {
     PlsState* st = nullptr;
     int64_t* P = nullptr;
     int64_t* Qp = nullptr;
-    size_t cap_m = 0, cap_q = 0;
+    int64_t* pmap = nullptr;
+    uint64_t* scratch = nullptr;
+    size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
     size_t h_r_cap = 0;
     unsigned long long* d_digest = nullptr;
@@ -100,6 +103,7 @@ int ensure_init() {
     CK(cudaMalloc(&g.st, sizeof(PlsState)));
     CK(cudaMalloc(&g.d_digest, sizeof(unsigned long long)));
     setup_leaf_kernels();
+    setup_leafupd_kernels();
     setup_trsm_kernels();
     setup_m4rm_kernels();
     setup_misc_kernels();
@@ -108,11 +112,18 @@ int ensure_init() {
     return F2_OK;
 }
 
-int ensure_workspace(size_t m, size_t nq, size_t npanels) {
+int ensure_workspace(size_t m, size_t nq, size_t npanels, size_t scratch_words) {
     if (m > g.cap_m) {
         if (g.P) cudaFree(g.P);
+        if (g.pmap) cudaFree(g.pmap);
         CK(cudaMalloc(&g.P, sizeof(int64_t) * std::max<size_t>(m, 1)));
+        CK(cudaMalloc(&g.pmap, sizeof(int64_t) * std::max<size_t>(m, 1)));
         g.cap_m = m;
+    }
+    if (scratch_words > g.cap_scratch) {
+        if (g.scratch) cudaFree(g.scratch);
+        CK(cudaMalloc(&g.scratch, sizeof(uint64_t) * scratch_words));
+        g.cap_scratch = scratch_words;
     }
     if (nq > g.cap_q) {
         if (g.Qp) cudaFree(g.Qp);
@@ -239,10 +250,12 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     if (m == 0 || n == 0) return F2_OK;
     const int64_t nw = (n + 63) / 64;
     const int64_t npanels = (n + W - 1) / W;
-    int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels));
+    int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
+                              static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
     if (rc) return rc;
     cudaStream_t s = g.stream;
     CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), s));
+    launch_pmap_init(s, g.pmap, m);
     std::vector<cudaEvent_t> evs;
     evs.reserve(npanels);
     int64_t checked = 0;
@@ -258,38 +271,17 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
             {
                 LaunchTimer t(1, 0, 0);
-                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp);
+                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap);
             }
             {
                 LaunchTimer t(3, 0, 0);
-                launch_row_moves(s, A, nw, g.st);
+                launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
             }
-            {
-                LaunchTimer t(3, 0, 0);
-                launch_leaf_finalize(s, A, wl, g.st, g.nsm);
-            }
-            if (wl + 1 < pw1) {
-                {
-                    LaunchTimer t(2, 0, 0);
-                    launch_pivot_trsm(s, A, wl, 1, wl + 1, pw1, g.st, PivotSet{0, 0, 0}, nullptr);
-                }
-                TableApply ta{};
-                ta.C = A;
-                ta.c_r1 = m;
-                ta.cw0 = wl + 1;
-                ta.cw1 = pw1;
-                ta.A = A;
-                ta.aw0 = wl;
-                ta.kw = 1;
-                ta.kbits = lw;
-                ta.B = A;
-                ta.bw0 = wl + 1;
-                ta.brow = g.st->brow + 64 * j;
-                ta.row_mode = ROWS_AFTER_LEAF;
-                ta.st = g.st;
-                LaunchTimer t(3, 0, 0);
-                launch_table_apply(s, ta, g.nsm);
-            }
+        }
+        {
+            LaunchTimer t(3, 0, 0);
+            launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+            ++g.launches;  // save + put
         }
         if (pw1 < nw) {
             {
@@ -682,6 +674,15 @@ int f2_stats_reset(void) {
 }
 
 uint64_t f2_last_launch_count(void) { return g.launches; }
+
+// phase clocks recorded by builds compiled with -DF2_LEAF_PROFILE (development aid)
+int f2_debug_clocks(long long* out, int n) {
+    if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
+    long long tmp[16];
+    CK(cudaMemcpy(tmp, &g.st->dbg[0], sizeof(tmp), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 16; ++i) out[i] = tmp[i];
+    return F2_OK;
+}
 
 }  // extern "C"
 

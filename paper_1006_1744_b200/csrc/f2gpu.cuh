@@ -16,6 +16,7 @@ constexpr int kWinSlots = 4;                 // leaf search window: 32 lanes x 4
 constexpr int kWin = 32 * kWinSlots;         // 128 candidate positions in registers
 constexpr int kMaxSwaps = kWin + 64;         // window slots + outside positions
 constexpr int kOmapSlots = 128;              // open-addressing map for outside swaps
+constexpr int kMaxMoved = 8192;              // positions re-mapped during one panel (<= 32 leaves x 192)
 
 struct Mat {
     uint64_t* w;
@@ -25,21 +26,28 @@ struct Mat {
 // Device-resident elimination state.  Every kernel of the engine reads its
 // row offsets and pivot counts from here, so the host enqueues a fixed,
 // data-independent launch sequence and never synchronises mid-factorisation.
+//
+// Row order inside a panel is virtual: position x of the current row order lives
+// in physical row pmap[x] (a separate device array).  The leaves of a panel only
+// rewrite pmap; the panel's row transpositions reach the whole row width in one
+// gather when the panel ends (k_perm_save / k_perm_put), so a panel's leaves never
+// touch columns right of the panel.
 struct PlsState {
     int64_t r;         // next pivot position (= pivots found so far)
     int64_t leaf_r;    // r at the start of the current leaf
     int64_t leaf_kb;   // pivots found by the current leaf
     int64_t panel_r;   // r at the start of the current panel
     int64_t panel_kb;  // pivots found so far in the current panel
-    int32_t nswap;     // row moves produced by the current leaf
+    int32_t nmoved;    // positions whose pmap entry changed during the panel
     int32_t pad0;
     uint64_t leaf_mask;                 // pivot columns within the leaf word
     uint64_t ustrict[64];               // leaf pivot words, bits <= pivot cleared
+    uint64_t ufull[64];                 // leaf pivot words (L bits, leading 1, S bits)
     int32_t q[64];                      // leaf pivot bit positions (0..63)
-    int64_t swap_dst[kMaxSwaps];        // position that receives ...
-    int64_t swap_src[kMaxSwaps];        // ... the pre-leaf content of this physical row
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
+    int64_t moved[kMaxMoved];           // positions with pmap[x] != x (may repeat)
+    long long dbg[16];                  // phase clocks (F2_LEAF_PROFILE builds only)
 };
 
 // How a table-apply launch finds its C/A rows (device-side offsets).

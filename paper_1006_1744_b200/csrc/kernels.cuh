@@ -9,10 +9,17 @@ namespace f2g {
 
 // leaf.cu
 void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp);
-void launch_row_moves(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st);
-void launch_leaf_finalize(cudaStream_t s, const Mat& A, int64_t wl, const PlsState* st, int nsm);
+                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap);
+void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch);
+void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
 void setup_leaf_kernels();
+
+// leafupd.cu — one leaf's update of its panel (virtual row order via pmap):
+// finalize the leaf word of every row below the pivots (-> L coefficients),
+// solve the leaf pivot rows over the rest of the panel, table-apply the rest.
+void launch_leaf_update(cudaStream_t s, const Mat& A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap,
+                        const PlsState* st);
+void setup_leafupd_kernels();
 
 // trsm.cu — forward substitution of pivot rows by 8-column groups with
 // Gray tables (the M4RI-style TRSM of mul.cpp:109-131, blocked for SMEM).

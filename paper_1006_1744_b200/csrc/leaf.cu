@@ -1,8 +1,9 @@
 // Leaf of the PLS engine: one 64-column word of the panel.
 //
-//   k_leaf_pivot    exact Gaussian pivot search on the leaf word (1 CTA)
-//   k_row_moves     applies the leaf's row transpositions to whole rows
-//   k_leaf_finalize eliminates the leaf word of every row >= leaf_r
+//   k_leaf_pivot    exact Gaussian pivot search on the leaf word (1 CTA); the
+//                   leaf's transpositions only re-map positions (pmap)
+//   k_perm_save/put at the end of a panel, the panel's transpositions applied to
+//                   whole rows in one gather
 //
 // Bit-exactness rests on the pivot rule of gauss_pls (proj/src/gauss.cpp:33-49):
 // the pivot is the leftmost column that has a nonzero at or below position r,
@@ -83,8 +84,8 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&v)[S], int s) {
 }
 
 template <int S>
-__device__ __forceinline__ int64_t pick(const int64_t (&v)[S], int s) {
-    int64_t r = v[0];
+__device__ __forceinline__ int32_t pick(const int32_t (&v)[S], int s) {
+    int32_t r = v[0];
 #pragma unroll
     for (int i = 1; i < S; ++i)
         if (s == i) r = v[i];
@@ -93,170 +94,196 @@ __device__ __forceinline__ int64_t pick(const int64_t (&v)[S], int s) {
 
 }  // namespace
 
-// One CTA of 1024 threads.  Warp 0 keeps a window of the first 128 positions
-// of the leaf (r .. r+127) in registers, eagerly eliminated, and finds pivots
-// there without any block-level synchronisation.  The window is exact whenever
-// the leftmost nonzero column among its candidates equals the next unprocessed
-// column (it then cannot be beaten, and window positions precede all others).
-// Otherwise the whole block scans the positions past the window, catching each
-// row up on the pivots found so far, for the leftmost column below the window's
-// candidate (SURVEY.md §7 "Hard parts" 1).
+// One CTA of 1024 threads.  Warp 0 keeps a sliding window of 32 consecutive
+// positions (lane l holds position bb + l), eagerly eliminated, and finds pivots
+// there without block-level synchronisation:
+//   * fast path: the row at the next pivot position p has a 1 in the next
+//     unprocessed column -> it is the pivot, no swap (the common dense case);
+//   * otherwise the leftmost nonzero column c* among the window's candidates;
+//     exact whenever c* is the next column or nothing lies past the window.
+// Once 16 candidates are consumed the window slides to start at p (new rows are
+// caught up on the pivots so far).  When rows past the window could hold an
+// earlier column, the whole block scans them, catching each row up, for the
+// leftmost column below c* (SURVEY.md §7 "Hard parts" 1).
+//
+// Positions are relative to base = st->r; `src` is the relative (pre-leaf)
+// position of the content a lane holds.  Rows are read through pmap.
 __global__ void __launch_bounds__(1024, 1)
 k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, int panel_bits,
-             PlsState* st, int64_t* P, int64_t* Qp) {
-    constexpr int S = kWinSlots;
+             PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap) {
     __shared__ uint64_t s_u[64];
+    __shared__ uint64_t s_uf[64];
     __shared__ int s_q[64];
     __shared__ Omap s_om;
+    __shared__ int64_t s_mv_dst[kMaxSwaps], s_mv_phys[kMaxSwaps];
+    __shared__ int s_nmv;
     __shared__ unsigned long long s_red[32];
     __shared__ unsigned long long s_best;
     __shared__ uint64_t s_bword;
     __shared__ int64_t s_bsrc;
-    __shared__ int s_cmd, s_col, s_lim, s_t;
+    __shared__ int s_cmd, s_col, s_lim, s_t, s_ob;
     __shared__ int s_nom;
     __shared__ int64_t s_om_pos[64];
 
+#ifdef F2_LEAF_PROFILE
+    long long c_start = clock64();
+#define F2_MARK(i) do { if (threadIdx.x == 0) st->dbg[i] = clock64() - c_start; } while (0)
+#else
+#define F2_MARK(i) do { } while (0)
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     const int64_t m = A.m, stride = A.stride;
     const int64_t base = st->r;
-    const int64_t ob = base + kWin;  // first position outside the window
+    const int64_t span64 = m - base;
+    const int span = span64 > (1 << 30) ? (1 << 30) : static_cast<int>(span64);  // positions left
 
     for (int i = tid; i < kOmapSlots; i += blockDim.x) s_om.key[i] = -1;
     if (first_in_panel)
         for (int i = tid; i < panel_bits; i += blockDim.x) st->brow[i] = -1;
-    if (tid == 0) s_nom = 0;
+    if (tid == 0) {
+        s_nom = 0;
+        if (first_in_panel) st->nmoved = 0;
+    }
     __syncthreads();
 
-    // warp-0 register window
-    uint64_t wv[S];
-    int64_t src[S];
-    int t = 0, col = 0;
-    int64_t pos = base;
-    if (warp == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            int64_t p = base + lane + 32 * s;
-            wv[s] = p < m ? A.w[p * stride + wl] : 0ull;
-            src[s] = p;
-        }
-    }
+    uint64_t w = 0;
+    int src = 0;
+    int t = 0, col = 0, p = 0, bb = 0, nmv = 0;
 
-    // swap position `pos` with window slot (ls, ss) / bring in an outside word,
-    // record the pivot and eliminate the window below it
-    auto take_pivot = [&](int cstar, uint64_t u, int64_t usrc, int64_t pstar, bool from_window,
-                          int ln, int sl) {
-        const int ps = static_cast<int>((pos - base) >> 5), pl = static_cast<int>((pos - base) & 31);
-        uint64_t vpos = __shfl_sync(FULL, pick<S>(wv, ps), pl);
-        int64_t spos = __shfl_sync(FULL, pick<S>(src, ps), pl);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            if (from_window && lane == ln && s == sl) {
-                wv[s] = vpos;
-                src[s] = spos;
-            }
+    // fresh content of relative position x (outside the registers), caught up on tt pivots
+    auto load_fresh = [&](int x, int tt, uint64_t& wo, int& so) {
+        if (x >= span) {
+            wo = 0;
+            so = x;
+            return;
         }
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            if (lane == pl && s == ps) {
-                wv[s] = u;
-                src[s] = usrc;
-            }
+        const int64_t sabs = omap_get(s_om, base + x);
+        so = static_cast<int>(sabs - base);
+        uint64_t v = A.w[pmap[sabs] * stride + wl];
+        for (int l = 0; l < tt; ++l)
+            if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
+        wo = v;
+    };
+    // append (position base+x <- pre-leaf position base+sx) to the move list, warp-wide
+    auto record_moves = [&](bool moved, int x, int sx) {
+        const unsigned b = __ballot_sync(FULL, moved);
+        if (moved) {
+            const int idx = nmv + __popc(b & ((1u << lane) - 1));
+            s_mv_dst[idx] = base + x;
+            s_mv_phys[idx] = pmap[base + sx];
         }
-        const uint64_t us = u & above(cstar);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            int64_t p = base + lane + 32 * s;
-            if (p > pos && p < m && ((wv[s] >> cstar) & 1ull)) wv[s] ^= us;
-        }
+        nmv += __popc(b);
+    };
+    auto record_pivot = [&](int cstar, uint64_t u, int64_t pabs_src) {
         if (lane == 0) {
-            s_u[t] = us;
+            s_u[t] = u & above(cstar);
+            s_uf[t] = u;
             s_q[t] = cstar;
-            P[pos] = pstar;
-            Qp[pos] = wl * 64 + cstar;
-            if (!from_window) {
-                omap_put(s_om, pstar, spos);
-                s_om_pos[s_nom] = pstar;
-                s_nom = s_nom + 1;
-            }
+            P[base + p] = pabs_src;
+            Qp[base + p] = wl * 64 + cstar;
         }
         __syncwarp();
-        ++t;
-        ++pos;
-        col = cstar + 1;
     };
+
+    F2_MARK(0);
+    if (warp == 0) load_fresh(lane, 0, w, src);
+    F2_MARK(1);
 
     while (true) {
         if (warp == 0) {
             int cmd = 0, lim = 64;
             while (true) {
-                if (pos >= m || col >= lw) {
+                if (col >= lw || p >= span) {
                     cmd = 0;
                     break;
                 }
-                const uint64_t cmask = ~0ull << col;
-                uint64_t orv = 0;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    int64_t p = base + lane + 32 * s;
-                    if (p >= pos && p < m) orv |= wv[s] & cmask;
+                if (p - bb >= 16 && bb + 32 < span) {  // slide the window to start at p
+                    const int d = p - bb;
+                    record_moves(lane < d && src != bb + lane, bb + lane, src);
+                    uint64_t wn = __shfl_down_sync(FULL, w, d);
+                    int sn = __shfl_down_sync(FULL, src, d);
+                    if (lane >= 32 - d) load_fresh(p + lane, t, wn, sn);
+                    w = wn;
+                    src = sn;
+                    bb = p;
                 }
-                const uint64_t any = warp_or64(orv);
-                const int cstar = any ? __ffsll(static_cast<long long>(any)) - 1 : 64;
-                if (ob < m && cstar != col) {  // rows past the window may hold an earlier column
-                    cmd = 1;
-                    lim = cstar;
-                    break;
-                }
-                if (!any) {
-                    cmd = 0;
-                    break;
-                }
-                int sl = -1, ln = 0;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    int64_t p = base + lane + 32 * s;
-                    unsigned b = __ballot_sync(FULL, p >= pos && p < m && ((wv[s] >> cstar) & 1ull));
-                    if (sl < 0 && b) {
-                        sl = s;
-                        ln = __ffs(b) - 1;
+                const int pr = p - bb;
+                const bool outside = bb + 32 < span;
+                const uint64_t wp = __shfl_sync(FULL, w, pr);
+                int cstar, ln;
+                uint64_t u;
+                if ((wp >> col) & 1ull) {  // the row at p already has the next column
+                    cstar = col;
+                    ln = pr;
+                    u = wp;
+                } else {
+                    const uint64_t any = warp_or64(lane >= pr ? (w & (~0ull << col)) : 0ull);
+                    cstar = any ? __ffsll(static_cast<long long>(any)) - 1 : 64;
+                    if (outside && cstar != col) {
+                        cmd = 1;
+                        lim = cstar;
+                        break;
+                    }
+                    if (!any) {
+                        cmd = 0;
+                        break;
+                    }
+                    const unsigned hit = __ballot_sync(FULL, lane >= pr && ((w >> cstar) & 1ull));
+                    ln = __ffs(hit) - 1;
+                    u = __shfl_sync(FULL, w, ln);
+                    const int usrc = __shfl_sync(FULL, src, ln);
+                    const int psrc = __shfl_sync(FULL, src, pr);
+                    if (lane == ln) {
+                        w = wp;
+                        src = psrc;
+                    }
+                    if (lane == pr) {
+                        w = u;
+                        src = usrc;
                     }
                 }
-                const uint64_t u = __shfl_sync(FULL, pick<S>(wv, sl), ln);
-                const int64_t usrc = __shfl_sync(FULL, pick<S>(src, sl), ln);
-                take_pivot(cstar, u, usrc, base + ln + 32 * sl, true, ln, sl);
+                record_pivot(cstar, u, base + bb + ln);
+                const uint64_t us = u & above(cstar);
+                if (lane > pr && ((w >> cstar) & 1ull)) w ^= us;
+                ++t;
+                ++p;
+                col = cstar + 1;
             }
             if (lane == 0) {
                 s_cmd = cmd;
                 s_col = col;
                 s_lim = lim;
                 s_t = t;
+                s_ob = bb + 32;
             }
+            F2_MARK(2);
         }
         __syncthreads();
         if (s_cmd == 0) break;
 
         // ---- block-wide scan of positions [ob, m) for the leftmost column in [col, lim)
+        const int64_t ob = base + s_ob;
         {
             const int c0 = s_col, tt = s_t;
             int lim = s_lim;
             if (tid == 0) s_best = KEY_NONE;
             __syncthreads();
             for (int64_t b = ob; b < m; b += blockDim.x) {
-                const int64_t p = b + tid;
+                const int64_t pp = b + tid;
                 unsigned long long key = KEY_NONE;
-                uint64_t w = 0;
-                int64_t sp = p;
-                if (p < m) {
-                    sp = omap_get(s_om, p);
-                    w = A.w[sp * stride + wl];
+                uint64_t v = 0;
+                int64_t sp = pp;
+                if (pp < m) {
+                    sp = omap_get(s_om, pp);
+                    v = A.w[pmap[sp] * stride + wl];
                     for (int l = 0; l < tt; ++l)
-                        if ((w >> s_q[l]) & 1ull) w ^= s_u[l];
-                    uint64_t v = w & (~0ull << c0);
-                    if (lim < 64) v &= (1ull << lim) - 1;
-                    if (v)
-                        key = (static_cast<unsigned long long>(__ffsll(static_cast<long long>(v)) - 1) << 48) |
-                              static_cast<unsigned long long>(p - ob);
+                        if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
+                    uint64_t z = v & (~0ull << c0);
+                    if (lim < 64) z &= (1ull << lim) - 1;
+                    if (z)
+                        key = (static_cast<unsigned long long>(__ffsll(static_cast<long long>(z)) - 1) << 48) |
+                              static_cast<unsigned long long>(pp - ob);
                 }
                 unsigned long long k = warp_min64(key);
                 if (lane == 0) s_red[warp] = k;
@@ -269,7 +296,7 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
                 __syncthreads();
                 const unsigned long long bk = s_best;
                 if (key != KEY_NONE && key == bk) {
-                    s_bword = w;
+                    s_bword = v;
                     s_bsrc = sp;
                 }
                 if (bk != KEY_NONE) {
@@ -284,26 +311,51 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
         if (warp == 0) {
             const unsigned long long bk = s_best;
             const int lim = s_lim;
+            const int pr = p - bb;
             if (bk != KEY_NONE && static_cast<int>(bk >> 48) < lim) {
+                // the outside row enters at p; the content of p leaves for pstar
                 const int cstar = static_cast<int>(bk >> 48);
                 const int64_t pstar = ob + static_cast<int64_t>(bk & ((1ull << 48) - 1));
-                take_pivot(cstar, s_bword, s_bsrc, pstar, false, 0, 0);
+                const uint64_t u = s_bword;
+                const int psrc = __shfl_sync(FULL, src, pr);
+                if (lane == pr) {
+                    w = u;
+                    src = static_cast<int>(s_bsrc - base);
+                }
+                if (lane == 0) {
+                    omap_put(s_om, pstar, base + psrc);
+                    s_om_pos[s_nom] = pstar;
+                    s_nom = s_nom + 1;
+                }
+                record_pivot(cstar, u, pstar);
+                const uint64_t us = u & above(cstar);
+                if (lane > pr && ((w >> cstar) & 1ull)) w ^= us;
+                ++t;
+                ++p;
+                col = cstar + 1;
             } else if (lim < 64) {
                 // columns [col, lim) are zero everywhere: pivot in the window at column lim
                 const int cstar = lim;
-                int sl = -1, ln = 0;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    int64_t p = base + lane + 32 * s;
-                    unsigned b = __ballot_sync(FULL, p >= pos && p < m && ((wv[s] >> cstar) & 1ull));
-                    if (sl < 0 && b) {
-                        sl = s;
-                        ln = __ffs(b) - 1;
-                    }
+                const unsigned hit = __ballot_sync(FULL, lane >= pr && ((w >> cstar) & 1ull));
+                const int ln = __ffs(hit) - 1;
+                const uint64_t u = __shfl_sync(FULL, w, ln);
+                const uint64_t wp = __shfl_sync(FULL, w, pr);
+                const int usrc = __shfl_sync(FULL, src, ln);
+                const int psrc = __shfl_sync(FULL, src, pr);
+                if (lane == ln) {
+                    w = wp;
+                    src = psrc;
                 }
-                const uint64_t u = __shfl_sync(FULL, pick<S>(wv, sl), ln);
-                const int64_t usrc = __shfl_sync(FULL, pick<S>(src, sl), ln);
-                take_pivot(cstar, u, usrc, base + ln + 32 * sl, true, ln, sl);
+                if (lane == pr) {
+                    w = u;
+                    src = usrc;
+                }
+                record_pivot(cstar, u, base + bb + ln);
+                const uint64_t us = u & above(cstar);
+                if (lane > pr && ((w >> cstar) & 1ull)) w ^= us;
+                ++t;
+                ++p;
+                col = cstar + 1;
             } else {
                 col = 64;  // nothing left in this leaf
             }
@@ -311,125 +363,111 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
         __syncthreads();
     }
 
-    // ---- outputs
+    // ---- outputs: re-map the moved positions (pmap[dst] <- pmap[pre-leaf source]),
+    // write the pivot rows' final leaf words, publish the pivots
+    F2_MARK(3);
     if (warp == 0) {
-        const int kb = t;
-        int n_out = 0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            int64_t p = base + lane + 32 * s;
-            bool moved = p < m && src[s] != p;
-            unsigned b = __ballot_sync(FULL, moved);
-            if (moved) {
-                int idx = n_out + __popc(b & ((1u << lane) - 1));
-                st->swap_dst[idx] = p;
-                st->swap_src[idx] = src[s];
-            }
-            n_out += __popc(b);
-        }
+        record_moves(bb + lane < span && src != bb + lane, bb + lane, src);
         if (lane == 0) {
             for (int i = 0; i < s_nom; ++i) {
-                int64_t p = s_om_pos[i];
+                const int64_t pp = s_om_pos[i];
+                if (pp < base + bb + 32) continue;  // absorbed by the window: recorded above
                 bool dup = false;
-                for (int j = 0; j < i; ++j) dup |= (s_om_pos[j] == p);
+                for (int j = 0; j < i; ++j) dup |= (s_om_pos[j] == pp);
                 if (dup) continue;
-                int64_t v = omap_get(s_om, p);
-                if (v != p) {
-                    st->swap_dst[n_out] = p;
-                    st->swap_src[n_out] = v;
-                    ++n_out;
+                const int64_t v = omap_get(s_om, pp);
+                if (v != pp) {
+                    s_mv_dst[nmv] = pp;
+                    s_mv_phys[nmv] = pmap[v];
+                    ++nmv;
                 }
             }
-            st->nswap = n_out;
-            st->leaf_r = base;
-            st->leaf_kb = kb;
-            st->r = base + kb;
-            uint64_t mask = 0;
-            for (int l = 0; l < kb; ++l) mask |= 1ull << s_q[l];
-            st->leaf_mask = mask;
-            int64_t pkb = first_in_panel ? 0 : st->panel_kb;
-            if (first_in_panel) st->panel_r = base;
-            for (int l = 0; l < kb; ++l) {
-                st->panel_q[pkb + l] = leaf_in_panel * 64 + s_q[l];
-                st->brow[leaf_in_panel * 64 + s_q[l]] = base + l;
-            }
-            st->panel_kb = pkb + kb;
+            s_nmv = nmv;
         }
-        for (int l = lane; l < 64; l += 32) {
-            st->ustrict[l] = l < kb ? s_u[l] : 0ull;
-            st->q[l] = l < kb ? s_q[l] : 64;
+    }
+    __syncthreads();
+    const int nmv_all = s_nmv;
+    const int mv0 = first_in_panel ? 0 : st->nmoved;
+    for (int i = tid; i < nmv_all; i += blockDim.x) {
+        pmap[s_mv_dst[i]] = s_mv_phys[i];
+        st->moved[mv0 + i] = s_mv_dst[i];
+    }
+    __syncthreads();
+    const int kb = s_t;
+    // pivot rows carry their final leaf word (L bits, leading 1, S bits) from here on
+    for (int l = tid; l < kb; l += blockDim.x) A.w[pmap[base + l] * stride + wl] = s_uf[l];
+    if (tid == 0) {
+        st->nmoved = mv0 + nmv_all;
+        st->leaf_r = base;
+        st->leaf_kb = kb;
+        st->r = base + kb;
+        uint64_t mask = 0;
+        for (int l = 0; l < kb; ++l) mask |= 1ull << s_q[l];
+        st->leaf_mask = mask;
+        const int64_t pkb = first_in_panel ? 0 : st->panel_kb;
+        if (first_in_panel) st->panel_r = base;
+        for (int l = 0; l < kb; ++l) {
+            st->panel_q[pkb + l] = leaf_in_panel * 64 + s_q[l];
+            st->brow[leaf_in_panel * 64 + s_q[l]] = base + l;
         }
+        st->panel_kb = pkb + kb;
+    }
+    F2_MARK(4);
+    for (int l = tid; l < 64; l += blockDim.x) {
+        st->ustrict[l] = l < kb ? s_u[l] : 0ull;
+        st->ufull[l] = l < kb ? s_uf[l] : 0ull;
+        st->q[l] = l < kb ? s_q[l] : 64;
     }
 }
 
-// Row moves of one leaf: position swap_dst[i] receives the pre-leaf content of
-// physical row swap_src[i].  The sets of destinations and sources coincide, so
-// every CTA stages its column slice of all sources before writing.
-__global__ void __launch_bounds__(256)
-k_row_moves(Mat A, int64_t nwords, const PlsState* st) {
-    extern __shared__ uint64_t s_buf[];  // [kMaxSwaps][32]
-    const int ns = st->nswap;
-    if (ns == 0) return;
-    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * 32;
-    const int nw = static_cast<int>(nwords - w0 < 32 ? nwords - w0 : 32);
-    for (int i = threadIdx.x; i < ns * 32; i += blockDim.x) {
-        int e = i >> 5, k = i & 31;
-        if (k < nw) s_buf[i] = A.w[st->swap_src[e] * A.stride + w0 + k];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < ns * 32; i += blockDim.x) {
-        int e = i >> 5, k = i & 31;
-        if (k < nw) A.w[st->swap_dst[e] * A.stride + w0 + k] = s_buf[i];
+// Panel end, step 1: copy the rows that the panel's positions now refer to
+// (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
+__global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
+                                                  uint64_t* scratch) {
+    const int n = st->nmoved;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nwords) return;
+    for (int i = blockIdx.y; i < n; i += gridDim.y)
+        scratch[static_cast<int64_t>(i) * A.stride + k] = A.w[pmap[st->moved[i]] * A.stride + k];
+}
+
+// Panel end, step 2: physical row x <- saved content, pmap back to identity.
+// This applies the panel's transpositions (perm.cpp:8-16) to every column.
+__global__ void __launch_bounds__(256) k_perm_put(Mat A, int64_t nwords, const PlsState* st, int64_t* pmap,
+                                                 const uint64_t* scratch) {
+    const int n = st->nmoved;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (int i = blockIdx.y; i < n; i += gridDim.y) {
+        const int64_t x = st->moved[i];
+        if (k < nwords) A.w[x * A.stride + k] = scratch[static_cast<int64_t>(i) * A.stride + k];
+        if (k == 0) pmap[x] = x;
     }
 }
 
-// Eliminate the leaf word of every row at position >= leaf_r: the row at
-// position leaf_r + t (t < kb) is pivot row t and takes pivots l < t; every
-// other row takes all kb pivots.  Afterwards a non-pivot row's leaf word holds
-// exactly its L coefficients at the pivot columns (gauss.cpp:47-49).
-__global__ void __launch_bounds__(256)
-k_leaf_finalize(Mat A, int64_t wl, const PlsState* st) {
-    __shared__ uint64_t su[64];
-    __shared__ int sq[64];
-    const int64_t kb = st->leaf_kb, r0 = st->leaf_r;
-    if (kb == 0) return;
-    if (threadIdx.x < 64) {
-        su[threadIdx.x] = st->ustrict[threadIdx.x];
-        sq[threadIdx.x] = st->q[threadIdx.x];
-    }
-    __syncthreads();
-    for (int64_t p = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < A.m;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        uint64_t* wp = A.w + p * A.stride + wl;
-        uint64_t w = *wp;
-        const int tl = static_cast<int>(p - r0 < kb ? p - r0 : kb);
-        for (int l = 0; l < tl; ++l)
-            if ((w >> sq[l]) & 1ull) w ^= su[l];
-        *wp = w;
-    }
+__global__ void k_pmap_init(int64_t* pmap, int64_t m) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        pmap[i] = i;
 }
 
 void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp) {
-    k_leaf_pivot<<<1, 1024, 0, s>>>(A, wl, lw, first, leaf_in_panel, panel_bits, st, P, Qp);
+                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap) {
+    k_leaf_pivot<<<1, 1024, 0, s>>>(A, wl, lw, first, leaf_in_panel, panel_bits, st, P, Qp, pmap);
 }
 
-void launch_row_moves(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st) {
-    const int grid = static_cast<int>((nwords + 31) / 32);
-    const size_t smem = sizeof(uint64_t) * kMaxSwaps * 32;
-    k_row_moves<<<grid, 256, smem, s>>>(A, nwords, st);
+void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch) {
+    dim3 grid(static_cast<unsigned>((nwords + 255) / 256), 64);
+    k_perm_save<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
+    k_perm_put<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
 }
 
-void launch_leaf_finalize(cudaStream_t s, const Mat& A, int64_t wl, const PlsState* st, int nsm) {
-    int64_t blocks = (A.m + 255) / 256;
-    int grid = static_cast<int>(blocks < 4 * nsm ? blocks : 4 * nsm);
-    if (grid < 1) grid = 1;
-    k_leaf_finalize<<<grid, 256, 0, s>>>(A, wl, st);
+void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {
+    int64_t g = (m + 255) / 256;
+    if (g > 1024) g = 1024;
+    if (g < 1) g = 1;
+    k_pmap_init<<<static_cast<int>(g), 256, 0, s>>>(pmap, m);
 }
 
-void setup_leaf_kernels() {
-    cudaFuncSetAttribute(k_row_moves, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(uint64_t) * kMaxSwaps * 32));
-}
+void setup_leaf_kernels() {}
 
 }  // namespace f2g

@@ -36,7 +36,8 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
     extern __shared__ uint64_t smem[];
     uint64_t* X = smem;                          // [kMaxRows][kTW]
     uint64_t* T = X + kMaxRows * kTW;            // [256][kTW]
-    int32_t* sq = reinterpret_cast<int32_t*>(T + 256 * kTW);  // [kMaxRows]
+    uint64_t* cw = T + 256 * kTW;                // [kMaxRows] coefficient word of the current 8 groups
+    int32_t* sq = reinterpret_cast<int32_t*>(cw + kMaxRows);  // [kMaxRows]
     int32_t* gstart = sq + kMaxRows;             // [kMaxPanelBits/8 + 1]
 
     int64_t kb, r0;
@@ -76,26 +77,41 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
         }
         gstart[g] = lo;
     }
-    __syncthreads();
-
-    auto coef_byte = [&](int t, int g) -> unsigned {
-        const uint64_t w = ps.mode == 2 ? L.w[static_cast<int64_t>(t) * L.stride + (g >> 3)]
-                                        : A.w[(r0 + t) * A.stride + coef_w0 + (g >> 3)];
-        return static_cast<unsigned>((w >> (8 * (g & 7))) & 0xffu);
-    };
 
     for (int g = 0; g < ngroups; ++g) {
+        if ((g & 7) == 0) {
+            // stage coefficient word g/8 of every pivot row
+            __syncthreads();
+            for (int t = tid; t < nk; t += nth)
+                cw[t] = ps.mode == 2 ? L.w[static_cast<int64_t>(t) * L.stride + (g >> 3)]
+                                     : A.w[(r0 + t) * A.stride + coef_w0 + (g >> 3)];
+        }
+        __syncthreads();
         const int t0 = gstart[g], t1 = gstart[g + 1];
         if (t0 == t1) continue;
+        const int sh = 8 * (g & 7), base = 8 * g;
         if (t1 - t0 > 1 && tid < kTW) {
-            const int j = tid;
-            for (int t = t0 + 1; t < t1; ++t) {
-                unsigned cb = coef_byte(t, g) & ((1u << (sq[t] - 8 * g)) - 1u);
-                uint64_t v = X[t * kTW + j];
-                for (int l = t0; l < t; ++l)
-                    if ((cb >> (sq[l] - 8 * g)) & 1u) v ^= X[l * kTW + j];
-                X[t * kTW + j] = v;
+            // in-group forward substitution, rows held in registers
+            const int j = tid, ng = t1 - t0;
+            uint64_t x[8];
+            int qb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                x[u] = u < ng ? X[(t0 + u) * kTW + j] : 0ull;
+                qb[u] = u < ng ? sq[t0 + u] - base : 8;
             }
+#pragma unroll
+            for (int u = 1; u < 8; ++u) {
+                if (u < ng) {
+                    const unsigned cb = static_cast<unsigned>(cw[t0 + u] >> sh) & 0xffu;
+#pragma unroll
+                    for (int l = 0; l < u; ++l)
+                        if ((cb >> qb[l]) & 1u) x[u] ^= x[l];
+                }
+            }
+#pragma unroll
+            for (int u = 1; u < 8; ++u)
+                if (u < ng) X[(t0 + u) * kTW + j] = x[u];
         }
         if (t1 >= nk) break;
         __syncthreads();
@@ -103,15 +119,15 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
             const int e = i / kTW, j = i % kTW;
             uint64_t v = 0;
             for (int l = t0; l < t1; ++l)
-                if ((e >> (sq[l] - 8 * g)) & 1) v ^= X[l * kTW + j];
+                if ((e >> (sq[l] - base)) & 1) v ^= X[l * kTW + j];
             T[i] = v;
         }
         __syncthreads();
         for (int i = tid; i < (nk - t1) * kTW; i += nth) {
             const int t = t1 + i / kTW, j = i % kTW;
-            X[t * kTW + j] ^= T[coef_byte(t, g) * kTW + j];
+            const unsigned cb = static_cast<unsigned>(cw[t] >> sh) & 0xffu;
+            X[t * kTW + j] ^= T[cb * kTW + j];
         }
-        __syncthreads();
     }
     __syncthreads();
     for (int i = tid; i < nk * kTW; i += nth) {
@@ -121,7 +137,7 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
 }
 
 static size_t trsm_smem() {
-    return sizeof(uint64_t) * (kMaxRows * kTW + 256 * kTW) + sizeof(int32_t) * (kMaxRows + kMaxPanelBits / 8 + 8);
+    return sizeof(uint64_t) * (kMaxRows * kTW + 256 * kTW + kMaxRows) + sizeof(int32_t) * (kMaxRows + kMaxPanelBits / 8 + 8);
 }
 
 void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_words, int64_t tw0,
