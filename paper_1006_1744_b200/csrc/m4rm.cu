@@ -13,13 +13,13 @@
 // is zero in every row the kernel touches and maps to no B row), so no compaction
 // pass exists and the L bits are never rewritten.
 //
-// CTA tile: 1024 rows x 512 bits of C (16 warps), accumulated in registers over
-// all of K.  Per 8-bit chunk of K the CTA builds a 256 x 512-bit table in SMEM
-// (double buffered, 16 KB each) from 8 B rows staged by cp.async three chunks
-// ahead; every row then does one 16-byte LDS per thread (4 lanes cover one 64-byte
-// table row, 8 rows per warp instruction: conflict-free).  The coefficient words
-// of the tile's rows are staged in SMEM one K-word ahead.  SMEM bandwidth bounds
-// it: per chunk 1024 lookups x 64 B + 256 table rows x 64 B.
+// CTA tile: 1024 rows x 1024 bits of C (16 warps), accumulated in registers over
+// all of K.  Per 8-bit chunk of K the CTA builds a 256 x 1024-bit table in SMEM
+// (double buffered, 32 KB each) from 8 B rows staged by cp.async three chunks
+// ahead; every row then does one 16-byte LDS per thread (8 lanes cover one
+// 128-byte table row, so each quarter-warp reads one whole row: conflict-free).
+// The coefficient words of the tile's rows are staged in SMEM one K-word ahead.
+// SMEM bandwidth bounds it: per chunk 1024 lookups x 128 B + 256 table rows x 128 B.
 #include <cstdint>
 
 #include "f2gpu.cuh"
@@ -31,15 +31,15 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRPT = 8;                          // rows per thread
-constexpr int kTNW = 8;                          // 64-bit words per tile row (512 bits)
-constexpr int kTM = kWarps * 8 * kRPT;           // 1024 rows per CTA (8 rows per warp instruction)
+constexpr int kRPT = 16;                         // rows per thread
+constexpr int kTNW = 16;                         // 64-bit words per tile row (1024 bits)
+constexpr int kTM = kWarps * 4 * kRPT;           // 1024 rows per CTA (4 rows per warp instruction)
 constexpr int kStages = 4;                       // B-row ring depth
 constexpr int kMaxMap = kMaxPanelBits;           // K bits held in the SMEM row map
 
 // shared memory carve-up (bytes)
-constexpr size_t kOffT = 0;                                   // [2][256][kTNW] u64   32 KB
-constexpr size_t kOffRing = kOffT + 2 * 256 * kTNW * 8;        // [kStages][8][kTNW]    2 KB
+constexpr size_t kOffT = 0;                                   // [2][256][kTNW] u64   64 KB
+constexpr size_t kOffRing = kOffT + 2 * 256 * kTNW * 8;        // [kStages][8][kTNW]    4 KB
 constexpr size_t kOffA = kOffRing + kStages * 8 * kTNW * 8;    // [2][kTM] u64          16 KB
 constexpr size_t kOffMap = kOffA + 2 * kTM * 8;                // [kMaxMap] i32         8 KB
 constexpr size_t kOffLive = kOffMap + kMaxMap * 4;             // [kMaxMap/8/32] u32
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     const int64_t nrows = p.c_r1 - row_base < kTM ? p.c_r1 - row_base : kTM;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rq = lane >> 2, wp = lane & 3;
+    const int rq = lane >> 3, wp = lane & 7;
     const int64_t cwa = tile_w0 + 2 * wp, cwb = cwa + 1;
     const bool va = cwa < p.cw1, vb = cwb < p.cw1;
     const int nch = static_cast<int>((p.kbits + 7) / 8);
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     // B rows of chunk c -> ring stage c % kStages (threads 0..63, one word each)
     auto issue_b = [&](int c) {
         if (tid < 8 * kTNW) {
-            const int b = tid >> 3, k = tid & 7;
+            const int b = tid >> 4, k = tid & 15;
             const int64_t br = brow_of(c * 8 + b);
             const int64_t wcol = tile_w0 + k;
             const bool ok = br >= 0 && wcol < p.cw1;
@@ -142,25 +142,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         }
     };
     // 256-entry table of chunk c: entry e = xor of B rows b with bit b of e (LSB first)
+    // built by warps 0..3 only (fewer ring reads): thread = (16-byte column chunk wp,
+    // low nibble el of the entry); the high nibble is walked in Gray order
     auto build = [&](int c) {
+        if (warp >= 4) return;
         const uint64_t* rs = ring + (c % kStages) * 8 * kTNW + 2 * wp;
-        uint4 v[8];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) v[b] = lds128(rs + b * kTNW);
-        const int el = tid >> 2;  // low 7 bits of the entry
+        const int el = tid >> 3;  // 0..15
         uint4 lo = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int b = 0; b < 7; ++b)
-            if ((el >> b) & 1) lo = xor4(lo, v[b]);
+        for (int b = 0; b < 4; ++b) {
+            const uint4 v = lds128(rs + b * kTNW);
+            if ((el >> b) & 1) lo = xor4(lo, v);
+        }
+        uint4 hv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) hv[b] = lds128(rs + (4 + b) * kTNW);
         uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
-        sts128(tb + el * kTNW, lo);
-        sts128(tb + (el + 128) * kTNW, xor4(lo, v[7]));
+        uint4 x = lo;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (k) x = xor4(x, hv[(k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3))]);
+            const int eh = k ^ (k >> 1);
+            sts128(tb + (eh * 16 + el) * kTNW, x);
+        }
     };
 
     uint64_t acc0[kRPT], acc1[kRPT];
 #pragma unroll
     for (int i = 0; i < kRPT; ++i) {
-        const int64_t row = row_base + warp * 64 + rq + 8 * i;
+        const int64_t row = row_base + warp * 64 + rq + 4 * i;
         const bool rv = row < p.c_r1;
         const uint64_t* cr = p.C.w + row * p.C.stride;
         acc0[i] = (rv && va) ? cr[cwa] : 0ull;
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     __syncthreads();
     if (nch > 0 && live(0)) build(0);
 
-    uint64_t aw[kRPT];
+    uint32_t aw[kRPT];  // coefficient bits of the current half K-word (4 chunks)
     const int ngroups = (nch + 7) / 8;
     for (int g = 0; g < ngroups; ++g) {
 #pragma unroll
@@ -188,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
                 cp_async_commit();
                 cp_async_wait<2>();
                 __syncthreads();
-                if (j == 0) {
-                    const uint64_t* ab = abuf + (g & 1) * kTM + warp * 64 + rq;
+                if (j == 0 || j == 4) {
+                    const uint32_t* ab = reinterpret_cast<const uint32_t*>(abuf + (g & 1) * kTM + warp * 64 + rq) + (j >> 2);
 #pragma unroll
                     for (int i = 0; i < kRPT; ++i) aw[i] = ab[8 * i];
                 }
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
                     const uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
 #pragma unroll
                     for (int i = 0; i < kRPT; ++i) {
-                        const unsigned idx = static_cast<unsigned>(aw[i] >> (8 * j)) & 0xffu;
+                        const unsigned idx = (aw[i] >> (8 * (j & 3))) & 0xffu;
                         const uint4 t = lds128(tb + idx * kTNW);
                         acc0[i] ^= static_cast<uint64_t>(t.x) | (static_cast<uint64_t>(t.y) << 32);
                         acc1[i] ^= static_cast<uint64_t>(t.z) | (static_cast<uint64_t>(t.w) << 32);
@@ -211,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
 
 #pragma unroll
     for (int i = 0; i < kRPT; ++i) {
-        const int64_t row = row_base + warp * 64 + rq + 8 * i;
+        const int64_t row = row_base + warp * 64 + rq + 4 * i;
         if (row < p.c_r1) {
             uint64_t* cr = p.C.w + row * p.C.stride;
             if (va) cr[cwa] = acc0[i];
