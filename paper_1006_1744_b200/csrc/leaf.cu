@@ -152,6 +152,21 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
     int t = 0, col = 0, p = 0, bb = 0, nmv = 0;
 
     // fresh content of relative position x (outside the registers), caught up on tt pivots
+    // apply pivots 0..tt-1 to a pre-leaf word (loads independent of the chain)
+    auto catch_up = [&](uint64_t v, int tt) -> uint64_t {
+        int l = 0;
+        for (; l + 4 <= tt; l += 4) {
+            const uint64_t u0 = s_u[l], u1 = s_u[l + 1], u2 = s_u[l + 2], u3 = s_u[l + 3];
+            const int q0 = s_q[l], q1 = s_q[l + 1], q2 = s_q[l + 2], q3 = s_q[l + 3];
+            v ^= ((v >> q0) & 1ull) ? u0 : 0ull;
+            v ^= ((v >> q1) & 1ull) ? u1 : 0ull;
+            v ^= ((v >> q2) & 1ull) ? u2 : 0ull;
+            v ^= ((v >> q3) & 1ull) ? u3 : 0ull;
+        }
+        for (; l < tt; ++l) v ^= ((v >> s_q[l]) & 1ull) ? s_u[l] : 0ull;
+        return v;
+    };
+    // fresh content of relative position x (outside the registers), caught up on tt pivots
     auto load_fresh = [&](int x, int tt, uint64_t& wo, int& so) {
         if (x >= span) {
             wo = 0;
@@ -160,11 +175,12 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
         }
         const int64_t sabs = omap_get(s_om, base + x);
         so = static_cast<int>(sabs - base);
-        uint64_t v = A.w[pmap[sabs] * stride + wl];
-        for (int l = 0; l < tt; ++l)
-            if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
-        wo = v;
+        wo = catch_up(A.w[pmap[sabs] * stride + wl], tt);
     };
+    // raw pre-leaf word of relative position x, loaded early for the next slide
+    uint64_t pf_w = 0;
+    auto prefetch = [&](int x) { pf_w = x < span ? A.w[pmap[base + x] * stride + wl] : 0ull; };
+
     // append (position base+x <- pre-leaf position base+sx) to the move list, warp-wide
     auto record_moves = [&](bool moved, int x, int sx) {
         const unsigned b = __ballot_sync(FULL, moved);
@@ -187,7 +203,10 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
     };
 
     F2_MARK(0);
-    if (warp == 0) load_fresh(lane, 0, w, src);
+    if (warp == 0) {
+        load_fresh(lane, 0, w, src);
+        prefetch(32 + lane);
+    }
     F2_MARK(1);
 
     while (true) {
@@ -199,28 +218,34 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
                     break;
                 }
                 if (p - bb >= 16 && bb + 32 < span) {  // slide the window to start at p
+                    __syncwarp();
                     const int d = p - bb;
                     record_moves(lane < d && src != bb + lane, bb + lane, src);
                     uint64_t wn = __shfl_down_sync(FULL, w, d);
                     int sn = __shfl_down_sync(FULL, src, d);
-                    if (lane >= 32 - d) load_fresh(p + lane, t, wn, sn);
+                    const uint64_t pw = __shfl_sync(FULL, pf_w, (lane + d) & 31);
+                    if (lane >= 32 - d) {
+                        const int x = p + lane;
+                        if (s_nom != 0 || x >= span) {
+                            load_fresh(x, t, wn, sn);
+                        } else {
+                            wn = catch_up(pw, t);
+                            sn = x;
+                        }
+                    }
                     w = wn;
                     src = sn;
                     bb = p;
+                    prefetch(bb + 32 + lane);
                 }
                 const int pr = p - bb;
-                const bool outside = bb + 32 < span;
-                const uint64_t wp = __shfl_sync(FULL, w, pr);
-                int cstar, ln;
-                uint64_t u;
-                if ((wp >> col) & 1ull) {  // the row at p already has the next column
-                    cstar = col;
-                    ln = pr;
-                    u = wp;
-                } else {
-                    const uint64_t any = warp_or64(lane >= pr ? (w & (~0ull << col)) : 0ull);
+                const bool cand = lane >= pr;
+                unsigned hit = __ballot_sync(FULL, cand && ((w >> col) & 1ull));
+                int cstar = col;
+                if (hit == 0) {
+                    const uint64_t any = warp_or64(cand ? (w & (~0ull << col)) : 0ull);
                     cstar = any ? __ffsll(static_cast<long long>(any)) - 1 : 64;
-                    if (outside && cstar != col) {
+                    if (bb + 32 < span) {  // rows past the window may hold an earlier column
                         cmd = 1;
                         lim = cstar;
                         break;
@@ -229,9 +254,12 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
                         cmd = 0;
                         break;
                     }
-                    const unsigned hit = __ballot_sync(FULL, lane >= pr && ((w >> cstar) & 1ull));
-                    ln = __ffs(hit) - 1;
-                    u = __shfl_sync(FULL, w, ln);
+                    hit = __ballot_sync(FULL, cand && ((w >> cstar) & 1ull));
+                }
+                const int ln = __ffs(hit) - 1;
+                const uint64_t u = __shfl_sync(FULL, w, ln);
+                if (ln != pr) {
+                    const uint64_t wp = __shfl_sync(FULL, w, pr);
                     const int usrc = __shfl_sync(FULL, src, ln);
                     const int psrc = __shfl_sync(FULL, src, pr);
                     if (lane == ln) {
@@ -243,13 +271,23 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
                         src = usrc;
                     }
                 }
-                record_pivot(cstar, u, base + bb + ln);
                 const uint64_t us = u & above(cstar);
                 if (lane > pr && ((w >> cstar) & 1ull)) w ^= us;
+                if (lane == 0) {
+                    s_u[t] = us;
+                    s_uf[t] = u;
+                    s_q[t] = cstar;
+                    P[base + p] = base + bb + ln;
+                    Qp[base + p] = wl * 64 + cstar;
+                }
+#ifdef F2_LEAF_PROFILE
+                if (lane == 0 && t < 11) st->dbg[5 + t] = clock64() - c_start;
+#endif
                 ++t;
                 ++p;
                 col = cstar + 1;
             }
+            __syncwarp();
             if (lane == 0) {
                 s_cmd = cmd;
                 s_col = col;

@@ -4,17 +4,18 @@
 // their final leaf words in st->ufull, strict parts in st->ustrict), this kernel
 //   1. finalises the leaf word of every row below the pivots: the elimination
 //      chain of gauss_pls (proj/src/gauss.cpp:47-49) restricted to the leaf word,
-//      which leaves exactly the row's L coefficients at the pivot columns;
+//      which leaves exactly the row's L coefficients at the pivot columns.  The
+//      chain runs 8 pivot columns at a time through 256-entry correction tables
+//      (the corrected-prefix idea of make_table1, proj/src/mmpf.cpp:54-77);
 //   2. solves the pivot rows over the panel columns right of the leaf
 //      (U = L11^{-1} A12, trsm_lower_left_unit, mul.cpp:109-131), 8 pivot columns
 //      at a time;
 //   3. adds into every other row, per 8 coefficient bits, one row of the 256-entry
 //      table of combinations of the solved pivot rows (add_rows_from_table,
-//      m4ri.cpp:28-38, with make_table1's corrected ids, mmpf.cpp:54-77: the
-//      coefficient byte already is the combination, so no id fix-up is needed).
+//      m4ri.cpp:28-38).
 // The table of group g serves both the later pivot rows (step 2) and all other
 // rows (step 3), so each is built once per CTA.  Rows are addressed through pmap
-// (the panel's virtual row order).  Grid: x = 512-bit column tiles of the panel
+// (the panel's virtual row order).  Grid: x = 1024-bit column tiles of the panel
 // remainder (one empty tile when the leaf ends the panel), y = 1024-row tiles.
 #include <cstdint>
 
@@ -26,10 +27,11 @@ namespace f2g {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kRPT = 8;
-constexpr int kTM = (kThreads / 32) * 8 * kRPT;  // 1024 rows per CTA
-constexpr int kTNW = 8;                          // 512-bit column tile
-constexpr size_t kSmem = sizeof(uint64_t) * (64 * kTNW + 2 * 256 * kTNW + 2 * kTM);
+constexpr int kRPT = 16;
+constexpr int kTM = (kThreads / 32) * 4 * kRPT;  // 1024 rows per CTA
+constexpr int kTNW = 16;                         // 1024-bit column tile
+// smem: X[64][kTNW] | T[2][256][kTNW] | F[8][256] | cbuf[kTM] | pbuf[kTM]
+constexpr size_t kSmem = sizeof(uint64_t) * (64 * kTNW + 2 * 256 * kTNW + 8 * 256 + 2 * kTM);
 
 __device__ __forceinline__ uint4 lds128(const void* p) {
     uint4 v;
@@ -45,10 +47,12 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
     __shared__ uint64_t su[64], suf[64];
     __shared__ int sq[64];
     __shared__ int gstart[9];
+    __shared__ int brow8[8];
     extern __shared__ __align__(16) uint64_t dsm[];
     uint64_t* X = dsm;                                        // [64][kTNW]
     uint64_t* Tb = X + 64 * kTNW;                             // [2][256][kTNW]
-    uint64_t* cbuf = Tb + 2 * 256 * kTNW;                     // [kTM]
+    uint64_t* F = Tb + 2 * 256 * kTNW;                        // [8][256] finalize corrections
+    uint64_t* cbuf = F + 8 * 256;                             // [kTM]
     int64_t* pbuf = reinterpret_cast<int64_t*>(cbuf + kTM);   // [kTM]
 
     const int kb = static_cast<int>(st->leaf_kb);
@@ -68,36 +72,50 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
         sq[tid] = st->q[tid];
     }
     __syncthreads();
-
-    // 1. finalise the leaf word of the tile's rows -> coefficient words
-    for (int i = tid; i < nrows; i += kThreads) {
-        const int64_t phys = pmap[row_base + i];
-        uint64_t w = A.w[phys * A.stride + wl];
-        for (int l = 0; l < kb; ++l)
-            if ((w >> sq[l]) & 1ull) w ^= su[l];
-        cbuf[i] = w;
-        pbuf[i] = phys;
-        if (blockIdx.x == 0) A.w[phys * A.stride + wl] = w;
-    }
-    if (ntw == 0) return;
-
-    // pivot rows' slice of the tile, and the 8-column groups of pivots
-    for (int i = tid; i < kb * kTNW; i += kThreads) {
-        const int t = i / kTNW, k = i % kTNW;
-        X[i] = k < ntw ? A.w[pmap[r0 + t] * A.stride + tile_w0 + k] : 0ull;
-    }
     if (tid <= 8) {
         int lo = 0;
         while (lo < kb && sq[lo] < 8 * tid) ++lo;
         gstart[tid] = lo;
     }
     __syncthreads();
+    // finalize tables: F[g][v] = correction that the group-g pivots apply to a word
+    // whose byte g reads v (sequential within the group, as gauss_pls does)
+    for (int i = tid; i < 8 * 256; i += kThreads) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t x = static_cast<uint64_t>(v) << (8 * g), corr = 0;
+        for (int l = gstart[g]; l < gstart[g + 1]; ++l)
+            if ((x >> sq[l]) & 1ull) {
+                x ^= su[l];
+                corr ^= su[l];
+            }
+        F[i] = corr;
+    }
+    __syncthreads();
 
-    const int rq = lane >> 2, wp = lane & 3;
+    // 1. finalise the leaf word of the tile's rows -> coefficient words
+    for (int i = tid; i < nrows; i += kThreads) {
+        const int64_t phys = pmap[row_base + i];
+        uint64_t w = A.w[phys * A.stride + wl];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) w ^= F[g * 256 + ((w >> (8 * g)) & 0xffu)];
+        cbuf[i] = w;
+        pbuf[i] = phys;
+        if (blockIdx.x == 0) A.w[phys * A.stride + wl] = w;
+    }
+    if (ntw == 0) return;
+
+    // pivot rows' slice of the tile
+    for (int i = tid; i < kb * kTNW; i += kThreads) {
+        const int t = i / kTNW, k = i % kTNW;
+        X[i] = k < ntw ? A.w[pmap[r0 + t] * A.stride + tile_w0 + k] : 0ull;
+    }
+    __syncthreads();
+
+    const int rq = lane >> 3, wp = lane & 7;
     uint64_t acc0[kRPT], acc1[kRPT];
 #pragma unroll
     for (int j = 0; j < kRPT; ++j) {
-        const int i = warp * 64 + rq + 8 * j;
+        const int i = warp * 64 + rq + 4 * j;
         acc0[j] = acc1[j] = 0;
         if (i < nrows) {
             const uint64_t* cr = A.w + pbuf[i] * A.stride + tile_w0;
@@ -111,37 +129,68 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
         if (g0 == g1) continue;
         const int sh = 8 * g;
         // (a) pivots inside the group, in registers (one thread per tile word)
-        if (tid < kTNW && g1 - g0 > 1) {
+        if (tid < kTNW) {
             const int k = tid, ng = g1 - g0;
-            uint64_t x[8];
-            int qb[8];
+            if (ng > 1) {
+                uint64_t x[8];
+                int qb[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                x[u] = u < ng ? X[(g0 + u) * kTNW + k] : 0ull;
-                qb[u] = u < ng ? sq[g0 + u] - sh : 8;
-            }
-#pragma unroll
-            for (int u = 1; u < 8; ++u) {
-                if (u < ng) {
-                    const unsigned cb = static_cast<unsigned>(suf[g0 + u] >> sh) & ((1u << qb[u]) - 1u);
-#pragma unroll
-                    for (int l = 0; l < u; ++l)
-                        if ((cb >> qb[l]) & 1u) x[u] ^= x[l];
+                for (int u = 0; u < 8; ++u) {
+                    x[u] = u < ng ? X[(g0 + u) * kTNW + k] : 0ull;
+                    qb[u] = u < ng ? sq[g0 + u] - sh : 8;
                 }
-            }
 #pragma unroll
-            for (int u = 1; u < 8; ++u)
-                if (u < ng) X[(g0 + u) * kTNW + k] = x[u];
+                for (int u = 1; u < 8; ++u) {
+                    if (u < ng) {
+                        const unsigned cb = static_cast<unsigned>(suf[g0 + u] >> sh) & ((1u << qb[u]) - 1u);
+#pragma unroll
+                        for (int l = 0; l < u; ++l)
+                            if ((cb >> qb[l]) & 1u) x[u] ^= x[l];
+                    }
+                }
+#pragma unroll
+                for (int u = 1; u < 8; ++u)
+                    if (u < ng) X[(g0 + u) * kTNW + k] = x[u];
+            }
+        } else if (tid < kTNW + 8) {
+            const int b = tid - kTNW;  // which pivot row sits at raw bit b of the group
+            int r = -1;
+            for (int l = g0; l < g1; ++l)
+                if (sq[l] - sh == b) r = l;
+            brow8[b] = r;
         }
         __syncthreads();
-        // (b) table of the group's solved rows, indexed by the raw coefficient byte
+        // (b) table of the group's solved rows (entry e = xor of rows at set bits of e),
+        //     4 warps, low nibble fixed per thread, high nibble in Gray order
         uint64_t* tb = Tb + (g & 1) * 256 * kTNW;
-        for (int i = tid; i < 256 * kTNW; i += kThreads) {
-            const int e = i / kTNW, k = i % kTNW;
-            uint64_t v = 0;
-            for (int l = g0; l < g1; ++l)
-                if ((e >> (sq[l] - sh)) & 1) v ^= X[l * kTNW + k];
-            tb[i] = v;
+        if (warp < 4) {
+            const int el = tid >> 3;  // 0..15
+            uint64_t v0[8], v1[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int r = brow8[b];
+                v0[b] = r >= 0 ? X[r * kTNW + 2 * wp] : 0ull;
+                v1[b] = r >= 0 ? X[r * kTNW + 2 * wp + 1] : 0ull;
+            }
+            uint64_t l0 = 0, l1 = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if ((el >> b) & 1) {
+                    l0 ^= v0[b];
+                    l1 ^= v1[b];
+                }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k) {
+                    const int b = 4 + ((k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3)));
+                    l0 ^= v0[b];
+                    l1 ^= v1[b];
+                }
+                const int eh = k ^ (k >> 1);
+                uint64_t* e = tb + (eh * 16 + el) * kTNW + 2 * wp;
+                e[0] = l0;
+                e[1] = l1;
+            }
         }
         __syncthreads();
         // (c) later pivot rows and all other rows add one table row each
@@ -151,8 +200,8 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
         }
 #pragma unroll
         for (int j = 0; j < kRPT; ++j) {
-            const int i = warp * 64 + rq + 8 * j;
-            const unsigned idx = static_cast<unsigned>(cbuf[i < kTM ? i : 0] >> sh) & 0xffu;
+            const int i = warp * 64 + rq + 4 * j;
+            const unsigned idx = static_cast<unsigned>(cbuf[i] >> sh) & 0xffu;
             const uint4 v = lds128(tb + idx * kTNW + 2 * wp);
             acc0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
             acc1[j] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
@@ -162,7 +211,7 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
 
 #pragma unroll
     for (int j = 0; j < kRPT; ++j) {
-        const int i = warp * 64 + rq + 8 * j;
+        const int i = warp * 64 + rq + 4 * j;
         if (i < nrows) {
             uint64_t* cr = A.w + pbuf[i] * A.stride + tile_w0;
             if (2 * wp < ntw) cr[2 * wp] = acc0[j];
