@@ -27,8 +27,8 @@ namespace f2g {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kRPT = 16;
-constexpr int kTM = (kThreads / 32) * 4 * kRPT;  // 1024 rows per CTA
+constexpr int kRPT = 4;
+constexpr int kTM = (kThreads / 32) * 4 * kRPT;  // 256 rows per CTA (fills all SMs at m = 64K)
 constexpr int kTNW = 16;                         // 1024-bit column tile
 // smem: X[64][kTNW] | T[2][256][kTNW] | F[8][256] | cbuf[kTM] | pbuf[kTM]
 constexpr size_t kSmem = sizeof(uint64_t) * (64 * kTNW + 2 * 256 * kTNW + 8 * 256 + 2 * kTM);
@@ -42,7 +42,7 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, const PlsState* st) {
     __shared__ uint64_t su[64], suf[64];
     __shared__ int sq[64];
@@ -115,7 +115,7 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
     uint64_t acc0[kRPT], acc1[kRPT];
 #pragma unroll
     for (int j = 0; j < kRPT; ++j) {
-        const int i = warp * 64 + rq + 4 * j;
+        const int i = warp * 4 * kRPT + rq + 4 * j;
         acc0[j] = acc1[j] = 0;
         if (i < nrows) {
             const uint64_t* cr = A.w + pbuf[i] * A.stride + tile_w0;
@@ -200,7 +200,7 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
         }
 #pragma unroll
         for (int j = 0; j < kRPT; ++j) {
-            const int i = warp * 64 + rq + 4 * j;
+            const int i = warp * 4 * kRPT + rq + 4 * j;
             const unsigned idx = static_cast<unsigned>(cbuf[i] >> sh) & 0xffu;
             const uint4 v = lds128(tb + idx * kTNW + 2 * wp);
             acc0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
@@ -211,7 +211,7 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
 
 #pragma unroll
     for (int j = 0; j < kRPT; ++j) {
-        const int i = warp * 64 + rq + 4 * j;
+        const int i = warp * 4 * kRPT + rq + 4 * j;
         if (i < nrows) {
             uint64_t* cr = A.w + pbuf[i] * A.stride + tile_w0;
             if (2 * wp < ntw) cr[2 * wp] = acc0[j];

@@ -20,7 +20,7 @@ namespace f2g {
 
 namespace {
 
-constexpr int kTW = 4;           // target words per CTA
+constexpr int kTW = 8;           // target words per CTA
 constexpr int kMaxRows = kMaxPanelBits;
 
 struct TrsmCtx {
@@ -33,7 +33,7 @@ struct TrsmCtx {
 __global__ void __launch_bounds__(256)
 k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, const PlsState* st,
              PivotSet ps, Mat L) {
-    extern __shared__ uint64_t smem[];
+    extern __shared__ __align__(16) uint64_t smem[];
     uint64_t* X = smem;                          // [kMaxRows][kTW]
     uint64_t* T = X + kMaxRows * kTW;            // [256][kTW]
     uint64_t* cw = T + 256 * kTW;                // [kMaxRows] coefficient word of the current 8 groups
@@ -115,18 +115,45 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
         }
         if (t1 >= nk) break;
         __syncthreads();
-        for (int i = tid; i < 256 * kTW; i += nth) {
-            const int e = i / kTW, j = i % kTW;
-            uint64_t v = 0;
-            for (int l = t0; l < t1; ++l)
-                if ((e >> (sq[l] - base)) & 1) v ^= X[l * kTW + j];
-            T[i] = v;
+        // table of the group's solved rows: thread = (target word j, low nibble el),
+        // high nibble walked in Gray order (one XOR per entry)
+        if (tid < kTW * 16) {
+            const int j = tid % kTW, el = tid / kTW;
+            uint64_t v[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) v[b] = 0;
+            for (int l = t0; l < t1; ++l) {
+                const int b = sq[l] - base;
+#pragma unroll
+                for (int bb = 0; bb < 8; ++bb)
+                    if (bb == b) v[bb] = X[l * kTW + j];
+            }
+            uint64_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if ((el >> b) & 1) x ^= v[b];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k) x ^= v[4 + ((k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3)))];
+                const int eh = k ^ (k >> 1);
+                T[(eh * 16 + el) * kTW + j] = x;
+            }
         }
         __syncthreads();
-        for (int i = tid; i < (nk - t1) * kTW; i += nth) {
-            const int t = t1 + i / kTW, j = i % kTW;
+        for (int t = t1 + tid; t < nk; t += nth) {
             const unsigned cb = static_cast<unsigned>(cw[t] >> sh) & 0xffu;
-            X[t * kTW + j] ^= T[cb * kTW + j];
+            uint4* xr = reinterpret_cast<uint4*>(X + t * kTW);
+            const uint4* tr = reinterpret_cast<const uint4*>(T + cb * kTW);
+#pragma unroll
+            for (int j = 0; j < kTW / 2; ++j) {
+                uint4 a = xr[j];
+                const uint4 b = tr[j];
+                a.x ^= b.x;
+                a.y ^= b.y;
+                a.z ^= b.z;
+                a.w ^= b.w;
+                xr[j] = a;
+            }
         }
     }
     __syncthreads();
