@@ -129,6 +129,9 @@ int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int
 int f2_stats_enable(int enable);
 int f2_stats_get(int kind, uint64_t* launches, double* ms, double* bytes, double* bitops);
 int f2_stats_reset(void);
+/* CUDA-event timer on the library's stream (start/stop bracket device work) */
+int f2_timer_start(void);
+int f2_timer_stop(double* ms);
 /* kernel launches issued by the last compute call (all families) */
 uint64_t f2_last_launch_count(void);
 /* phase clocks of the last leaf (only builds compiled with -DF2_LEAF_PROFILE fill them) */

@@ -38,6 +38,7 @@ __all__ = [
     "mmpf_pls_host", "pls_recursive_host", "addmul", "mul_m4rm", "trsm_lower_left_unit", "compress_columns",
     "apply_rows", "default_cutoff_bytes", "auto_table_bits", "NoDeviceError", "F2Error", "host_words",
     "pinned_empty", "stats_enable", "stats_get", "stats_reset", "last_launch_count", "set_panel_bits",
+    "timer_start", "timer_stop", "set_device",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -111,6 +112,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_stats_reset": ([], i),
         "f2_last_launch_count": ([], C.c_uint64),
         "f2_set_panel_bits": ([C.c_uint], i),
+        "f2_timer_start": ([], i),
+        "f2_timer_stop": ([C.POINTER(C.c_double)], i),
+        "f2_debug_clocks": ([C.POINTER(C.c_longlong), i], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -389,6 +393,22 @@ def stats_get(kind: int) -> dict:
 
 def last_launch_count() -> int:
     return int(load_library().f2_last_launch_count())
+
+
+def timer_start() -> None:
+    """Record a CUDA event on the library's stream."""
+    _check(load_library().f2_timer_start())
+
+
+def timer_stop() -> float:
+    """Record a second event, wait for it, return device milliseconds since timer_start()."""
+    ms = C.c_double()
+    _check(load_library().f2_timer_stop(C.byref(ms)))
+    return ms.value
+
+
+def set_device(device: int) -> None:
+    _check(load_library().f2_set_device(device))
 
 
 def set_panel_bits(bits: int) -> None:

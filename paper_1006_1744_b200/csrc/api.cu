@@ -625,11 +625,26 @@ int f2_pls_recursive(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64
     return F2_OK;
 }
 
+// Host-buffer entry points keep one cached device matrix per shape, so a caller
+// that decomposes many host matrices pays for the transfers, not for allocation.
+static f2_matrix* g_host_mat = nullptr;
+
 static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
                     uint64_t* q, const f2_elim_config* cfg, unsigned k, uint64_t* rank) {
-    f2_matrix* a = nullptr;
-    int rc = f2_matrix_create(nrows, ncols, &a);
-    if (rc) return rc;
+    int rc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if ((rc = ensure_init())) return rc;
+        if (!g_host_mat || g_host_mat->m != nrows || g_host_mat->n != ncols) {
+            if (g_host_mat) {
+                cudaFree(g_host_mat->d);
+                delete g_host_mat;
+                g_host_mat = nullptr;
+            }
+            if ((rc = alloc_matrix(nrows, ncols, &g_host_mat))) return rc;
+        }
+    }
+    f2_matrix* a = g_host_mat;
     rc = f2_matrix_upload(a, words, stride_words);
     if (!rc) {
         f2_window w{0, 0, nrows, ncols};
@@ -637,7 +652,6 @@ static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols,
                        : f2_mmpf_pls(a, w, p, nrows, q, ncols, k, rank);
     }
     if (!rc) rc = f2_matrix_download(a, words, stride_words);
-    f2_matrix_destroy(a);
     return rc;
 }
 
@@ -674,6 +688,30 @@ int f2_stats_reset(void) {
 }
 
 uint64_t f2_last_launch_count(void) { return g.launches; }
+
+// device timer on the library's stream (bench.py: CUDA events, not host clocks)
+static cudaEvent_t g_t0 = nullptr, g_t1 = nullptr;
+int f2_timer_start(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (!g_t0) {
+        CK(cudaEventCreate(&g_t0));
+        CK(cudaEventCreate(&g_t1));
+    }
+    CK(cudaEventRecord(g_t0, g.stream));
+    return F2_OK;
+}
+int f2_timer_stop(double* ms) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_t0 || !ms) return fail(F2_INVALID_ARGUMENT, "timer not started");
+    CK(cudaEventRecord(g_t1, g.stream));
+    CK(cudaEventSynchronize(g_t1));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, g_t0, g_t1));
+    *ms = f;
+    return F2_OK;
+}
 
 // phase clocks recorded by builds compiled with -DF2_LEAF_PROFILE (development aid)
 int f2_debug_clocks(long long* out, int n) {
@@ -733,7 +771,11 @@ void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0
     ta.brow = nullptr;
     ta.row_mode = ROWS_STATIC;
     ta.st = nullptr;
-    LaunchTimer t(0, 0.0, 2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
+    // algorithmic HBM bytes: C read + written, the coefficient words of every row, the B rows
+    const double cbytes = 8.0 * static_cast<double>((q + 63) / 64);
+    const double abytes = 8.0 * static_cast<double>((s + 63) / 64);
+    LaunchTimer t(0, static_cast<double>(p) * (2.0 * cbytes + abytes) + static_cast<double>(s) * cbytes,
+                  2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
     launch_table_apply(g.stream, ta, g.nsm);
 }
 
