@@ -559,8 +559,8 @@ unsigned f2_auto_table_bits(size_t dim) {
 
 int f2_set_panel_bits(unsigned bits) {
     if (bits == 0) bits = 1024;
-    if (bits % 64 || bits > static_cast<unsigned>(kMaxPanelBits))
-        return fail(F2_INVALID_ARGUMENT, "panel bits must be a multiple of 64 and <= 2048");
+    if (bits % 64 || bits > 1024)
+        return fail(F2_INVALID_ARGUMENT, "panel bits must be a multiple of 64 and <= 1024");
     g.panel_bits = bits;
     return F2_OK;
 }
@@ -716,9 +716,9 @@ int f2_timer_stop(double* ms) {
 // phase clocks recorded by builds compiled with -DF2_LEAF_PROFILE (development aid)
 int f2_debug_clocks(long long* out, int n) {
     if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
-    long long tmp[16];
+    long long tmp[32];
     CK(cudaMemcpy(tmp, &g.st->dbg[0], sizeof(tmp), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n && i < 16; ++i) out[i] = tmp[i];
+    for (int i = 0; i < n && i < 32; ++i) out[i] = tmp[i];
     return F2_OK;
 }
 
@@ -783,7 +783,7 @@ void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0
 void trsm_rec(const Mat& Lm, const Mat& Bm, int64_t o, int64_t r) {
     if (r <= 1) return;
     const int64_t nwb = (Bm.n + 63) / 64;
-    if (r <= kMaxPanelBits) {
+    if (r <= 1024) {
         Mat lsub{Lm.w + o * Lm.stride + o / 64, r, r, Lm.stride};
         LaunchTimer t(2, 0, 0);
         launch_pivot_trsm(g.stream, Bm, 0, static_cast<int>((r + 63) / 64), 0, nwb, nullptr, PivotSet{2, o, r}, &lsub);

@@ -47,7 +47,7 @@ struct PlsState {
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
     int64_t moved[kMaxMoved];           // positions with pmap[x] != x (may repeat)
-    long long dbg[16];                  // phase clocks (F2_LEAF_PROFILE builds only)
+    long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)
 };
 
 // How a table-apply launch finds its C/A rows (device-side offsets).

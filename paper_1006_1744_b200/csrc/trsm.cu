@@ -7,10 +7,16 @@
 // pivot l sits at the pivot's raw column q_l of its coefficient words, which
 // is how the packed layout stores L before compress_columns (gauss.cpp:47-53).
 //
-// Blocking: each CTA owns TW target words of all kb rows in SMEM and walks the
-// raw columns 8 at a time.  For each group it solves the (<= 8) pivots inside
-// the group, builds the 256-entry Gray table of their combinations, and adds
-// one table row into every later pivot row (one lookup per row per group).
+// Blocking: each CTA owns kTW target words of all kb rows in SMEM and walks the
+// raw columns 8 at a time (group g).  The group's <= 8 pivots sit at raw bit
+// positions sb_l = q_l - 8g of the coefficient byte.  With R = rows of the
+// group's inverse 8x8 L block (R_l = e_l ^ xor_{l'<l, c_l bit} R_l'), a table T
+// over the group rows' *current* values and M(e) = xor_{b in e} R[b], every row
+// t >= t0 of the group and after it becomes X_t ^= T[M(c_t)], c_t its coefficient
+// byte (masked below its own pivot for the group's rows).  The M maps depend only
+// on the pivot rows' coefficients, which this kernel never modifies, so all of
+// them are prepared up front in parallel; each group then costs one table build
+// and one lookup pass (two barriers) and no serial in-group solve.
 #include <cstdint>
 
 #include "f2gpu.cuh"
@@ -20,25 +26,25 @@ namespace f2g {
 
 namespace {
 
-constexpr int kTW = 8;           // target words per CTA
-constexpr int kMaxRows = kMaxPanelBits;
-
-struct TrsmCtx {
-    int64_t kb, r0;
-    const int32_t* q;  // nullptr => identity pivots
-};
+constexpr int kTW = 8;                 // target words per CTA
+constexpr int kMaxTrsmBits = 1024;     // pivots per solve (the host never passes more)
+constexpr int kThreads = 512;
+constexpr int kCwPer = kMaxTrsmBits / kThreads;  // coefficient rows staged per thread
 
 }  // namespace
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kThreads)
 k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, const PlsState* st,
              PivotSet ps, Mat L) {
     extern __shared__ __align__(16) uint64_t smem[];
-    uint64_t* X = smem;                          // [kMaxRows][kTW]
-    uint64_t* T = X + kMaxRows * kTW;            // [256][kTW]
-    uint64_t* cw = T + 256 * kTW;                // [kMaxRows] coefficient word of the current 8 groups
-    int32_t* sq = reinterpret_cast<int32_t*>(cw + kMaxRows);  // [kMaxRows]
-    int32_t* gstart = sq + kMaxRows;             // [kMaxPanelBits/8 + 1]
+    const int rows_cap = coef_words * 64, ngroups = coef_words * 8;
+    uint64_t* X = smem;                                                   // [rows_cap][kTW]
+    uint64_t* T = X + rows_cap * kTW;                                     // [256][kTW]
+    uint64_t* cw = T + 256 * kTW;                                         // [rows_cap] current coefficient word
+    int32_t* sq = reinterpret_cast<int32_t*>(cw + rows_cap);              // [rows_cap]
+    int32_t* gstart = sq + rows_cap;                                      // [ngroups + 1]
+    int16_t* posrow = reinterpret_cast<int16_t*>(gstart + ngroups + 8);   // [ngroups][8]
+    uint8_t* Mall = reinterpret_cast<uint8_t*>(posrow + ngroups * 8);     // [ngroups][256]
 
     int64_t kb, r0;
     const int32_t* qsrc = nullptr;
@@ -61,110 +67,142 @@ k_pivot_trsm(Mat A, int64_t coef_w0, int coef_words, int64_t tw0, int64_t tw1, c
     const int tid = threadIdx.x, nth = blockDim.x;
     const int nk = static_cast<int>(kb);
 
+    auto coef_word = [&](int t, int wi) -> uint64_t {
+        return ps.mode == 2 ? L.w[static_cast<int64_t>(t) * L.stride + wi] : A.w[(r0 + t) * A.stride + coef_w0 + wi];
+    };
+
     for (int t = tid; t < nk; t += nth) sq[t] = qsrc ? qsrc[t] : t;
-    for (int i = tid; i < nk * kTW; i += nth) {
-        int t = i / kTW, j = i % kTW;
-        X[i] = j < ntw ? A.w[(r0 + t) * A.stride + tb + j] : 0ull;
+    for (int i0 = tid; i0 < nk * kTW; i0 += 4 * nth) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * nth, t = i / kTW, j = i % kTW;
+            v[u] = (i < nk * kTW && j < ntw) ? A.w[(r0 + t) * A.stride + tb + j] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * nth < nk * kTW) X[i0 + u * nth] = v[u];
     }
+    for (int i = tid; i < ngroups * 8; i += nth) posrow[i] = -1;
     __syncthreads();
-    const int ngroups = coef_words * 8;
     for (int g = tid; g <= ngroups; g += nth) {
         int lo = 0, hi = nk;  // first t with sq[t] >= 8g
         while (lo < hi) {
-            int mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (sq[mid] < 8 * g) lo = mid + 1;
             else hi = mid;
         }
         gstart[g] = lo;
     }
+    for (int t = tid; t < nk; t += nth) posrow[(sq[t] >> 3) * 8 + (sq[t] & 7)] = static_cast<int16_t>(t);
+    __syncthreads();
+    // index maps M of every group
+    for (int i = tid; i < ngroups * 256; i += nth) {
+        const int g = i >> 8, e = i & 255;
+        const int t0 = gstart[g], t1 = gstart[g + 1];
+        uint32_t Mv = 0;
+        if (t1 > t0) {
+            uint32_t Rb[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) Rb[b] = 0;
+            const int sh = 8 * (g & 7), base = 8 * g;
+            for (int l = t0; l < t1; ++l) {
+                const int sb = sq[l] - base;
+                const uint32_t c = static_cast<uint32_t>(coef_word(l, g >> 3) >> sh) & ((1u << sb) - 1u);
+                uint32_t R = 1u << sb;
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    if ((c >> b) & 1u) R ^= Rb[b];
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    if (b == sb) Rb[b] = R;
+            }
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                if ((e >> b) & 1) Mv ^= Rb[b];
+        }
+        Mall[i] = static_cast<uint8_t>(Mv);
+    }
+    uint64_t cwn[kCwPer];
+#pragma unroll
+    for (int u = 0; u < kCwPer; ++u) {
+        const int t = tid + u * nth;
+        cwn[u] = t < nk ? coef_word(t, 0) : 0ull;
+    }
 
+    const int lane = tid & 31, wq = lane & 3, rq = lane >> 2, wrp = tid >> 5;
     for (int g = 0; g < ngroups; ++g) {
         if ((g & 7) == 0) {
-            // stage coefficient word g/8 of every pivot row
+            // coefficient word g/8 of every pivot row (prefetched one word ahead)
             __syncthreads();
-            for (int t = tid; t < nk; t += nth)
-                cw[t] = ps.mode == 2 ? L.w[static_cast<int64_t>(t) * L.stride + (g >> 3)]
-                                     : A.w[(r0 + t) * A.stride + coef_w0 + (g >> 3)];
+#pragma unroll
+            for (int u = 0; u < kCwPer; ++u) {
+                const int t = tid + u * nth;
+                if (t < nk) cw[t] = cwn[u];
+            }
+            const int wn = (g >> 3) + 1;
+            if (wn < coef_words) {
+#pragma unroll
+                for (int u = 0; u < kCwPer; ++u) {
+                    const int t = tid + u * nth;
+                    if (t < nk) cwn[u] = coef_word(t, wn);
+                }
+            }
         }
         __syncthreads();
         const int t0 = gstart[g], t1 = gstart[g + 1];
         if (t0 == t1) continue;
         const int sh = 8 * (g & 7), base = 8 * g;
-        if (t1 - t0 > 1 && tid < kTW) {
-            // in-group forward substitution, rows held in registers
-            const int j = tid, ng = t1 - t0;
-            uint64_t x[8];
-            int qb[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                x[u] = u < ng ? X[(t0 + u) * kTW + j] : 0ull;
-                qb[u] = u < ng ? sq[t0 + u] - base : 8;
-            }
-#pragma unroll
-            for (int u = 1; u < 8; ++u) {
-                if (u < ng) {
-                    const unsigned cb = static_cast<unsigned>(cw[t0 + u] >> sh) & 0xffu;
-#pragma unroll
-                    for (int l = 0; l < u; ++l)
-                        if ((cb >> qb[l]) & 1u) x[u] ^= x[l];
-                }
-            }
-#pragma unroll
-            for (int u = 1; u < 8; ++u)
-                if (u < ng) X[(t0 + u) * kTW + j] = x[u];
-        }
-        if (t1 >= nk) break;
-        __syncthreads();
-        // table of the group's solved rows: thread = (target word j, low nibble el),
-        // high nibble walked in Gray order (one XOR per entry)
-        if (tid < kTW * 16) {
-            const int j = tid % kTW, el = tid / kTW;
+        const uint8_t* Mg = Mall + g * 256;
+        // table over the group rows' current values: thread = (word j, 4 entries)
+        {
+            const int j = tid % kTW;
+            const int16_t* pr = posrow + g * 8;
             uint64_t v[8];
 #pragma unroll
-            for (int b = 0; b < 8; ++b) v[b] = 0;
-            for (int l = t0; l < t1; ++l) {
-                const int b = sq[l] - base;
-#pragma unroll
-                for (int bb = 0; bb < 8; ++bb)
-                    if (bb == b) v[bb] = X[l * kTW + j];
+            for (int b = 0; b < 8; ++b) {
+                const int l = pr[b];
+                v[b] = l >= 0 ? X[l * kTW + j] : 0ull;
             }
-            uint64_t x = 0;
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((el >> b) & 1) x ^= v[b];
+            for (int u = 0; u < 4; ++u) {
+                const int e = tid / kTW + 64 * u;
+                uint64_t x = 0;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (k) x ^= v[4 + ((k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3)))];
-                const int eh = k ^ (k >> 1);
-                T[(eh * 16 + el) * kTW + j] = x;
+                for (int b = 0; b < 8; ++b)
+                    if ((e >> b) & 1) x ^= v[b];
+                T[e * kTW + j] = x;
             }
         }
         __syncthreads();
-        for (int t = t1 + tid; t < nk; t += nth) {
-            const unsigned cb = static_cast<unsigned>(cw[t] >> sh) & 0xffu;
-            uint4* xr = reinterpret_cast<uint4*>(X + t * kTW);
-            const uint4* tr = reinterpret_cast<const uint4*>(T + cb * kTW);
-#pragma unroll
-            for (int j = 0; j < kTW / 2; ++j) {
-                uint4 a = xr[j];
-                const uint4 b = tr[j];
-                a.x ^= b.x;
-                a.y ^= b.y;
-                a.z ^= b.z;
-                a.w ^= b.w;
-                xr[j] = a;
-            }
+        // rows >= t0: 4 lanes per row (16 B each), 8 rows per warp instruction, so the
+        // X accesses are contiguous 512-B runs (conflict-free)
+#pragma unroll 4
+        for (int t = t0 + wrp * 8 + rq; t < nk; t += (nth / 32) * 8) {
+            uint32_t cb = static_cast<uint32_t>(cw[t] >> sh) & 0xffu;
+            if (t < t1) cb &= (1u << (sq[t] - base)) - 1u;
+            const uint32_t idx = Mg[cb];
+            uint4* xr = reinterpret_cast<uint4*>(X + t * kTW) + wq;
+            const uint4 b = *(reinterpret_cast<const uint4*>(T + idx * kTW) + wq);
+            uint4 a = *xr;
+            a.x ^= b.x;
+            a.y ^= b.y;
+            a.z ^= b.z;
+            a.w ^= b.w;
+            *xr = a;
         }
     }
     __syncthreads();
     for (int i = tid; i < nk * kTW; i += nth) {
-        int t = i / kTW, j = i % kTW;
+        const int t = i / kTW, j = i % kTW;
         if (j < ntw) A.w[(r0 + t) * A.stride + tb + j] = X[i];
     }
 }
 
-static size_t trsm_smem() {
-    return sizeof(uint64_t) * (kMaxRows * kTW + 256 * kTW + kMaxRows) + sizeof(int32_t) * (kMaxRows + kMaxPanelBits / 8 + 8);
+static size_t trsm_smem(int coef_words) {
+    const size_t rows = static_cast<size_t>(coef_words) * 64, groups = static_cast<size_t>(coef_words) * 8;
+    return sizeof(uint64_t) * (rows * kTW + 256 * kTW + rows) + sizeof(int32_t) * (rows + groups + 8) +
+           sizeof(int16_t) * groups * 8 + 256 * groups;
 }
 
 void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_words, int64_t tw0,
@@ -172,11 +210,12 @@ void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_w
     if (tw1 <= tw0) return;
     const int grid = static_cast<int>((tw1 - tw0 + kTW - 1) / kTW);
     Mat l = L ? *L : Mat{nullptr, 0, 0, 0};
-    k_pivot_trsm<<<grid, 256, trsm_smem(), s>>>(A, coef_w0, coef_words, tw0, tw1, st, ps, l);
+    k_pivot_trsm<<<grid, kThreads, trsm_smem(coef_words), s>>>(A, coef_w0, coef_words, tw0, tw1, st, ps, l);
 }
 
 void setup_trsm_kernels() {
-    cudaFuncSetAttribute(k_pivot_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trsm_smem()));
+    cudaFuncSetAttribute(k_pivot_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(trsm_smem(kMaxTrsmBits / 64)));
 }
 
 }  // namespace f2g

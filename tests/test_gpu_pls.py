@@ -67,7 +67,7 @@ def test_golden_small_cases_mmpf_and_recursive(f2, small_cases):
         assert (d.download() == c["rc_w"]).all() and (res.P == c["rc_p"]).all() and (res.Q == c["rc_q"]).all()
 
 
-@pytest.mark.parametrize("panel", [64, 128, 1024, 2048])
+@pytest.mark.parametrize("panel", [64, 128, 512, 1024])
 def test_random_shapes_all_panels(f2, oracle, panel):
     rng = np.random.default_rng(panel)
     for t in range(25):
