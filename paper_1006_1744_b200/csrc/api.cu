@@ -275,6 +275,10 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             }
             {
                 LaunchTimer t(3, 0, 0);
+                launch_leaf_tables(s, g.st);
+            }
+            {
+                LaunchTimer t(3, 0, 0);
                 launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
             }
         }

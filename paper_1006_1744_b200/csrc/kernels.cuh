@@ -12,6 +12,7 @@ void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int fir
                        int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap);
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch);
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
+void launch_leaf_tables(cudaStream_t s, PlsState* st);
 void setup_leaf_kernels();
 
 // leafupd.cu — one leaf's update of its panel (virtual row order via pmap):

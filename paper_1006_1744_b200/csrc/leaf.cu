@@ -458,6 +458,64 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
     }
 }
 
+// Per 8-column group of the leaf word: the finalize table F[g][v] (correction the
+// group's pivots apply to a word whose byte g reads v, sequentially as gauss_pls
+// does) and the index map M[g][e] = xor_{b in e} R[b], R the rows of the group's
+// inverse 8x8 L block (see trsm.cu).  k_leaf_update consumes both.  One thread per
+// table entry (16 CTAs x 256).
+__global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st) {
+    __shared__ uint64_t s_u[64], s_uf[64];
+    __shared__ int s_q[64];
+    __shared__ int s_gs[9];
+    const int tid = threadIdx.x;
+    const int kb = static_cast<int>(st->leaf_kb);
+    if (kb == 0) return;
+    if (tid < 64) {
+        s_u[tid] = st->ustrict[tid];
+        s_uf[tid] = st->ufull[tid];
+        s_q[tid] = st->q[tid];
+    }
+    __syncthreads();
+    if (tid <= 8) {
+        int lo = 0;
+        while (lo < kb && s_q[lo] < 8 * tid) ++lo;
+        s_gs[tid] = lo;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * 256 + tid;
+    const int which = i >> 11, g = (i >> 8) & 7, v = i & 255;
+    const int g0 = s_gs[g], g1 = s_gs[g + 1];
+    if (which == 0) {
+        uint64_t x = static_cast<uint64_t>(v) << (8 * g), corr = 0;
+        for (int l = g0; l < g1; ++l)
+            if ((x >> s_q[l]) & 1ull) {
+                x ^= s_u[l];
+                corr ^= s_u[l];
+            }
+        st->leaf_F[g][v] = corr;
+    } else {
+        uint32_t Rb[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) Rb[b] = 0;
+        for (int l = g0; l < g1; ++l) {
+            const int sb = s_q[l] - 8 * g;
+            const uint32_t c = static_cast<uint32_t>(s_uf[l] >> (8 * g)) & ((1u << sb) - 1u);
+            uint32_t R = 1u << sb;
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                if ((c >> b) & 1u) R ^= Rb[b];
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                if (b == sb) Rb[b] = R;
+        }
+        uint32_t Mv = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if ((v >> b) & 1) Mv ^= Rb[b];
+        st->leaf_M[g][v] = static_cast<uint8_t>(Mv);
+    }
+}
+
 // Panel end, step 1: copy the rows that the panel's positions now refer to
 // (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
 __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
@@ -498,6 +556,8 @@ void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* s
     k_perm_save<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
     k_perm_put<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
 }
+
+void launch_leaf_tables(cudaStream_t s, PlsState* st) { k_leaf_tables<<<16, 256, 0, s>>>(st); }
 
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {
     int64_t g = (m + 255) / 256;

@@ -6,7 +6,8 @@
 //      chain of gauss_pls (proj/src/gauss.cpp:47-49) restricted to the leaf word,
 //      which leaves exactly the row's L coefficients at the pivot columns.  The
 //      chain runs 8 pivot columns at a time through 256-entry correction tables
-//      (the corrected-prefix idea of make_table1, proj/src/mmpf.cpp:54-77);
+//      (the corrected-prefix idea of make_table1, proj/src/mmpf.cpp:54-77) that
+//      k_leaf_pivot prepares once per leaf;
 //   2. solves the pivot rows over the panel columns right of the leaf
 //      (U = L11^{-1} A12, trsm_lower_left_unit, mul.cpp:109-131), 8 pivot columns
 //      at a time;
@@ -44,10 +45,11 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 
 __global__ void __launch_bounds__(kThreads, 2)
 k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, const PlsState* st) {
-    __shared__ uint64_t su[64], suf[64];
+    __shared__ uint64_t suf[64];
     __shared__ int sq[64];
     __shared__ int gstart[9];
-    __shared__ int brow8[8];
+    __shared__ int16_t posrow[64];
+    __shared__ uint8_t Ms[8 * 256];
     extern __shared__ __align__(16) uint64_t dsm[];
     uint64_t* X = dsm;                                        // [64][kTNW]
     uint64_t* Tb = X + 64 * kTNW;                             // [2][256][kTNW]
@@ -66,31 +68,22 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
     const int ntw = tile_w0 >= rw1 ? 0 : static_cast<int>(rw1 - tile_w0 < kTNW ? rw1 - tile_w0 : kTNW);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    // tables prepared by k_leaf_pivot (depend only on the leaf's pivots)
+    for (int i = tid; i < 8 * 256; i += kThreads) F[i] = (&st->leaf_F[0][0])[i];
+    for (int i = tid; i < 8 * 256 / 4; i += kThreads)
+        reinterpret_cast<uint32_t*>(Ms)[i] = reinterpret_cast<const uint32_t*>(&st->leaf_M[0][0])[i];
     if (tid < 64) {
-        su[tid] = st->ustrict[tid];
         suf[tid] = st->ufull[tid];
         sq[tid] = st->q[tid];
+        posrow[tid] = -1;
     }
     __syncthreads();
+    if (tid < kb) posrow[sq[tid]] = static_cast<int16_t>(tid);
     if (tid <= 8) {
         int lo = 0;
         while (lo < kb && sq[lo] < 8 * tid) ++lo;
         gstart[tid] = lo;
     }
-    __syncthreads();
-    // finalize tables: F[g][v] = correction that the group-g pivots apply to a word
-    // whose byte g reads v (sequential within the group, as gauss_pls does)
-    for (int i = tid; i < 8 * 256; i += kThreads) {
-        const int g = i >> 8, v = i & 255;
-        uint64_t x = static_cast<uint64_t>(v) << (8 * g), corr = 0;
-        for (int l = gstart[g]; l < gstart[g + 1]; ++l)
-            if ((x >> sq[l]) & 1ull) {
-                x ^= su[l];
-                corr ^= su[l];
-            }
-        F[i] = corr;
-    }
-    __syncthreads();
 
     // 1. finalise the leaf word of the tile's rows -> coefficient words
     for (int i = tid; i < nrows; i += kThreads) {
@@ -124,51 +117,23 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
         }
     }
 
+    // 2./3. per group of 8 leaf columns: a table T over the group's pivot rows as they
+    // are now; the group's pivot rows and every later row add T[M(c)] (c = the row's
+    // coefficient byte, masked below its own pivot for the group's rows), which
+    // equals adding the combination of the *solved* group rows (see trsm.cu)
     for (int g = 0; g < 8; ++g) {
         const int g0 = gstart[g], g1 = gstart[g + 1];
         if (g0 == g1) continue;
         const int sh = 8 * g;
-        // (a) pivots inside the group, in registers (one thread per tile word)
-        if (tid < kTNW) {
-            const int k = tid, ng = g1 - g0;
-            if (ng > 1) {
-                uint64_t x[8];
-                int qb[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    x[u] = u < ng ? X[(g0 + u) * kTNW + k] : 0ull;
-                    qb[u] = u < ng ? sq[g0 + u] - sh : 8;
-                }
-#pragma unroll
-                for (int u = 1; u < 8; ++u) {
-                    if (u < ng) {
-                        const unsigned cb = static_cast<unsigned>(suf[g0 + u] >> sh) & ((1u << qb[u]) - 1u);
-#pragma unroll
-                        for (int l = 0; l < u; ++l)
-                            if ((cb >> qb[l]) & 1u) x[u] ^= x[l];
-                    }
-                }
-#pragma unroll
-                for (int u = 1; u < 8; ++u)
-                    if (u < ng) X[(g0 + u) * kTNW + k] = x[u];
-            }
-        } else if (tid < kTNW + 8) {
-            const int b = tid - kTNW;  // which pivot row sits at raw bit b of the group
-            int r = -1;
-            for (int l = g0; l < g1; ++l)
-                if (sq[l] - sh == b) r = l;
-            brow8[b] = r;
-        }
-        __syncthreads();
-        // (b) table of the group's solved rows (entry e = xor of rows at set bits of e),
-        //     4 warps, low nibble fixed per thread, high nibble in Gray order
+        const uint8_t* Mg = Ms + g * 256;
         uint64_t* tb = Tb + (g & 1) * 256 * kTNW;
+        // table: 4 warps, thread = (16-byte column chunk wp, low nibble el), Gray walk
         if (warp < 4) {
             const int el = tid >> 3;  // 0..15
             uint64_t v0[8], v1[8];
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const int r = brow8[b];
+                const int r = posrow[sh + b];
                 v0[b] = r >= 0 ? X[r * kTNW + 2 * wp] : 0ull;
                 v1[b] = r >= 0 ? X[r * kTNW + 2 * wp + 1] : 0ull;
             }
@@ -193,15 +158,16 @@ k_leaf_update(Mat A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap, 
             }
         }
         __syncthreads();
-        // (c) later pivot rows and all other rows add one table row each
-        for (int i = tid; i < (kb - g1) * kTNW; i += kThreads) {
-            const int t = g1 + i / kTNW, k = i % kTNW;
-            X[t * kTNW + k] ^= tb[((suf[t] >> sh) & 0xffu) * kTNW + k];
+        for (int i = tid; i < (kb - g0) * kTNW; i += kThreads) {
+            const int t = g0 + i / kTNW, k = i % kTNW;
+            uint32_t cb = static_cast<uint32_t>(suf[t] >> sh) & 0xffu;
+            if (t < g1) cb &= (1u << (sq[t] - sh)) - 1u;
+            X[t * kTNW + k] ^= tb[Mg[cb] * kTNW + k];
         }
 #pragma unroll
         for (int j = 0; j < kRPT; ++j) {
             const int i = warp * 4 * kRPT + rq + 4 * j;
-            const unsigned idx = static_cast<unsigned>(cbuf[i] >> sh) & 0xffu;
+            const unsigned idx = Mg[static_cast<unsigned>(cbuf[i] >> sh) & 0xffu];
             const uint4 v = lds128(tb + idx * kTNW + 2 * wp);
             acc0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
             acc1[j] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
