@@ -62,6 +62,7 @@ struct Ctx {
     // stats
     bool stats = false;
     uint64_t launches = 0;
+    uint64_t graph_launches = 0;
     struct Family {
         uint64_t n = 0;
         double ms = 0, bytes = 0, bitops = 0;
@@ -112,7 +113,9 @@ int ensure_init() {
     return F2_OK;
 }
 
+extern uint64_t g_ws_gen;
 int ensure_workspace(size_t m, size_t nq, size_t npanels, size_t scratch_words) {
+    if (m > g.cap_m || nq > g.cap_q || scratch_words > g.cap_scratch) ++g_ws_gen;
     if (m > g.cap_m) {
         if (g.P) cudaFree(g.P);
         if (g.pmap) cudaFree(g.pmap);
@@ -242,22 +245,15 @@ struct EngineOut {
     std::vector<int64_t> Qp;  // pivot columns
 };
 
-int run_engine(const Mat& A, unsigned W, EngineOut& out) {
+// One right-looking PLS pass, enqueued on `s`.  poll = snapshot r after every panel
+// and stop enqueueing once every row is a pivot (not usable inside a graph capture).
+int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
     const int64_t m = A.m, n = A.n;
-    out.rank = 0;
-    out.P.clear();
-    out.Qp.clear();
-    if (m == 0 || n == 0) return F2_OK;
     const int64_t nw = (n + 63) / 64;
     const int64_t npanels = (n + W - 1) / W;
-    int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
-                              static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
-    if (rc) return rc;
-    cudaStream_t s = g.stream;
     CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), s));
     launch_pmap_init(s, g.pmap, m);
     std::vector<cudaEvent_t> evs;
-    evs.reserve(npanels);
     int64_t checked = 0;
     bool stop = false;
 
@@ -310,22 +306,88 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             LaunchTimer t(0, static_cast<double>(pi), -1.0);
             launch_table_apply(s, ta, g.nsm);
         }
-        // early exit once every row is a pivot: snapshot r without blocking
-        CK(cudaMemcpyAsync(g.h_r + pi, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, s));
-        evs.push_back(ev);
-        while (checked < static_cast<int64_t>(evs.size()) && cudaEventQuery(evs[checked]) == cudaSuccess) {
-            if (g.h_r[checked] >= m) stop = true;
-            ++checked;
+        if (poll) {  // early exit once every row is a pivot: snapshot r without blocking
+            CK(cudaMemcpyAsync(g.h_r + pi, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, s));
+            evs.push_back(ev);
+            while (checked < static_cast<int64_t>(evs.size()) && cudaEventQuery(evs[checked]) == cudaSuccess) {
+                if (g.h_r[checked] >= m) stop = true;
+                ++checked;
+            }
         }
+    }
+    CK(cudaGetLastError());
+    if (poll) {
+        CK(cudaStreamSynchronize(s));
+        for (auto ev : evs) cudaEventDestroy(ev);
+    }
+    return F2_OK;
+}
+
+// Graph cache: the launch sequence depends only on (matrix, m, n, stride, W) and the
+// workspace buffers, so square-ish factorisations replay one captured CUDA graph
+// (per-launch overhead of ~3300 small launches at 64K^2 drops to graph-node cost).
+struct GraphCache {
+    uint64_t* w = nullptr;
+    int64_t m = 0, n = 0, stride = 0;
+    unsigned W = 0;
+    uint64_t gen = 0;
+    cudaGraphExec_t exec = nullptr;
+};
+GraphCache g_graph;
+uint64_t g_ws_gen = 1;  // bumped whenever a workspace buffer is reallocated
+
+int run_engine(const Mat& A, unsigned W, EngineOut& out) {
+    const int64_t m = A.m, n = A.n;
+    out.rank = 0;
+    out.P.clear();
+    out.Qp.clear();
+    if (m == 0 || n == 0) return F2_OK;
+    const int64_t nw = (n + 63) / 64;
+    const int64_t npanels = (n + W - 1) / W;
+    int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
+                              static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
+    if (rc) return rc;
+    cudaStream_t s = g.stream;
+    const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && !std::getenv("F2_NO_GRAPH");
+    if (use_graph) {
+        const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
+                         g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen;
+        if (!hit) {
+            if (g_graph.exec) cudaGraphExecDestroy(g_graph.exec);
+            g_graph.exec = nullptr;
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            const uint64_t l0 = g.launches;
+            rc = enqueue_engine(A, W, s, false);
+            const uint64_t per_call = g.launches - l0;
+            cudaError_t e = cudaStreamEndCapture(s, &graph);
+            if (rc) return rc;
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+            e = cudaGraphInstantiate(&g_graph.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+            g_graph.w = A.w;
+            g_graph.m = m;
+            g_graph.n = n;
+            g_graph.stride = A.stride;
+            g_graph.W = W;
+            g_graph.gen = g_ws_gen;
+            g.graph_launches = per_call;
+        } else {
+            g.launches += g.graph_launches;
+        }
+        CK(cudaGraphLaunch(g_graph.exec, s));
+    } else {
+        rc = enqueue_engine(A, W, s, true);
+        if (rc) return rc;
     }
     CK(cudaGetLastError());
     int64_t r = 0;
     CK(cudaMemcpyAsync(&r, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    for (auto ev : evs) cudaEventDestroy(ev);
     out.rank = r;
     out.P.resize(r);
     out.Qp.resize(r);
