@@ -271,7 +271,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             }
             {
                 LaunchTimer t(3, 0, 0);
-                launch_leaf_tables(s, g.st);
+                launch_leaf_tables(s, g.st, j);
             }
             {
                 LaunchTimer t(3, 0, 0);
@@ -286,7 +286,9 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         if (pw1 < nw) {
             {
                 LaunchTimer t(2, 0, 0);
-                launch_pivot_trsm(s, A, pw0, nleaves, pw1, nw, g.st, PivotSet{1, 0, 0}, nullptr);
+                launch_panel_lmaps(s, A, pw0, nleaves, g.st);
+                ++g.launches;
+                launch_panel_trsm(s, A, pw0, nleaves, pw1, nw, g.st);
             }
             TableApply ta{};
             ta.C = A;

@@ -45,6 +45,7 @@ struct PlsState {
     uint64_t ufull[64];                 // leaf pivot words (L bits, leading 1, S bits)
     uint64_t leaf_F[8][256];            // leaf finalize tables: correction of a word whose byte g reads v
     uint8_t leaf_M[8][256];             // leaf group index maps (inverse 8x8 L blocks, see trsm.cu)
+    uint64_t lmap[kMaxPanelBits / 64][8][256];  // per leaf of the panel: c -> c * L_leaf^{-1}, bytewise
     int32_t q[64];                      // leaf pivot bit positions (0..63)
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none

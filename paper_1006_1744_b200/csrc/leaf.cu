@@ -463,7 +463,7 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
 // does) and the index map M[g][e] = xor_{b in e} R[b], R the rows of the group's
 // inverse 8x8 L block (see trsm.cu).  k_leaf_update consumes both.  One thread per
 // table entry (16 CTAs x 256).
-__global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st) {
+__global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st, int leaf_in_panel) {
     __shared__ uint64_t s_u[64], s_uf[64];
     __shared__ int s_q[64];
     __shared__ int s_gs[9];
@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st) {
         s_gs[tid] = lo;
     }
     __syncthreads();
+
     const int i = blockIdx.x * 256 + tid;
     const int which = i >> 11, g = (i >> 8) & 7, v = i & 255;
     const int g0 = s_gs[g], g1 = s_gs[g + 1];
@@ -514,6 +515,75 @@ __global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st) {
             if ((v >> b) & 1) Mv ^= Rb[b];
         st->leaf_M[g][v] = static_cast<uint8_t>(Mv);
     }
+}
+
+// Per leaf j of the finished panel (one CTA each, in parallel): the bytewise map
+// c -> c * L_jj^{-1} of the leaf's 64x64 unit lower block, for k_panel_trsm.
+// lmap[j][g][v] = xor over bits b of v of R(pivot at raw 64j+8g+b), R_l = e_{q_l} ^
+// sum_{l'<l} c_l[l'] R_l' (c_l = pivot row l's L bits); built group by group, earlier
+// groups through their finished byte maps.  Runs after the panel's row gather, so the
+// pivot rows sit at physical positions panel_r + t.
+__global__ void __launch_bounds__(256) k_panel_lmaps(Mat A, int64_t pw0, PlsState* st) {
+    __shared__ uint64_t s_uf[64];
+    __shared__ int s_q[64];
+    __shared__ int s_gs[9];
+    __shared__ int s_pos[64];
+    __shared__ uint64_t s_R[64];
+    __shared__ uint64_t s_L[8][256];
+    const int j = blockIdx.x, tid = threadIdx.x;
+    const int nk = static_cast<int>(st->panel_kb);
+    const int64_t r0 = st->panel_r;
+    __shared__ int s_t0, s_t1;
+    if (tid == 0) {
+        int lo = 0;
+        while (lo < nk && st->panel_q[lo] < 64 * j) ++lo;
+        int hi = lo;
+        while (hi < nk && st->panel_q[hi] < 64 * j + 64) ++hi;
+        s_t0 = lo;
+        s_t1 = hi;
+    }
+    if (tid < 64) s_pos[tid] = -1;
+    __syncthreads();
+    const int t0 = s_t0, kb = s_t1 - s_t0;
+    if (kb == 0) return;
+    if (tid < kb) {
+        s_q[tid] = st->panel_q[t0 + tid] - 64 * j;
+        s_uf[tid] = A.w[(r0 + t0 + tid) * A.stride + pw0 + j];
+    }
+    __syncthreads();
+    if (tid < kb) s_pos[s_q[tid]] = tid;
+    if (tid <= 8) {
+        int lo = 0;
+        while (lo < kb && s_q[lo] < 8 * tid) ++lo;
+        s_gs[tid] = lo;
+    }
+    __syncthreads();
+    for (int g = 0; g < 8; ++g) {
+        if (tid == 0) {
+            for (int l = s_gs[g]; l < s_gs[g + 1]; ++l) {
+                const uint64_t c = s_uf[l] & ((1ull << s_q[l]) - 1ull);
+                uint64_t R = 1ull << s_q[l];
+                for (int g2 = 0; g2 < g; ++g2) R ^= s_L[g2][(c >> (8 * g2)) & 0xffu];
+                const unsigned inb = static_cast<unsigned>(c >> (8 * g)) & 0xffu;
+                for (int b = 0; b < 8; ++b)
+                    if ((inb >> b) & 1u) R ^= s_R[s_pos[8 * g + b]];
+                s_R[l] = R;
+            }
+        }
+        __syncthreads();
+        uint64_t x = 0;
+        for (int b = 0; b < 8; ++b) {
+            const int l = s_pos[8 * g + b];
+            if (((tid >> b) & 1) && l >= 0) x ^= s_R[l];
+        }
+        s_L[g][tid] = x;
+        __syncthreads();
+    }
+    for (int g = 0; g < 8; ++g) st->lmap[j][g][tid] = s_L[g][tid];
+}
+
+void launch_panel_lmaps(cudaStream_t s, const Mat& A, int64_t pw0, int nleaves, PlsState* st) {
+    k_panel_lmaps<<<nleaves, 256, 0, s>>>(A, pw0, st);
 }
 
 // Panel end, step 1: copy the rows that the panel's positions now refer to
@@ -557,7 +627,9 @@ void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* s
     k_perm_put<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
 }
 
-void launch_leaf_tables(cudaStream_t s, PlsState* st) { k_leaf_tables<<<16, 256, 0, s>>>(st); }
+void launch_leaf_tables(cudaStream_t s, PlsState* st, int leaf_in_panel) {
+    k_leaf_tables<<<16, 256, 0, s>>>(st, leaf_in_panel);
+}
 
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {
     int64_t g = (m + 255) / 256;
