@@ -160,6 +160,8 @@ def run_ours(args):
     import paper_1006_1744_b200 as f2
 
     f2.set_device(local)
+    if ws > 1:
+        return run_sharded(args, f2, dist, ws, rank, local)
     cfg = f2.EliminationConfig(cutoff_bytes=CUTOFF)
     a0 = f2.DeviceMatrix(N, N)
     a0.randomize(0.5, SEED + rank)
@@ -292,6 +294,60 @@ def run_ours(args):
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+    return 0
+
+
+def run_sharded(args, f2, dist, ws, rank, local):
+    """N > 1: one 65536^2 PLS column-sharded over the ranks (paper_1006_1744_b200/dist.py),
+    panel data broadcast with NCCL; strong scaling (total work fixed)."""
+    import numpy as np
+    import torch
+
+    from paper_1006_1744_b200 import dist as D
+
+    W = 1024
+    full = f2.DeviceMatrix(N, N)
+    full.randomize(0.5, SEED)
+    host = full.download()
+    del full
+    shard = D.split_columns(host, N, rank, ws, W)
+    ncols = D.local_ncols(rank, ws, N, W)
+    a0 = f2.DeviceMatrix.from_host(shard, ncols)
+    a = f2.DeviceMatrix(N, ncols)
+    del host, shard
+    ops, comm = D.GpuOps(f2), D.TorchComm()
+
+    def step():
+        a.copy_from(a0)
+        return D.pls_sharded(ops, comm, a, N, N, W, rank, ws)
+
+    for _ in range(args.warmup):
+        res = step()
+    t = torch.zeros(1, device="cuda")
+    dist.all_reduce(t)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": args.steps * BITOPS / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u64 (GF(2) bit-packed)",
+                "data": "synthetic (BitMatrix::randomize SplitMix64 stream, seed 3)",
+                "config": dict(CONFIG, parallelism=f"column-sharded x{ws} (block-cyclic {W}-bit panels, NCCL broadcast)"),
+                "rank": res.rank, "clocks": clk.summary(), "e2e": None, "roofline": None, "cpu_baseline": None,
+                "gpu_launches": None}
+        print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 

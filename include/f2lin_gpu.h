@@ -120,6 +120,27 @@ int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t q
 /* Permutation::apply_rows / apply_rows_inverse — perm.hpp:42-45, perm.cpp:29-38 */
 int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int inverse);
 
+/* ---- column-sharded PLS (one rank per GPU; paper_1006_1744_b200/dist.py) ----
+ * Rank k holds panels k, k+N, ... of W bits side by side in a local matrix.  Per
+ * panel the owner calls f2_dist_factor_panel (fills a header of
+ * f2_dist_header_words(W) words and the panel's words for rows >= r), the caller
+ * broadcasts both (NCCL), then every rank calls f2_dist_apply_panel on its trailing
+ * columns (owner = 1 on the owner, which already applied the row gather). */
+size_t f2_dist_header_words(unsigned panel_bits);
+int f2_dist_begin(f2_matrix* a);
+int f2_dist_factor_panel(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t r, uint64_t panel_col,
+                         uint64_t* hdr_dev, uint64_t* words_dev, size_t words_stride, uint64_t* kb_out);
+int f2_dist_apply_panel(f2_matrix* a, size_t tw0, unsigned width_bits, int owner, const uint64_t* hdr_dev,
+                        const uint64_t* words_dev, size_t words_stride);
+/* compress_columns of a packed PLS result from its pivot columns (perm.cpp:18-21) */
+int f2_pls_compress(f2_matrix* a, uint64_t rank, const uint64_t* pivcols);
+/* pls_recursive's full Q (tail included) from (m, n, cutoff, pivot columns) — pls.cpp:63-103 */
+int f2_recursive_q(size_t m, size_t n, uint64_t cutoff, uint64_t rank, const uint64_t* pivcols, uint64_t* q);
+/* raw device buffers (exchange buffers of the sharded path) */
+void* f2_device_alloc(size_t bytes);
+void f2_device_free(void* p);
+int f2_device_copy(void* dst, const void* src, size_t bytes, int kind);
+
 /* ---- instrumentation (bench.py roofline) -------------------------------- */
 /* When enabled, the library brackets every launch of kernel family `kind`
  * with CUDA events on its own stream and accumulates launches, device ms and

@@ -267,7 +267,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
             {
                 LaunchTimer t(1, 0, 0);
-                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap);
+                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, 0);
             }
             {
                 LaunchTimer t(3, 0, 0);
@@ -288,7 +288,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 LaunchTimer t(2, 0, 0);
                 launch_panel_lmaps(s, A, pw0, nleaves, g.st);
                 ++g.launches;
-                launch_panel_trsm(s, A, pw0, nleaves, pw1, nw, g.st);
+                launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
             }
             TableApply ta{};
             ta.C = A;
@@ -992,6 +992,160 @@ int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int
     cudaError_t e = cudaStreamSynchronize(g.stream);
     cudaFree(dmap);
     if (e != cudaSuccess) return cuda_fail(e, "apply_rows");
+    return F2_OK;
+}
+
+}  // extern "C"
+
+// ---- column-sharded PLS building blocks (paper_1006_1744_b200/dist.py) ----------------
+// Rank k holds the panels p = k, k+N, k+2N, ... (W bits each) side by side in a local
+// matrix with all m rows.  Per panel: the owner factors it (leaf chain, virtual row
+// order), exports a header (pivots, re-mapped rows, P entries) and the panel's words
+// for rows >= r; both are broadcast; every rank then applies the panel to its own
+// trailing columns (row gather, panel TRSM, Schur multiply) reading L from the
+// broadcast words.  The packed result, P and the pivot columns equal the single-GPU
+// engine's (same pivot rule, same operations per column).
+extern "C" {
+
+size_t f2_dist_header_words(unsigned panel_bits) {
+    return 4 + 2 * static_cast<size_t>(panel_bits) + 2 * static_cast<size_t>(kMaxMoved);
+}
+
+int f2_dist_begin(f2_matrix* a) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
+    int rc = ensure_init();
+    if (rc) return rc;
+    if ((rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride)))
+        return rc;
+    CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), g.stream));
+    launch_pmap_init(g.stream, g.pmap, static_cast<int64_t>(a->m));
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int f2_dist_factor_panel(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t r, uint64_t panel_col,
+                         uint64_t* hdr_dev, uint64_t* words_dev, size_t words_stride, uint64_t* kb_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || !hdr_dev || !words_dev || !kb_out) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (width_bits == 0 || width_bits > 1024 || (pw0 * 64 + width_bits) > a->n || r > a->m)
+        return fail(F2_INVALID_ARGUMENT, "panel out of range");
+    const int nleaves = static_cast<int>((width_bits + 63) / 64);
+    if (words_stride < static_cast<size_t>(nleaves)) return fail(F2_INVALID_ARGUMENT, "words stride too small");
+    int rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride);
+    if (rc) return rc;
+    const Mat A = mat_of(a);
+    const int64_t m = A.m, nw = (A.n + 63) / 64, pw1 = static_cast<int64_t>(pw0) + nleaves;
+    cudaStream_t s = g.stream;
+    launch_set_r(s, g.st, static_cast<int64_t>(r));
+    const int64_t qoff = static_cast<int64_t>(panel_col) - static_cast<int64_t>(pw0) * 64;
+    for (int j = 0; j < nleaves; ++j) {
+        const int64_t wl = static_cast<int64_t>(pw0) + j;
+        const int lw = static_cast<int>(std::min<int64_t>(64, static_cast<int64_t>(width_bits) - 64 * j));
+        launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, qoff);
+        launch_leaf_tables(s, g.st, j);
+        launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
+    }
+    launch_dist_export(s, g.st, g.pmap, g.P, reinterpret_cast<int64_t*>(hdr_dev), nleaves * 64);
+    launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+    if (static_cast<int64_t>(r) < m)
+        CK(cudaMemcpy2DAsync(words_dev + r * words_stride, words_stride * 8, A.w + static_cast<int64_t>(r) * A.stride + pw0,
+                             A.stride * 8, nleaves * 8, m - static_cast<int64_t>(r), cudaMemcpyDeviceToDevice, s));
+    int64_t kb = 0;
+    CK(cudaMemcpyAsync(&kb, &g.st->panel_kb, sizeof(kb), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *kb_out = static_cast<uint64_t>(kb);
+    return F2_OK;
+}
+
+int f2_dist_apply_panel(f2_matrix* a, size_t tw0, unsigned width_bits, int owner, const uint64_t* hdr_dev,
+                        const uint64_t* words_dev, size_t words_stride) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || !hdr_dev || !words_dev) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (width_bits == 0 || width_bits > 1024) return fail(F2_INVALID_ARGUMENT, "panel width out of range");
+    const int nleaves = static_cast<int>((width_bits + 63) / 64);
+    int rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride);
+    if (rc) return rc;
+    const Mat A = mat_of(a);
+    const int64_t nw = (A.n + 63) / 64;
+    cudaStream_t s = g.stream;
+    if (!owner) {
+        launch_dist_import(s, g.st, g.pmap, reinterpret_cast<const int64_t*>(hdr_dev), nleaves * 64);
+        launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+    }
+    if (static_cast<int64_t>(tw0) < nw) {
+        const Mat Cf{const_cast<uint64_t*>(words_dev), A.m, static_cast<int64_t>(width_bits),
+                     static_cast<int64_t>(words_stride)};
+        launch_panel_lmaps(s, Cf, 0, nleaves, g.st);
+        launch_panel_trsm(s, A, Cf, 0, nleaves, static_cast<int64_t>(tw0), nw, g.st);
+        TableApply ta{};
+        ta.C = A;
+        ta.c_r1 = A.m;
+        ta.cw0 = static_cast<int64_t>(tw0);
+        ta.cw1 = nw;
+        ta.A = Cf;
+        ta.aw0 = 0;
+        ta.kw = nleaves;
+        ta.kbits = width_bits;
+        ta.B = A;
+        ta.bw0 = static_cast<int64_t>(tw0);
+        ta.brow = g.st->brow;
+        ta.row_mode = ROWS_AFTER_PANEL;
+        ta.st = g.st;
+        launch_table_apply(s, ta, g.nsm);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return F2_OK;
+}
+
+// compress_columns of a packed PLS result given its pivot columns (k_compress)
+int f2_pls_compress(f2_matrix* a, uint64_t rank, const uint64_t* pivcols) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!pivcols && rank)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (rank == 0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    if ((rc = ensure_workspace(a->m, rank, 1, static_cast<size_t>(kMaxMoved) * a->stride))) return rc;
+    std::vector<int64_t> q(pivcols, pivcols + rank);
+    bool ident = true;
+    for (uint64_t t = 0; t < rank; ++t) ident &= q[t] == static_cast<int64_t>(t);
+    if (ident) return F2_OK;
+    CK(cudaMemcpyAsync(g.Qp, q.data(), sizeof(int64_t) * rank, cudaMemcpyHostToDevice, g.stream));
+    launch_compress(g.stream, mat_of(a), static_cast<int64_t>(rank), g.Qp, g.nsm);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+// pls_recursive's Q (tail included) from the pivot columns — host only (pls.cpp:63-103)
+int f2_recursive_q(size_t m, size_t n, uint64_t cutoff, uint64_t rank, const uint64_t* pivcols, uint64_t* q) {
+    if (!q && n) return fail(F2_INVALID_ARGUMENT, "null argument");
+    std::vector<int64_t> piv(pivcols, pivcols + rank);
+    replay_q(m, n, cutoff ? cutoff : default_cutoff(), piv.data(), static_cast<size_t>(rank), q);
+    return F2_OK;
+}
+
+void* f2_device_alloc(size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (ensure_init()) return nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaMemset(p, 0, std::max<size_t>(bytes, 8));
+    return p;
+}
+
+void f2_device_free(void* p) {
+    if (p) cudaFree(p);
+}
+
+int f2_device_copy(void* dst, const void* src, size_t bytes, int kind) {
+    // kind: 0 = device->device, 1 = host->device, 2 = device->host
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpy(dst, src, bytes, k));
     return F2_OK;
 }
 

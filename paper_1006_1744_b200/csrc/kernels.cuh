@@ -9,11 +9,14 @@ namespace f2g {
 
 // leaf.cu
 void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap);
+                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off);
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch);
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
 void launch_leaf_tables(cudaStream_t s, PlsState* st, int leaf_in_panel);
-void launch_panel_lmaps(cudaStream_t s, const Mat& A, int64_t pw0, int nleaves, PlsState* st);
+void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves, PlsState* st);
+void launch_dist_export(cudaStream_t s, const PlsState* st, const int64_t* pmap, const int64_t* P, int64_t* hdr, int W);
+void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, const int64_t* hdr, int W);
+void launch_set_r(cudaStream_t s, PlsState* st, int64_t r);
 void setup_leaf_kernels();
 
 // leafupd.cu — one leaf's update of its panel (virtual row order via pmap):
@@ -32,8 +35,8 @@ struct PivotSet {
 };
 void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_words, int64_t tw0,
                        int64_t tw1, const PlsState* st, PivotSet ps, const Mat* L);
-void launch_panel_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1,
-                       const PlsState* st);
+void launch_panel_trsm(cudaStream_t s, const Mat& A, const Mat& Cf, int64_t coef_w0, int nleaves, int64_t tw0,
+                       int64_t tw1, const PlsState* st);
 void setup_trsm_kernels();
 
 // m4rm.cu — C ^= A * B by 8-bit Gray tables in SMEM (M4RM, mul.cpp:21-68),

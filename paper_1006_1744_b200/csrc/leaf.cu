@@ -110,7 +110,7 @@ __device__ __forceinline__ int32_t pick(const int32_t (&v)[S], int s) {
 // position of the content a lane holds.  Rows are read through pmap.
 __global__ void __launch_bounds__(1024, 1)
 k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, int panel_bits,
-             PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap) {
+             PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off) {
     __shared__ uint64_t s_u[64];
     __shared__ uint64_t s_uf[64];
     __shared__ int s_q[64];
@@ -197,7 +197,7 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
             s_uf[t] = u;
             s_q[t] = cstar;
             P[base + p] = pabs_src;
-            Qp[base + p] = wl * 64 + cstar;
+            Qp[base + p] = qcol_off + wl * 64 + cstar;
         }
         __syncwarp();
     };
@@ -278,7 +278,7 @@ k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, i
                     s_uf[t] = u;
                     s_q[t] = cstar;
                     P[base + p] = base + bb + ln;
-                    Qp[base + p] = wl * 64 + cstar;
+                    Qp[base + p] = qcol_off + wl * 64 + cstar;
                 }
 #ifdef F2_LEAF_PROFILE
                 if (lane == 0 && t < 11) st->dbg[5 + t] = clock64() - c_start;
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st, int leaf_in_p
 // sum_{l'<l} c_l[l'] R_l' (c_l = pivot row l's L bits); built group by group, earlier
 // groups through their finished byte maps.  Runs after the panel's row gather, so the
 // pivot rows sit at physical positions panel_r + t.
-__global__ void __launch_bounds__(256) k_panel_lmaps(Mat A, int64_t pw0, PlsState* st) {
+__global__ void __launch_bounds__(256) k_panel_lmaps(Mat Cf, int64_t pw0, PlsState* st) {
     __shared__ uint64_t s_uf[64];
     __shared__ int s_q[64];
     __shared__ int s_gs[9];
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256) k_panel_lmaps(Mat A, int64_t pw0, PlsStat
     if (kb == 0) return;
     if (tid < kb) {
         s_q[tid] = st->panel_q[t0 + tid] - 64 * j;
-        s_uf[tid] = A.w[(r0 + t0 + tid) * A.stride + pw0 + j];
+        s_uf[tid] = Cf.w[(r0 + t0 + tid) * Cf.stride + pw0 + j];
     }
     __syncthreads();
     if (tid < kb) s_pos[s_q[tid]] = tid;
@@ -582,9 +582,79 @@ __global__ void __launch_bounds__(256) k_panel_lmaps(Mat A, int64_t pw0, PlsStat
     for (int g = 0; g < 8; ++g) st->lmap[j][g][tid] = s_L[g][tid];
 }
 
-void launch_panel_lmaps(cudaStream_t s, const Mat& A, int64_t pw0, int nleaves, PlsState* st) {
-    k_panel_lmaps<<<nleaves, 256, 0, s>>>(A, pw0, st);
+void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves, PlsState* st) {
+    k_panel_lmaps<<<nleaves, 256, 0, s>>>(Cf, pw0, st);
 }
+
+// ---- column-sharded (multi-GPU) panel exchange --------------------------------------
+// Header of one factored panel (int64): [0] kb, [1] panel_r, [2] nmoved, [3] reserved,
+// [4, 4+W) pivot columns (panel-relative), then kMaxMoved re-mapped positions, then
+// their source rows (pmap values), then W entries P[panel_r + t].
+__global__ void __launch_bounds__(256) k_dist_export(const PlsState* st, const int64_t* pmap, const int64_t* P,
+                                                    int64_t* hdr, int W) {
+    const int kb = static_cast<int>(st->panel_kb), nm = st->nmoved;
+    const int64_t r0 = st->panel_r;
+    int64_t* q = hdr + 4;
+    int64_t* mv = q + W;
+    int64_t* src = mv + kMaxMoved;
+    int64_t* pp = src + kMaxMoved;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    if (tid == 0) {
+        hdr[0] = kb;
+        hdr[1] = r0;
+        hdr[2] = nm;
+        hdr[3] = 0;
+    }
+    for (int t = tid; t < kb; t += nth) {
+        q[t] = st->panel_q[t];
+        pp[t] = P[r0 + t];
+    }
+    for (int i = tid; i < nm; i += nth) {
+        mv[i] = st->moved[i];
+        src[i] = pmap[st->moved[i]];
+    }
+}
+
+// A rank that does not own the panel adopts the owner's header: pivot bookkeeping
+// for the TRSM/Schur kernels and the re-mapped positions for the row gather.
+__global__ void __launch_bounds__(1024) k_dist_import(PlsState* st, int64_t* pmap, const int64_t* hdr, int W) {
+    const int kb = static_cast<int>(hdr[0]), nm = static_cast<int>(hdr[2]);
+    const int64_t r0 = hdr[1];
+    const int64_t* q = hdr + 4;
+    const int64_t* mv = q + W;
+    const int64_t* src = mv + kMaxMoved;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (int i = tid; i < W; i += nth) st->brow[i] = -1;
+    __syncthreads();
+    for (int t = tid; t < kb; t += nth) {
+        st->panel_q[t] = static_cast<int32_t>(q[t]);
+        st->brow[q[t]] = r0 + t;
+    }
+    for (int i = tid; i < nm; i += nth) {
+        st->moved[i] = mv[i];
+        pmap[mv[i]] = src[i];
+    }
+    if (tid == 0) {
+        st->panel_kb = kb;
+        st->panel_r = r0;
+        st->r = r0 + kb;
+        st->nmoved = nm;
+    }
+}
+
+__global__ void k_set_r(PlsState* st, int64_t r) {
+    st->r = r;
+    st->panel_kb = 0;
+    st->nmoved = 0;
+}
+
+void launch_dist_export(cudaStream_t s, const PlsState* st, const int64_t* pmap, const int64_t* P, int64_t* hdr, int W) {
+    k_dist_export<<<32, 256, 0, s>>>(st, pmap, P, hdr, W);
+}
+void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, const int64_t* hdr, int W) {
+    k_dist_import<<<1, 1024, 0, s>>>(st, pmap, hdr, W);
+}
+void launch_set_r(cudaStream_t s, PlsState* st, int64_t r) { k_set_r<<<1, 1, 0, s>>>(st, r); }
 
 // Panel end, step 1: copy the rows that the panel's positions now refer to
 // (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
@@ -617,8 +687,8 @@ __global__ void k_pmap_init(int64_t* pmap, int64_t m) {
 }
 
 void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap) {
-    k_leaf_pivot<<<1, 1024, 0, s>>>(A, wl, lw, first, leaf_in_panel, panel_bits, st, P, Qp, pmap);
+                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off) {
+    k_leaf_pivot<<<1, 1024, 0, s>>>(A, wl, lw, first, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off);
 }
 
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch) {

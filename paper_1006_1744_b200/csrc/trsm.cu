@@ -227,7 +227,7 @@ constexpr int kPTW = 4;  // target words per CTA
 }
 
 __global__ void __launch_bounds__(512, 1)
-k_panel_trsm(Mat A, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1, const PlsState* st) {
+k_panel_trsm(Mat A, Mat Cf, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1, const PlsState* st) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int rows_cap = nleaves * 64;
     uint64_t* X = smem;                                   // [rows_cap][kPTW]
@@ -277,7 +277,7 @@ k_panel_trsm(Mat A, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1, cons
         if (t0 == t1) continue;
         // this block's inverse map and every row's coefficient word for the block
         for (int i = tid; i < 8 * 256; i += nth) Lm[i] = (&st->lmap[j][0][0])[i];
-        for (int t = t0 + tid; t < nk; t += nth) cw[t] = A.w[(r0 + t) * A.stride + coef_w0 + j];
+        for (int t = t0 + tid; t < nk; t += nth) cw[t] = Cf.w[(r0 + t) * Cf.stride + coef_w0 + j];
         // 8 tables over block j's rows as they are now: thread = (table g, word w, low nibble)
         {
             const int g = tid >> 6, w = (tid >> 4) & 3, el = tid & 15;
@@ -331,11 +331,11 @@ static size_t panel_trsm_smem(int nleaves) {
            sizeof(int16_t) * rows + sizeof(int32_t) * (nleaves + 8);
 }
 
-void launch_panel_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1,
-                       const PlsState* st) {
+void launch_panel_trsm(cudaStream_t s, const Mat& A, const Mat& Cf, int64_t coef_w0, int nleaves, int64_t tw0,
+                       int64_t tw1, const PlsState* st) {
     if (tw1 <= tw0) return;
     const int grid = static_cast<int>((tw1 - tw0 + kPTW - 1) / kPTW);
-    k_panel_trsm<<<grid, 512, panel_trsm_smem(nleaves), s>>>(A, coef_w0, nleaves, tw0, tw1, st);
+    k_panel_trsm<<<grid, 512, panel_trsm_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
 }
 
 void setup_trsm_kernels() {
