@@ -106,6 +106,11 @@ uint64_t f2_default_cutoff_bytes(void);
 /* detail::auto_table_bits — mul.cpp:9-14 */
 unsigned f2_auto_table_bits(size_t dim);
 
+/* void rref_from_pls(MatrixWindow a, size_t rank, span<const size_t> q) — pls.hpp:54, pls.cpp:128-155 */
+int f2_rref_from_pls(f2_matrix* a, f2_window w, uint64_t rank, const uint64_t* q, size_t qlen);
+/* echelonize: RREF via pls_recursive + rref_from_pls (equals gauss_rref / m4ri_rref, gauss.hpp:28) */
+int f2_rref(f2_matrix* a, f2_window w, const f2_elim_config* cfg, uint64_t* rank);
+
 /* ---- multiply / triangular solve --------------------------------------- */
 /* void addmul(MatrixWindow c, MatrixWindow a, MatrixWindow b, unsigned k=0) — mul.hpp:20, mul.cpp:102-107 */
 int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix* b, f2_window wb,

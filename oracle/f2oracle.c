@@ -225,3 +225,71 @@ int f2o_pls_check(const uint64_t* orig, const uint64_t* packed, size_t m, size_t
     free(out);
     return ok;
 }
+
+/* gauss_rref — src/gauss.cpp:7-23: column by column, first row >= r with a 1,
+ * swap it up, clear the column in every other row. */
+size_t f2o_gauss_rref(uint64_t* w, size_t m, size_t n) {
+    size_t s = WORDS(n), r = 0;
+    for (size_t c = 0; c < n && r < m; ++c) {
+        size_t piv = m;
+        for (size_t i = r; i < m; ++i)
+            if (GET(w, s, i, c)) {
+                piv = i;
+                break;
+            }
+        if (piv == m) continue;
+        for (size_t k = 0; k < s; ++k) {
+            uint64_t t = w[r * s + k];
+            w[r * s + k] = w[piv * s + k];
+            w[piv * s + k] = t;
+        }
+        for (size_t i = 0; i < m; ++i)
+            if (i != r && GET(w, s, i, c))
+                for (size_t k = 0; k < s; ++k) w[i * s + k] ^= w[r * s + k];
+        ++r;
+    }
+    return r;
+}
+
+static void col_swap_rows(uint64_t* w, size_t s, size_t r0, size_t r1, size_t a, size_t b) {
+    for (size_t i = r0; i < r1; ++i) {
+        uint64_t* row = w + i * s;
+        uint64_t va = (row[a / 64] >> (a % 64)) & 1u, vb = (row[b / 64] >> (b % 64)) & 1u;
+        if (va != vb) {
+            row[a / 64] ^= 1ull << (a % 64);
+            row[b / 64] ^= 1ull << (b % 64);
+        }
+    }
+}
+
+/* rref_from_pls — src/pls.cpp:128-155, step for step: validation (:130-135);
+ * zero the L storage and the rows >= rank (:137-138); complete the column swaps
+ * over the rows above (:145-146); unit upper triangular solve of the top block
+ * against columns rank..n (:148-149, trsm_upper_left_unit mul.cpp:133-155,
+ * restated as plain back substitution, bottom row first); identity pivot block
+ * (:151); undo the swaps in reverse (:153-154).  Returns 1 on invalid_argument. */
+int f2o_rref_from_pls(uint64_t* w, size_t m, size_t n, size_t rank, const uint64_t* q, size_t qlen) {
+    size_t s = WORDS(n);
+    if (rank > m || rank > n || qlen < rank) return 1;
+    for (size_t t = 0; t < rank; ++t)
+        if (q[t] >= n || q[t] < t || (t > 0 && q[t] <= q[t - 1])) return 1;
+    for (size_t i = 1; i < m; ++i)
+        for (size_t j = 0; j < (i < rank ? i : rank); ++j) w[i * s + j / 64] &= ~(1ull << (j % 64));
+    for (size_t i = rank; i < m; ++i)
+        for (size_t k = 0; k < s; ++k) w[i * s + k] = 0;
+    for (size_t j = 0; j < rank; ++j)
+        if (q[j] != j) col_swap_rows(w, s, 0, j, j, (size_t)q[j]);
+    if (rank > 0 && rank < n) {
+        /* row u -= sum_{v>u} T[u][v] * row v over columns >= rank, v descending */
+        for (size_t u = rank; u-- > 0;)
+            for (size_t v = u + 1; v < rank; ++v)
+                if (GET(w, s, u, v))
+                    for (size_t j = rank; j < n; ++j)
+                        if (GET(w, s, v, j)) w[u * s + j / 64] ^= 1ull << (j % 64);
+    }
+    for (size_t u = 0; u < rank; ++u)
+        for (size_t j = u + 1; j < rank; ++j) w[u * s + j / 64] &= ~(1ull << (j % 64));
+    for (size_t j = rank; j-- > 0;)
+        if (q[j] != j) col_swap_rows(w, s, 0, rank, j, (size_t)q[j]);
+    return 0;
+}

@@ -26,4 +26,6 @@ unsigned f2o_auto_table_bits(size_t dim);
 uint64_t f2o_digest(const uint64_t* w, size_t nwords);
 int f2o_pls_check(const uint64_t* orig, const uint64_t* packed, size_t m, size_t n, size_t rank,
                   const uint64_t* p, const uint64_t* q);
+size_t f2o_gauss_rref(uint64_t* w, size_t m, size_t n);
+int f2o_rref_from_pls(uint64_t* w, size_t m, size_t n, size_t rank, const uint64_t* q, size_t qlen);
 #endif

@@ -7,6 +7,7 @@
 //   pls_recursive       (proj/include/f2lin/pls.hpp:42-47, proj/src/pls.cpp:105-126)
 //   gauss_pls           (proj/src/gauss.cpp:26-55)
 //   rref_from_pls       (proj/src/pls.cpp:128-161)
+//   gauss_rref          (proj/src/gauss.cpp:7-23)
 //   mul_m4rm / addmul   (proj/src/mul.cpp:90-107)
 //   trsm_*_left_unit    (proj/src/mul.cpp:109-157)
 //   BitMatrix::randomize(proj/src/bitmat.cpp:136-154)
@@ -110,6 +111,14 @@ int ref_rref_from_pls(uint64_t* w, size_t m, size_t n, uint64_t rank, const uint
         BitMatrix a = load(w, m, n);
         std::vector<size_t> qv(q, q + qlen);
         rref_from_pls(a.view(), rank, std::span<const size_t>(qv));
+        store(a, w);
+    });
+}
+
+int ref_gauss_rref(uint64_t* w, size_t m, size_t n, uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        *rank = gauss_rref(a);
         store(a, w);
     });
 }

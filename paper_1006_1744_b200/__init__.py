@@ -100,6 +100,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_pls_recursive": ([vp, _Window, _u64p, sz, _u64p, sz, C.POINTER(_Cfg), _u64p], i),
         "f2_mmpf_pls_host": ([_u64p, sz, sz, sz, _u64p, _u64p, C.c_uint, _u64p], i),
         "f2_pls_recursive_host": ([_u64p, sz, sz, sz, _u64p, _u64p, C.POINTER(_Cfg), _u64p], i),
+        "f2_rref_from_pls": ([vp, _Window, C.c_uint64, _u64p, sz], i),
+        "f2_rref": ([vp, _Window, C.POINTER(_Cfg), _u64p], i),
         "f2_default_cutoff_bytes": ([], C.c_uint64),
         "f2_auto_table_bits": ([sz], C.c_uint),
         "f2_addmul": ([vp, _Window, vp, _Window, vp, _Window, C.c_uint], i),
@@ -310,6 +312,29 @@ def pls_recursive(a: DeviceMatrix, cfg: Optional[EliminationConfig] = None,
     cc = cfg.c()
     _check(_lib.f2_pls_recursive(a.handle, w.c(), _ptr(p), p.size, _ptr(q), q.size, C.byref(cc), C.byref(r)))
     return PlsResult(int(r.value), p, q)
+
+
+def rref_from_pls(a: DeviceMatrix, rank: int, q: np.ndarray, window: Optional[Window] = None,
+                  p: Optional[np.ndarray] = None) -> None:
+    """Reduced row echelon form from a packed PLS result, in place; pls.hpp:54-59,
+    pls.cpp:128-161.  ``q`` is the pivot-column prefix (Q[:rank] or all of Q);
+    ``p``, when given, is only length-checked like the BitMatrix overload (pls.cpp:157-161)."""
+    w = _win(a, window)
+    if p is not None and len(p) != w.r1 - w.r0:
+        raise ValueError("rref_from_pls: P has the wrong length")
+    q = np.ascontiguousarray(q, dtype=np.uint64)
+    if p is not None:
+        q = q[:min(q.size, rank)].copy()
+    _check(_lib.f2_rref_from_pls(a.handle, w.c(), rank, _ptr(q), q.size))
+
+
+def rref(a: DeviceMatrix, cfg: Optional[EliminationConfig] = None, window: Optional[Window] = None) -> int:
+    """Echelonize in place (pls_recursive + rref_from_pls, the reference's Algorithm::pls
+    RREF, acceptance.cpp:37-41); returns the rank.  Equals gauss_rref bit for bit."""
+    cc = (cfg or EliminationConfig()).c()
+    r = C.c_uint64()
+    _check(_lib.f2_rref(a.handle, _win(a, window).c(), C.byref(cc), C.byref(r)))
+    return int(r.value)
 
 
 def _pls_host(fn, words, ncols, extra):

@@ -108,6 +108,7 @@ int ensure_init() {
     setup_trsm_kernels();
     setup_m4rm_kernels();
     setup_misc_kernels();
+    setup_rref_kernels();
     CK(cudaGetLastError());
     g.init = true;
     return F2_OK;
@@ -1147,6 +1148,94 @@ int f2_device_copy(void* dst, const void* src, size_t bytes, int kind) {
     const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     CK(cudaMemcpy(dst, src, bytes, k));
     return F2_OK;
+}
+
+}  // extern "C"
+
+// ---- echelonize -------------------------------------------------------------------
+namespace {
+
+// RREF of the original matrix from a packed PLS result in the aligned matrix T
+// (rref_from_pls, pls.cpp:128-155).  The reduced rows are U^{-1} S, U = S at the
+// pivot columns (unit upper triangular): a backward substitution, run as the
+// forward solver on row- and column-reversed coefficients.
+int rref_on(f2_matrix* t, uint64_t rank, const std::vector<int64_t>& q) {
+    const int64_t m = static_cast<int64_t>(t->m);
+    const int64_t r = static_cast<int64_t>(rank);
+    int rc;
+    if ((rc = ensure_workspace(t->m, std::max<size_t>(t->m, rank) + 1, 1, static_cast<size_t>(kMaxMoved) * t->stride)))
+        return rc;
+    if (r) CK(cudaMemcpyAsync(g.Qp, q.data(), sizeof(int64_t) * r, cudaMemcpyHostToDevice, g.stream));
+    launch_rref_prepare(g.stream, mat_of(t), r, g.Qp);
+    if (r > 1) {
+        TmpMat lrev, xrev;
+        if ((rc = alloc_matrix(rank, rank, &lrev.m)) || (rc = alloc_matrix(rank, t->n, &xrev.m))) return rc;
+        launch_rref_coeffs(g.stream, mat_of(t), r, g.Qp, mat_of(lrev.m), g.nsm);
+        std::vector<int64_t> rev(rank);
+        for (int64_t i = 0; i < r; ++i) rev[i] = r - 1 - i;
+        int64_t* dmap = nullptr;
+        CK(cudaMalloc(&dmap, sizeof(int64_t) * rank));
+        CK(cudaMemcpyAsync(dmap, rev.data(), sizeof(int64_t) * rank, cudaMemcpyHostToDevice, g.stream));
+        launch_gather_rows(g.stream, mat_of(xrev.m), mat_of(t), dmap, r, static_cast<int64_t>(t->stride));
+        trsm_rec(mat_of(lrev.m), mat_of(xrev.m), 0, r);
+        launch_gather_rows(g.stream, mat_of(t), mat_of(xrev.m), dmap, r, static_cast<int64_t>(t->stride));
+        cudaError_t e = cudaStreamSynchronize(g.stream);
+        cudaFree(dmap);
+        if (e != cudaSuccess) return cuda_fail(e, "rref");
+    }
+    (void)m;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+int rref_window(f2_matrix* a, const f2_window& w, uint64_t rank, const std::vector<int64_t>& q) {
+    if (full_window(a, w)) return rref_on(a, rank, q);
+    TmpMat t;
+    int rc = extract_tmp(a, w, t);
+    if (rc) return rc;
+    if ((rc = rref_on(t.m, rank, q))) return rc;
+    launch_insert(g.stream, mat_of(a), static_cast<int64_t>(w.r0), static_cast<int64_t>(w.c0), mat_of(t.m));
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// void rref_from_pls(MatrixWindow a, size_t rank, span<const size_t> q) — pls.cpp:128-155;
+// validation as pls.cpp:130-135.
+int f2_rref_from_pls(f2_matrix* a, f2_window w, uint64_t rank, const uint64_t* q, size_t qlen) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!a || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
+    if (rank > m || rank > n || qlen < rank) return fail(F2_INVALID_ARGUMENT, "rref_from_pls: rank out of range");
+    for (uint64_t t = 0; t < rank; ++t)
+        if (q[t] >= n || q[t] < t || (t > 0 && q[t] <= q[t - 1]))
+            return fail(F2_INVALID_ARGUMENT, "rref_from_pls: Q is not a pivot-column prefix");
+    if (m == 0 || n == 0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    std::vector<int64_t> qq(q, q + rank);
+    return rref_window(a, w, rank, qq);
+}
+
+// Echelonize: reduced row echelon form via PLS + rref_from_pls (the reference's
+// rref with Algorithm::pls, acceptance.cpp:39-44 / f2mat rref).  The RREF is
+// unique, so this equals gauss_rref / m4ri_rref / hybrid_rref on the same input.
+int f2_rref(f2_matrix* a, f2_window w, const f2_elim_config* cfg, uint64_t* rank) {
+    if (!a || !rank) return fail(F2_INVALID_ARGUMENT, "null argument");
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    }
+    const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
+    std::vector<uint64_t> p(m), q(n);
+    int rc = f2_pls_recursive(a, w, p.data(), m, q.data(), n, cfg, rank);
+    if (rc) return rc;
+    return f2_rref_from_pls(a, w, *rank, q.data(), static_cast<size_t>(*rank));
 }
 
 }  // extern "C"

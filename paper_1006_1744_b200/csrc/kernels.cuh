@@ -67,5 +67,8 @@ void launch_gather_rows(cudaStream_t s, const Mat& dst, const Mat& src, const in
                         int64_t nwords);
 void launch_col_swaps(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* q, int nsm);
 void setup_misc_kernels();
+void launch_rref_prepare(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp);
+void launch_rref_coeffs(cudaStream_t s, const Mat& S, int64_t rank, const int64_t* Qp, const Mat& Lrev, int nsm);
+void setup_rref_kernels();
 
 }  // namespace f2g

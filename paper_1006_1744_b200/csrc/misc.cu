@@ -236,3 +236,74 @@ void setup_misc_kernels() {
 }
 
 }  // namespace f2g
+
+namespace f2g {
+
+// rref_from_pls, step 1 (pls.cpp:137-138 with pls_echelon_factor, gauss.cpp:74-83):
+// row t < rank becomes S row t in original column order (1 at q[t], the packed bits
+// right of it, nothing left of it); rows >= rank become zero.
+__global__ void k_rref_prepare(Mat A, int64_t rank, const int64_t* Qp) {
+    const int64_t nw = (A.n + 63) >> 6;
+    const int64_t total = A.m * nw;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / nw, k = idx - i * nw;
+        uint64_t* wp = A.w + i * A.stride + k;
+        if (i >= rank) {
+            *wp = 0;
+            continue;
+        }
+        const int64_t q = Qp[i], lo = 64 * k;
+        uint64_t v = *wp;
+        if (q >= lo + 64) v = 0;
+        else if (q >= lo) {
+            const int b = static_cast<int>(q - lo);
+            v = (b == 63 ? 0ull : (v & (~0ull << (b + 1)))) | (1ull << b);
+        }
+        *wp = v;
+    }
+}
+
+// Coefficients of the backward substitution, row- and column-reversed so the
+// lower-triangular solver applies: Lrev[t'][l'] = S[rank-1-t'] at column q[rank-1-l'].
+// One CTA per output row, the S row staged in SMEM.
+__global__ void k_rref_coeffs(Mat S, int64_t rank, const int64_t* Qp, Mat Lrev) {
+    extern __shared__ uint64_t srow[];
+    const int64_t nws = (S.n + 63) >> 6, nwl = (rank + 63) >> 6;
+    for (int64_t tp = blockIdx.x; tp < rank; tp += gridDim.x) {
+        const uint64_t* row = S.w + (rank - 1 - tp) * S.stride;
+        __syncthreads();
+        for (int64_t k = threadIdx.x; k < nws; k += blockDim.x) srow[k] = row[k];
+        __syncthreads();
+        for (int64_t w = threadIdx.x; w < nwl; w += blockDim.x) {
+            uint64_t v = 0;
+            const int64_t l0 = 64 * w;
+            const int nb = static_cast<int>(rank - l0 < 64 ? rank - l0 : 64);
+            for (int b = 0; b < nb; ++b) {
+                const int64_t col = Qp[rank - 1 - (l0 + b)];
+                v |= ((srow[col >> 6] >> (col & 63)) & 1ull) << b;
+            }
+            Lrev.w[tp * Lrev.stride + w] = v;
+        }
+    }
+}
+
+void launch_rref_prepare(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp) {
+    const int64_t total = A.m * ((A.n + 63) >> 6);
+    if (total == 0) return;
+    int64_t g = (total + 255) / 256;
+    if (g > 148 * 32) g = 148 * 32;
+    k_rref_prepare<<<static_cast<int>(g), 256, 0, s>>>(A, rank, Qp);
+}
+
+void launch_rref_coeffs(cudaStream_t s, const Mat& S, int64_t rank, const int64_t* Qp, const Mat& Lrev, int nsm) {
+    if (rank == 0) return;
+    const int64_t g = rank < 8 * nsm ? rank : 8 * nsm;
+    k_rref_coeffs<<<static_cast<int>(g), 256, sizeof(uint64_t) * S.stride, s>>>(S, rank, Qp, Lrev);
+}
+
+void setup_rref_kernels() {
+    cudaFuncSetAttribute(k_rref_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+}  // namespace f2g

@@ -6,7 +6,8 @@ reference exists; the outputs are committed so the GPU box never needs it.
     python tests/golden/make_golden.py configs   # tests/golden/configs.json   (~10 min, 1 core)
 
 configs.json pins, for the five BASELINE.json configurations, the digest of the
-seeded input and of the reference's packed output, P and Q, plus the rank.
+seeded input and of the reference's packed output, P and Q, plus the rank, and
+(configs up to 2^31 bits) the digest of rref_from_pls applied to the recursive result.
 """
 import json
 import os
@@ -66,6 +67,12 @@ def configs(only=None):
                           q_digest=str(digest(Q)), q_prefix_identity=bool((Q[:r] == np.arange(r, dtype=np.uint64)).all()),
                           q_tail_nonidentity=int((Q[r:] != np.arange(r, cfg["n"], dtype=np.uint64)).sum()),
                           ref_seconds=round(dt, 2))
+            if p == "recursive" and cfg["m"] * cfg["n"] <= (1 << 31):
+                t2 = time.time()
+                rf = R.rref_from_pls(w, cfg["n"], r, Q[:r])
+                rec[p]["rref_digest"] = str(digest(rf))
+                rec[p]["rref_seconds"] = round(time.time() - t2, 2)
+                del rf
             print(name, p, rec[p], flush=True)
             del w, P, Q
         out[name] = rec
@@ -94,8 +101,11 @@ def small():
         cut = [8, 64, 4096, 1 << 30][i % 4]
         wm, Pm, Qm, rm = R.mmpf_pls(a, n)
         wr, Pr, Qr, rr = R.pls_recursive(a, n, cut)
+        rf = R.rref_from_pls(wr, n, rr, Qr[:rr])       # rref_via_pls, test_pls.cpp:21-25
+        gr, grr = R.gauss_rref(a, n)                   # gauss_rref, gauss.cpp:7-23
+        assert grr == rr and (gr == rf).all()
         cases.append(dict(m=m, n=n, density=d, seed=seed, cutoff=cut, a=a, mm_w=wm, mm_p=Pm, mm_q=Qm, mm_r=rm,
-                          rc_w=wr, rc_p=Pr, rc_q=Qr, rc_r=rr))
+                          rc_w=wr, rc_p=Pr, rc_q=Qr, rc_r=rr, rref_w=rf))
     flat = {}
     for i, c in enumerate(cases):
         for k, v in c.items():

@@ -65,6 +65,10 @@ class Oracle:
         L.f2o_digest.restype = C.c_uint64
         L.f2o_pls_check.argtypes = [u64p, u64p, sz, sz, sz, u64p, u64p]
         L.f2o_pls_check.restype = C.c_int
+        L.f2o_gauss_rref.argtypes = [u64p, sz, sz]
+        L.f2o_gauss_rref.restype = sz
+        L.f2o_rref_from_pls.argtypes = [u64p, sz, sz, sz, u64p, sz]
+        L.f2o_rref_from_pls.restype = C.c_int
 
     def randomize(self, m, n, density, seed):
         w = np.zeros((m, words(n)), dtype=np.uint64)
@@ -106,6 +110,18 @@ class Oracle:
         w = np.ascontiguousarray(w)
         return int(self.lib.f2o_digest(ptr(w), w.size))
 
+    def gauss_rref(self, w, n):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        r = self.lib.f2o_gauss_rref(ptr(w), w.shape[0], n)
+        return w, int(r)
+
+    def rref_from_pls(self, w, n, rank, q):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        q = np.ascontiguousarray(q, dtype=np.uint64)
+        if self.lib.f2o_rref_from_pls(ptr(w), w.shape[0], n, rank, ptr(q) if q.size else None, q.size):
+            raise ValueError("rref_from_pls: invalid_argument")
+        return w
+
 
 class RefLib:
     """The reference library itself (built from /root/reference sources)."""
@@ -119,6 +135,7 @@ class RefLib:
         L.ref_pls_recursive.argtypes = [u64p, sz, sz, C.c_uint, C.c_uint64, u64p, u64p, u64p]
         L.ref_gauss_pls.argtypes = [u64p, sz, sz, u64p, u64p, u64p]
         L.ref_rref_from_pls.argtypes = [u64p, sz, sz, C.c_uint64, u64p, sz]
+        L.ref_gauss_rref.argtypes = [u64p, sz, sz, u64p]
         L.ref_mul_m4rm.argtypes = [u64p, sz, sz, u64p, sz, C.c_uint, u64p]
         L.ref_mul_naive.argtypes = [u64p, sz, sz, u64p, sz, u64p]
         L.ref_trsm_lower_left_unit.argtypes = [u64p, sz, u64p, sz]
@@ -151,6 +168,20 @@ class RefLib:
 
     def gauss_pls(self, w, n):
         return self._pls(self.lib.ref_gauss_pls, w, n)
+
+    def gauss_rref(self, w, n):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        r = np.zeros(1, dtype=np.uint64)
+        assert self.lib.ref_gauss_rref(ptr(w), w.shape[0], n, ptr(r)) == 0
+        return w, int(r[0])
+
+    def rref_from_pls(self, w, n, rank, q):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        q = np.ascontiguousarray(q, dtype=np.uint64)
+        rc = self.lib.ref_rref_from_pls(ptr(w), w.shape[0], n, rank, ptr(q) if q.size else None, q.size)
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return w
 
     def mul_m4rm(self, a, s, b, n, k=0):
         m = a.shape[0]

@@ -54,3 +54,18 @@ def test_config_against_reference_digests(f2, oracle, name):
         assert digest(res.P) == int(ref["p_digest"]), path
         assert digest(res.Q) == int(ref["q_digest"]), path
         assert a.digest() == int(ref["packed_digest"]), path
+        if "rref_digest" in ref:
+            f2.rref_from_pls(a, res.rank, res.Q[:res.rank])
+            assert a.digest() == int(ref["rref_digest"]), "rref_from_pls"
+
+
+def test_config3_rref_is_identity(f2):
+    """Size-independent property at full size: config 3 has full rank, so its RREF
+    (pls_recursive + rref_from_pls, a 65536-row backward substitution) is I."""
+    a = f2.DeviceMatrix(65536, 65536)
+    a.randomize(0.5, 3)
+    assert f2.rref(a, f2.EliminationConfig(cutoff_bytes=2 << 20)) == 65536
+    idw = np.zeros((65536, 1024), np.uint64)
+    i = np.arange(65536)
+    idw[i, i // 64] = np.uint64(1) << (i % 64).astype(np.uint64)
+    assert a.digest() == digest(idw)
