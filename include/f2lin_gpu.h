@@ -37,7 +37,8 @@ enum f2_status {
     F2_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference      */
     F2_CUDA_ERROR = 3,
     F2_NO_DEVICE = 4,
-    F2_OUT_OF_MEMORY = 5
+    F2_OUT_OF_MEMORY = 5,
+    F2_FORMAT_ERROR = 6      /* io::FormatError in the reference            */
 };
 
 /* enum class Algorithm — pls.hpp:18 */
@@ -145,6 +146,23 @@ int f2_recursive_q(size_t m, size_t n, uint64_t cutoff, uint64_t rank, const uin
 void* f2_device_alloc(size_t bytes);
 void f2_device_free(void* p);
 int f2_device_copy(void* dst, const void* src, size_t bytes, int kind);
+
+/* ---- on-disk formats (io.hpp:3-11, io.cpp) ------------------------------ */
+enum f2_format { F2_FMT_ASCII = 0, F2_FMT_BINARY = 1 }; /* io::Format (io.hpp:22) */
+/* header only: dimensions and the sniffed format (io.cpp:118-126) */
+int f2_io_probe(const char* path, uint64_t* nrows, uint64_t* ncols, int* format);
+/* io::read_matrix(path) into a host buffer of the probed shape (any row stride >= ceil(n/64)) */
+int f2_io_read_host(const char* path, uint64_t* words, size_t stride_words, uint64_t nrows, uint64_t ncols);
+/* io::write_matrix(path, a, fmt) from a host buffer */
+int f2_io_write_host(const char* path, const uint64_t* words, size_t stride_words, uint64_t nrows, uint64_t ncols,
+                     int format);
+/* io::read_matrix(path, &detected) straight into HBM (pinned double-buffered stream) */
+int f2_matrix_load(const char* path, f2_matrix** out, int* detected);
+/* io::write_matrix(path, a, fmt) straight from HBM */
+int f2_matrix_store(const f2_matrix* a, const char* path, int format);
+/* io::write_permutation / read_permutation (io.cpp:135-160); *len always set, entries copied when len <= cap */
+int f2_write_permutation(const char* path, const uint64_t* p, size_t len);
+int f2_read_permutation(const char* path, uint64_t* p, size_t cap, size_t* len);
 
 /* ---- instrumentation (bench.py roofline) -------------------------------- */
 /* When enabled, the library brackets every launch of kernel family `kind`

@@ -8,6 +8,7 @@
 //   gauss_pls           (proj/src/gauss.cpp:26-55)
 //   rref_from_pls       (proj/src/pls.cpp:128-161)
 //   gauss_rref          (proj/src/gauss.cpp:7-23)
+//   io::read/write_matrix, read/write_permutation (proj/src/io.cpp)
 //   mul_m4rm / addmul   (proj/src/mul.cpp:90-107)
 //   trsm_*_left_unit    (proj/src/mul.cpp:109-157)
 //   BitMatrix::randomize(proj/src/bitmat.cpp:136-154)
@@ -20,6 +21,8 @@
 #include <vector>
 
 #include <f2lin/gauss.hpp>
+#include <f2lin/io.hpp>
+#include <filesystem>
 #include <f2lin/mmpf.hpp>
 #include <f2lin/mul.hpp>
 #include <f2lin/perm.hpp>
@@ -50,6 +53,8 @@ int guard(F&& f) {
         return 1;
     } catch (const std::out_of_range&) {
         return 2;
+    } catch (const io::FormatError&) {
+        return 6;
     } catch (...) {
         return 9;
     }
@@ -158,5 +163,42 @@ int ref_trsm_upper_left_unit(const uint64_t* u, size_t r, uint64_t* b, size_t n)
 size_t ref_default_cutoff_bytes() { return default_cutoff_bytes(); }
 
 unsigned ref_auto_table_bits(size_t dim) { return detail::auto_table_bits(dim); }
+
+// io::write_matrix(path, a, fmt) — fmt 0 ascii, 1 binary
+int ref_write_matrix(const char* path, const uint64_t* w, size_t m, size_t n, int fmt) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        io::write_matrix(std::filesystem::path(path), a, fmt ? io::Format::binary : io::Format::ascii);
+    });
+}
+
+// io::read_matrix(path): dims and format always reported; words copied when they fit
+int ref_read_matrix(const char* path, uint64_t* w, size_t cap_words, uint64_t* m, uint64_t* n, int* fmt) {
+    return guard([&] {
+        io::Format f;
+        BitMatrix a = io::read_matrix(std::filesystem::path(path), &f);
+        *m = a.nrows();
+        *n = a.ncols();
+        *fmt = f == io::Format::binary ? 1 : 0;
+        if (w && a.nrows() * a.stride() <= cap_words) store(a, w);
+    });
+}
+
+int ref_write_permutation(const char* path, const uint64_t* p, size_t len) {
+    return guard([&] {
+        Permutation q = Permutation::identity(len);
+        for (size_t i = 0; i < len; ++i) q[i] = p[i];
+        io::write_permutation(std::filesystem::path(path), q);
+    });
+}
+
+int ref_read_permutation(const char* path, uint64_t* p, size_t cap, size_t* len) {
+    return guard([&] {
+        Permutation q = io::read_permutation(std::filesystem::path(path));
+        *len = q.size();
+        if (p && q.size() <= cap)
+            for (size_t i = 0; i < q.size(); ++i) p[i] = q[i];
+    });
+}
 
 } // extern "C"

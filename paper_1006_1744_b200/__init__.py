@@ -38,13 +38,13 @@ __all__ = [
     "mmpf_pls_host", "pls_recursive_host", "addmul", "mul_m4rm", "trsm_lower_left_unit", "compress_columns",
     "apply_rows", "default_cutoff_bytes", "auto_table_bits", "NoDeviceError", "F2Error", "host_words",
     "pinned_empty", "stats_enable", "stats_get", "stats_reset", "last_launch_count", "set_panel_bits",
-    "timer_start", "timer_stop", "set_device",
+    "timer_start", "timer_stop", "set_device", "rref_from_pls", "rref", "FormatError",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libf2gpu.so")
 
-F2_OK, F2_INVALID_ARGUMENT, F2_OUT_OF_RANGE, F2_CUDA_ERROR, F2_NO_DEVICE, F2_OUT_OF_MEMORY = range(6)
+F2_OK, F2_INVALID_ARGUMENT, F2_OUT_OF_RANGE, F2_CUDA_ERROR, F2_NO_DEVICE, F2_OUT_OF_MEMORY, F2_FORMAT_ERROR = range(7)
 ALG_GAUSS, ALG_M4RI, ALG_MMPF, ALG_PLS, ALG_HYBRID = range(5)
 
 
@@ -54,6 +54,10 @@ class F2Error(RuntimeError):
 
 class NoDeviceError(F2Error):
     pass
+
+
+class FormatError(F2Error):
+    """io::FormatError (io.hpp:24-26)."""
 
 
 class _Window(C.Structure):
@@ -103,6 +107,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_rref_from_pls": ([vp, _Window, C.c_uint64, _u64p, sz], i),
         "f2_rref": ([vp, _Window, C.POINTER(_Cfg), _u64p], i),
         "f2_default_cutoff_bytes": ([], C.c_uint64),
+        "f2_io_probe": ([C.c_char_p, _u64p, _u64p, C.POINTER(i)], i),
+        "f2_io_read_host": ([C.c_char_p, _u64p, sz, C.c_uint64, C.c_uint64], i),
+        "f2_io_write_host": ([C.c_char_p, _u64p, sz, C.c_uint64, C.c_uint64, i], i),
+        "f2_matrix_load": ([C.c_char_p, C.POINTER(vp), C.POINTER(i)], i),
+        "f2_matrix_store": ([vp, C.c_char_p, i], i),
+        "f2_write_permutation": ([C.c_char_p, _u64p, sz], i),
+        "f2_read_permutation": ([C.c_char_p, _u64p, sz, C.POINTER(sz)], i),
         "f2_auto_table_bits": ([sz], C.c_uint),
         "f2_addmul": ([vp, _Window, vp, _Window, vp, _Window, C.c_uint], i),
         "f2_mul_m4rm": ([vp, vp, C.c_uint, C.POINTER(vp)], i),
@@ -138,6 +149,8 @@ def _check(rc: int) -> None:
         raise NoDeviceError(msg)
     if rc == F2_OUT_OF_MEMORY:
         raise MemoryError(msg)
+    if rc == F2_FORMAT_ERROR:
+        raise FormatError(msg)
     raise F2Error(f"CUDA error: {msg}")
 
 

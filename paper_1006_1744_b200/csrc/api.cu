@@ -493,6 +493,16 @@ extern "C" {
 
 const char* f2_last_error(void) { return g_err.c_str(); }
 
+}  // extern "C"
+
+namespace f2g {
+// for the host-side modules (io.cu): same thread-local message as fail()
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+int set_cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+}  // namespace f2g
+
+extern "C" {
+
 int f2_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -4,6 +4,7 @@ reference exists; the outputs are committed so the GPU box never needs it.
 
     python tests/golden/make_golden.py small     # tests/golden/small_cases.npz (seconds)
     python tests/golden/make_golden.py configs   # tests/golden/configs.json   (~10 min, 1 core)
+    python tests/golden/make_golden.py io        # tests/golden/io/ (files written by io::write_*)
 
 configs.json pins, for the five BASELINE.json configurations, the digest of the
 seeded input and of the reference's packed output, P and Q, plus the rank, and
@@ -115,9 +116,43 @@ def small():
     print("wrote", len(cases), "small cases")
 
 
+def io_fixtures():
+    """Files written by the reference's io::write_matrix / write_permutation
+    (io.cpp) + the words they hold: tests/golden/io/."""
+    import ctypes as C
+    R = RefLib()
+    d = os.path.join(HERE, "io")
+    os.makedirs(d, exist_ok=True)
+    u64p = C.POINTER(C.c_uint64)
+    R.lib.ref_write_matrix.argtypes = [C.c_char_p, u64p, C.c_size_t, C.c_size_t, C.c_int]
+    R.lib.ref_write_permutation.argtypes = [C.c_char_p, u64p, C.c_size_t]
+    rng = np.random.default_rng(1744)
+    shapes = [(2, 3), (1, 65), (0, 5), (3, 0), (1, 1), (7, 64), (9, 130), (33, 200), (40, 127), (5, 1000)]
+    flat = {}
+    for i, (m, n) in enumerate(shapes):
+        a = R.randomize(m, n, [0.4, 0.5, 0.1][i % 3], int(rng.integers(1, 2 ** 62)))
+        if (m, n) == (2, 3):
+            a = np.array([[0b101], [0b010]], np.uint64)          # test_io.cpp:12-21
+        if (m, n) == (1, 65):
+            a = np.array([[1, 1]], np.uint64)                     # test_io.cpp:23-39
+        flat[f"m{i}"] = a
+        flat[f"n{i}"] = np.asarray(n)
+        for fmt, ext in [(0, "txt"), (1, "bmf2")]:
+            path = os.path.join(d, f"mat{i}_{m}x{n}.{ext}").encode()
+            buf = np.ascontiguousarray(a) if a.size else np.zeros(1, np.uint64)
+            assert R.lib.ref_write_matrix(path, buf.ctypes.data_as(u64p), m, n, fmt) == 0
+    flat["count"] = np.asarray(len(shapes))
+    np.savez_compressed(os.path.join(d, "matrices.npz"), **flat)
+    p = np.array([2, 1, 2, 3], np.uint64)                         # test_io.cpp:81-89
+    assert R.lib.ref_write_permutation(os.path.join(d, "perm4.txt").encode(), p.ctypes.data_as(u64p), 4) == 0
+    print("wrote io fixtures to", d)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
         small()
+    elif what == "io":
+        io_fixtures()
     else:
         configs(sys.argv[2:] or None)
