@@ -180,6 +180,8 @@ int f2_timer_stop(double* ms);
 uint64_t f2_last_launch_count(void);
 /* phase clocks of the last leaf (only builds compiled with -DF2_LEAF_PROFILE fill them) */
 int f2_debug_clocks(long long* out, int n);
+/* globaltimer stamps of the panel kernel (only builds compiled with -DF2_PANEL_PROFILE fill them) */
+int f2_debug_prof(long long* out, int n);
 /* engine tuning (panel width in bits for pls_recursive; 0 = default) */
 int f2_set_panel_bits(unsigned bits);
 

@@ -54,6 +54,8 @@ struct Ctx {
     int64_t* P = nullptr;
     int64_t* Qp = nullptr;
     int64_t* pmap = nullptr;
+    unsigned* bar = nullptr;  // grid barrier counter of k_panel_leaves
+    bool fused = true;        // panel leaves in one persistent kernel (F2_UNFUSED=1: three launches per leaf)
     uint64_t* scratch = nullptr;
     size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
@@ -109,6 +111,9 @@ int ensure_init() {
     setup_m4rm_kernels();
     setup_misc_kernels();
     setup_rref_kernels();
+    setup_panel_kernels();
+    CK(cudaMalloc(&g.bar, sizeof(unsigned)));
+    g.fused = !(std::getenv("F2_UNFUSED") && std::getenv("F2_UNFUSED")[0] == '1');
     CK(cudaGetLastError());
     g.init = true;
     return F2_OK;
@@ -263,20 +268,25 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         const int64_t cw = std::min<int64_t>(W, n - c);
         const int nleaves = static_cast<int>((cw + 63) / 64);
         const int64_t pw0 = c / 64, pw1 = pw0 + nleaves;
-        for (int j = 0; j < nleaves; ++j) {
-            const int64_t wl = pw0 + j;
-            const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
-            {
-                LaunchTimer t(1, 0, 0);
-                launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, 0);
-            }
-            {
-                LaunchTimer t(3, 0, 0);
-                launch_leaf_tables(s, g.st, j);
-            }
-            {
-                LaunchTimer t(3, 0, 0);
-                launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
+        if (g.fused) {
+            LaunchTimer t(1, 0, 0);
+            launch_panel_leaves(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
+        } else {
+            for (int j = 0; j < nleaves; ++j) {
+                const int64_t wl = pw0 + j;
+                const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
+                {
+                    LaunchTimer t(1, 0, 0);
+                    launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, 0);
+                }
+                {
+                    LaunchTimer t(3, 0, 0);
+                    launch_leaf_tables(s, g.st, j);
+                }
+                {
+                    LaunchTimer t(3, 0, 0);
+                    launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
+                }
             }
         }
         {
@@ -793,6 +803,14 @@ int f2_timer_stop(double* ms) {
 }
 
 // phase clocks recorded by builds compiled with -DF2_LEAF_PROFILE (development aid)
+int f2_debug_prof(long long* out, int n) {
+    if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
+    long long tmp[64];
+    CK(cudaMemcpy(tmp, &g.st->prof[0], sizeof(tmp), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 64; ++i) out[i] = tmp[i];
+    return F2_OK;
+}
+
 int f2_debug_clocks(long long* out, int n) {
     if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
     long long tmp[32];
@@ -1050,12 +1068,17 @@ int f2_dist_factor_panel(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t
     cudaStream_t s = g.stream;
     launch_set_r(s, g.st, static_cast<int64_t>(r));
     const int64_t qoff = static_cast<int64_t>(panel_col) - static_cast<int64_t>(pw0) * 64;
-    for (int j = 0; j < nleaves; ++j) {
-        const int64_t wl = static_cast<int64_t>(pw0) + j;
-        const int lw = static_cast<int>(std::min<int64_t>(64, static_cast<int64_t>(width_bits) - 64 * j));
-        launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, qoff);
-        launch_leaf_tables(s, g.st, j);
-        launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
+    if (g.fused) {
+        launch_panel_leaves(s, A, static_cast<int64_t>(pw0), static_cast<int>(width_bits), pw1, g.st, g.P, g.Qp,
+                            g.pmap, qoff, g.bar, g.nsm);
+    } else {
+        for (int j = 0; j < nleaves; ++j) {
+            const int64_t wl = static_cast<int64_t>(pw0) + j;
+            const int lw = static_cast<int>(std::min<int64_t>(64, static_cast<int64_t>(width_bits) - 64 * j));
+            launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, qoff);
+            launch_leaf_tables(s, g.st, j);
+            launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
+        }
     }
     launch_dist_export(s, g.st, g.pmap, g.P, reinterpret_cast<int64_t*>(hdr_dev), nleaves * 64);
     launch_perm(s, A, nw, g.st, g.pmap, g.scratch);

@@ -51,7 +51,40 @@ struct PlsState {
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
     int64_t moved[kMaxMoved];           // positions with pmap[x] != x (may repeat)
     long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)
+    long long prof[64];                 // globaltimer stamps (F2_PANEL_PROFILE builds only)
 };
+
+// Leaf update geometry (leafupd.cu): kLuRPT rows per quarter-warp lane group, 1024-bit
+// column tiles; dynamic smem X[64][kLuTNW] | T[2][256][kLuTNW] | F[8][256] | cbuf | pbuf.
+constexpr int kLuRPT = 4;
+constexpr int kLuTNW = 16;
+constexpr size_t leaf_update_smem(int nthreads) {
+    return sizeof(uint64_t) * (64 * kLuTNW + 2 * 256 * kLuTNW + 8 * 256 + 2 * ((nthreads / 32) * 4 * kLuRPT));
+}
+
+// Loads of data other CTAs may have written during the same (persistent) kernel go
+// through L2 (ld.global.cg): the per-SM L1 is not coherent.
+__device__ __forceinline__ uint64_t ldw(const uint64_t* p) {
+    return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ int64_t ldi(const int64_t* p) { return __ldcg(reinterpret_cast<const long long*>(p)); }
+
+#ifdef F2_PANEL_PROFILE
+static __device__ int g_prof_on = 0;
+#define F2_STAMP(stp, k)                                                               \
+    do {                                                                               \
+        if (g_prof_on && threadIdx.x == 0 && blockIdx.x == 0) {                                       \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            const_cast<PlsState*>(stp)->prof[k] = static_cast<long long>(t_);          \
+            const_cast<PlsState*>(stp)->dbg[(k) & 31] = clock64();                     \
+        }                                                                              \
+    } while (0)
+#else
+#define F2_STAMP(stp, k) \
+    do {                 \
+    } while (0)
+#endif
 
 // How a table-apply launch finds its C/A rows (device-side offsets).
 enum RowMode : int { ROWS_STATIC = 0, ROWS_AFTER_LEAF = 1, ROWS_AFTER_PANEL = 2 };
