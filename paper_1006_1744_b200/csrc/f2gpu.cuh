@@ -40,6 +40,7 @@ struct PlsState {
     int64_t panel_kb;  // pivots found so far in the current panel
     int32_t nmoved;    // positions whose pmap entry changed during the panel
     int32_t pad0;
+    int64_t pmap_hi;   // pmap[x] == x for every position x >= pmap_hi (this panel)
     uint64_t leaf_mask;                 // pivot columns within the leaf word
     uint64_t ustrict[64];               // leaf pivot words, bits <= pivot cleared
     uint64_t ufull[64];                 // leaf pivot words (L bits, leading 1, S bits)
@@ -50,6 +51,8 @@ struct PlsState {
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
     int64_t moved[kMaxMoved];           // positions with pmap[x] != x (may repeat)
+    uint64_t uleaf[64][16];             // the current leaf's solved pivot rows over the rest of the panel
+    uint64_t fbasis[64];                // the current leaf's finalize basis (see panel.cu)
     long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)
     long long prof[64];                 // globaltimer stamps (F2_PANEL_PROFILE builds only)
 };

@@ -23,7 +23,7 @@ namespace f2g {
 __global__ void __launch_bounds__(1024, 1)
 k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, int panel_bits,
              PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off) {
-    leaf_pivot_body(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, wl + 1);
+    leaf_pivot_body(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, wl + 1, nullptr);
 }
 
 __global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st, int leaf_in_panel) {

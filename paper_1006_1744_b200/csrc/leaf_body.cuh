@@ -121,7 +121,6 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
 
 struct FastSmem {
     uint32_t colw[64 * 4];       // leaf columns: 4 x 32 slots each
-    uint64_t rest[128 * 15];     // window rows' pre-leaf words wl+1.. (row form)
     uint64_t linv[64];           // rows of L11^{-1} over pivot indices
     int64_t phys[128];           // pre-leaf physical row of each slot
     int step_p[64], step_c[64];  // pivot steps
@@ -133,14 +132,19 @@ struct FastSmem {
 
 static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, int lw, int first_in_panel,
                                                     int leaf_in_panel, int panel_bits, PlsState* st, int64_t* P,
-                                                    int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1) {
+                                                    int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1,
+                                                    uint64_t* scratch) {
     constexpr int kFW = 128;
     __shared__ FastSmem F;
+    // scratch (dynamic smem, >= (128 + 256) * 15 words when solving): window rows'
+    // pre-leaf rest words (row form), then the 4-bit tables over the pivot rows' ones
+    uint64_t* const Frest = scratch;
+    uint64_t* const Ft16 = scratch + 128 * 15;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = A.m, stride = A.stride;
     const int64_t base = st->r;
     const int64_t span = m - base;
-    const int nrest = rw1 > wl + 1 ? static_cast<int>(rw1 - wl - 1) : 0;  // <= 15
+    const int nrest = (scratch && rw1 > wl + 1) ? static_cast<int>(rw1 - wl - 1) : 0;  // <= 15
 
     if (tid < kFW) F.phys[tid] = tid < span ? ldi(pmap + base + tid) : -1;
     __syncthreads();
@@ -154,7 +158,7 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
     for (int i = tid; i < kFW * nrest; i += blockDim.x) {  // rest of the panel, row form
         const int sl = i / nrest, k = i - sl * nrest;
         const int64_t ph = F.phys[sl];
-        F.rest[sl * 15 + k] = ph >= 0 ? ldw(A.w + ph * stride + wl + 1 + k) : 0ull;
+        Frest[sl * 15 + k] = ph >= 0 ? ldw(A.w + ph * stride + wl + 1 + k) : 0ull;
     }
     __syncthreads();
     F2_STAMP(st, 16);
@@ -237,64 +241,102 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
     const int kb = F.final_kb;
     if (kb < 0) return false;
 
-    // slot sources: walk the transpositions backwards (LAPACK order, perm.cpp:8-16)
     if (tid < kFW) {
+        // slot sources: walk the transpositions backwards (LAPACK order, perm.cpp:8-16)
         int x = tid;
-        for (int u = kb - 1; u >= 0; --u) {
-            const int pu = F.step_p[u];
-            x = x == u ? pu : (x == pu ? u : x);
+        for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
+            int pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pv[i] = F.step_p[u0 + i];
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                const int u = u0 + i;
+                if (u < kb) x = x == u ? pv[i] : (x == pv[i] ? u : x);
+            }
         }
         F.src[tid] = x;
-    }
-    if (first_in_panel)
-        for (int i = tid; i < panel_bits; i += blockDim.x) st->brow[i] = -1;
-    __syncthreads();
-    F2_STAMP(st, 19);
-    // solved rest words of the pivot rows: U_l = sum over t of Linv[l][t] A12(src_t)
-    for (int i = tid; i < kb * nrest; i += blockDim.x) {
-        const int l = i / nrest, k = i - l * nrest;
-        uint64_t lv = F.linv[l], acc = 0;
-        while (lv) {
-            const int tt = __ffsll(static_cast<long long>(lv)) - 1;
-            lv &= lv - 1;
-            acc ^= F.rest[F.src[tt] * 15 + k];
+    } else if (tid < kFW + 64) {
+        // finalize basis for the update (see panel.cu): the elimination chain of byte
+        // group g (gauss.cpp:47-49) run on the single bit b
+        const int e = tid - kFW, g = e >> 3, b = e & 7;
+        int lo = 0, hi = kb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (F.step_c[mid] < 8 * g) lo = mid + 1;
+            else hi = mid;
         }
-        A.w[F.phys[F.src[l]] * stride + wl + 1 + k] = acc;
-    }
-    const int mv0 = first_in_panel ? 0 : static_cast<int>(st->nmoved);
-    // re-mapped positions (pre-leaf pmap values are in F.phys)
-    int moved = 0, off = 0;
-    if (warp < 4) {
-        const int s = tid;
-        moved = s < span && F.src[s] != s;
-        const unsigned b = __ballot_sync(FULL, moved);
-        off = __popc(b & ((1u << lane) - 1));
-        if (lane == 0) F.wcount[warp] = __popc(b);
-    }
-    __syncthreads();
-    if (warp < 4 && moved) {
-        int o = off;
-        for (int w2 = 0; w2 < warp; ++w2) o += F.wcount[w2];
-        pmap[base + tid] = F.phys[F.src[tid]];
-        st->moved[mv0 + o] = base + tid;
-    }
-    // pivot rows: final leaf word; P, Q
-    for (int l = tid; l < kb; l += blockDim.x) {
-        A.w[F.phys[F.src[l]] * stride + wl] = F.uf[l];
-        P[base + l] = base + F.step_p[l];
-        Qp[base + l] = qcol_off + wl * 64 + F.step_c[l];
-    }
-    const int64_t pkb = first_in_panel ? 0 : st->panel_kb;
-    for (int l = tid; l < 64; l += blockDim.x) {
+        uint64_t x = 1ull << (8 * g + b), corr = 0;
+        for (int l = lo; l < kb && F.step_c[l] < 8 * g + 8; ++l) {
+            const int q = F.step_c[l];
+            if ((x >> q) & 1ull) {
+                const uint64_t ul = F.uf[l] & above(q);
+                x ^= ul;
+                corr ^= ul;
+            }
+        }
+        st->fbasis[e] = corr;
+    } else if (tid >= 256 && tid < 320) {
+        const int l = tid - 256;
         const bool in = l < kb;
         const int q = in ? F.step_c[l] : 64;
         st->ustrict[l] = in ? F.uf[l] & above(q) : 0ull;
         st->ufull[l] = in ? F.uf[l] : 0ull;
         st->q[l] = q;
-        if (in) {
-            st->panel_q[pkb + l] = leaf_in_panel * 64 + q;
-            st->brow[leaf_in_panel * 64 + q] = base + l;
-        }
+    }
+    if (first_in_panel)
+        for (int i = tid; i < panel_bits; i += blockDim.x) st->brow[i] = -1;
+    __syncthreads();
+    F2_STAMP(st, 19);
+    const int mv0 = first_in_panel ? 0 : static_cast<int>(st->nmoved);
+    const int64_t pkb = first_in_panel ? 0 : st->panel_kb;
+    // re-mapped positions (pre-leaf pmap values are in F.phys)
+    int moved = 0, off = 0;
+    if (warp < 4) {
+        const int s = tid;
+        moved = s < span && F.src[s] != s;
+        const unsigned bm = __ballot_sync(FULL, moved);
+        off = __popc(bm & ((1u << lane) - 1));
+        if (lane == 0) F.wcount[warp] = __popc(bm);
+    }
+    // pivot rows: final leaf word; P, Q; the panel's pivot bookkeeping
+    for (int l = tid; l < kb; l += blockDim.x) {
+        A.w[F.phys[F.src[l]] * stride + wl] = F.uf[l];
+        P[base + l] = base + F.step_p[l];
+        Qp[base + l] = qcol_off + wl * 64 + F.step_c[l];
+        st->panel_q[pkb + l] = leaf_in_panel * 64 + F.step_c[l];
+        st->brow[leaf_in_panel * 64 + F.step_c[l]] = base + l;
+    }
+    F2_STAMP(st, 21);
+    // solved rest words of the pivot rows: U_l = sum over t of Linv[l][t] A12_t with
+    // A12_t = the pre-leaf rest words of the row that became pivot t (slot src_t):
+    // sixteen 4-bit tables over A12 (T16[g][e] = xor of A12_{4g+b}, b in e), then 16
+    // independent lookups per output word
+    for (int i = tid; i < 16 * 16 * nrest; i += blockDim.x) {
+        const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
+        uint64_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (((e >> b) & 1) && 4 * g + b < kb) v ^= Frest[F.src[4 * g + b] * 15 + k];
+        Ft16[ge * 15 + k] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < kb * nrest; i += blockDim.x) {
+        const int l = i / nrest, k = i - l * nrest;
+        const uint64_t lv = F.linv[l];
+        uint64_t acc = 0;
+#pragma unroll
+        for (int g = 0; g < 16; ++g) acc ^= Ft16[((g << 4) | static_cast<int>((lv >> (4 * g)) & 15u)) * 15 + k];
+        A.w[F.phys[F.src[l]] * stride + wl + 1 + k] = acc;
+        st->uleaf[l][k] = acc;
+    }
+    F2_STAMP(st, 22);
+    __syncthreads();
+    F2_STAMP(st, 23);
+    if (warp < 4 && moved) {
+        int o = off;
+        for (int w2 = 0; w2 < warp; ++w2) o += F.wcount[w2];
+        pmap[base + tid] = F.phys[F.src[tid]];
+        st->moved[mv0 + o] = base + tid;
     }
     if (warp == 0) {
         uint64_t mk = 0;
@@ -302,9 +344,15 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
         mk = warp_or64(mk);
         int nm = 0;
         for (int w2 = 0; w2 < 4; ++w2) nm += F.wcount[w2];
+        int hi = -1;  // highest re-mapped slot
+        for (int w2 = 3; w2 >= 0 && hi < 0; --w2)
+            if (F.wcount[w2]) hi = w2;
         if (lane == 0) {
             st->leaf_mask = mk;
             st->nmoved = mv0 + nm;
+            const int64_t h = hi < 0 ? 0 : base + 32 * (hi + 1);
+            const int64_t prev = first_in_panel ? 0 : st->pmap_hi;
+            st->pmap_hi = h > prev ? h : prev;
             st->leaf_r = base;
             st->leaf_kb = kb;
             st->r = base + kb;
@@ -335,8 +383,9 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
 // rows over words wl+1..rw1); false after the general search.
 static __device__ __noinline__ bool leaf_pivot_body(const Mat& A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel,
                                 int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap,
-                                int64_t qcol_off, int64_t rw1) {
-    if (leaf_pivot_fast(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, rw1))
+                                int64_t qcol_off, int64_t rw1, uint64_t* scratch) {
+    if (leaf_pivot_fast(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, rw1,
+                        scratch))
         return true;
     __syncthreads();
     __shared__ uint64_t s_u[64];
@@ -667,6 +716,7 @@ static __device__ __noinline__ bool leaf_pivot_body(const Mat& A, int64_t wl, in
     for (int l = tid; l < kb; l += blockDim.x) A.w[pmap[base + l] * stride + wl] = s_uf[l];
     if (tid == 0) {
         st->nmoved = mv0 + nmv_all;
+        st->pmap_hi = m;  // outside swaps may have re-mapped any position
         st->leaf_r = base;
         st->leaf_kb = kb;
         st->r = base + kb;

@@ -36,9 +36,11 @@ namespace {
 constexpr int kPT = 1024;                  // threads per CTA
 constexpr int kRows = (kPT / 32) * 4 * 4;  // rows per update tile (512): 4 lane groups x 4 rows per warp
 constexpr int kW = 16;                     // words of the panel remainder a tile covers (W <= 1024)
-constexpr int kTab = 256 * kW;             // one group table, words
-// dynamic smem: tables[4][256][kW] | X[64][kW] | F[8][256] | cbuf[kRows] | pbuf[kRows]
-constexpr size_t kSmem = sizeof(uint64_t) * (4 * kTab + 64 * kW + 8 * 256 + 2 * kRows);
+constexpr int kTab = 256 * kW;             // one 8-bit group table (CTA 0's fallback solve), words
+// dynamic smem: tab[256][kW] (8-bit table of the fallback solve, or the sixteen 4-bit
+// tables T4[16][16][kW] of the update) | X[64][kW] | F[8][256]
+constexpr size_t kSmem = sizeof(uint64_t) * (kTab + 64 * kW + 8 * 256);
+static_assert(kSmem >= sizeof(uint64_t) * (128 + 256) * 15, "CTA 0's fast path scratch");
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
     __syncthreads();
@@ -55,6 +57,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
     }
     __syncthreads();
 }
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
 
 __device__ __forceinline__ uint4 lds128(const void* p) {
     uint4 v;
@@ -74,6 +78,7 @@ struct LeafInfo {
     uint8_t rb[64];   // per group: rows of the inverse 8x8 L block (M[g][e] = xor of rb[8g+b])
     int kb;
     int64_t r0;
+    int64_t pmap_hi;  // positions >= pmap_hi are not re-mapped
 };
 
 // Loads the current leaf's pivots (st written by CTA 0 before the barrier) and
@@ -83,6 +88,7 @@ __device__ void load_leaf(const PlsState* st, LeafInfo& L) {
     if (tid == 0) {
         L.kb = static_cast<int>(ldi(&st->leaf_kb));
         L.r0 = ldi(&st->leaf_r);
+        L.pmap_hi = ldi(&st->pmap_hi);
     }
     if (tid < 64) {
         L.u[tid] = ldw(&st->ustrict[tid]);
@@ -93,9 +99,13 @@ __device__ void load_leaf(const PlsState* st, LeafInfo& L) {
     __syncthreads();
     const int kb = L.kb;
     if (tid < kb) L.pos[L.q[tid]] = tid;
-    if (tid <= 8) {
-        int lo = 0;
-        while (lo < kb && L.q[lo] < 8 * tid) ++lo;
+    if (tid <= 8) {  // first pivot of group tid: lower bound of 8*tid in the sorted q
+        int lo = 0, hi = kb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (L.q[mid] < 8 * tid) lo = mid + 1;
+            else hi = mid;
+        }
         L.gs[tid] = lo;
     }
     __syncthreads();
@@ -141,7 +151,7 @@ __device__ __forceinline__ unsigned mgroup(const LeafInfo& L, int g, unsigned e)
 // CTA 0, after the pivot search: U = L11^{-1} A12 on the pivot rows' words [rw0, rw1),
 // written back in place (the pivot rows sit at positions r0 .. r0+kb via pmap).
 __device__ void solve_pivot_rows(const Mat& A, int64_t rw0, int64_t rw1, const int64_t* pmap, const LeafInfo& L,
-                                 uint64_t* X, uint64_t* tb, const PlsState* st_prof) {
+                                 uint64_t* X, uint64_t* tb, PlsState* st_out) {
     const int kb = L.kb, tid = threadIdx.x;
     const int ntw = rw1 > rw0 ? static_cast<int>(rw1 - rw0) : 0;
     if (kb == 0 || ntw == 0) return;
@@ -194,121 +204,134 @@ __device__ void solve_pivot_rows(const Mat& A, int64_t rw0, int64_t rw1, const i
             X[t * kW + k] ^= tb[mgroup(L, g, cb) * kW + k];
         }
         __syncthreads();
-        F2_STAMP(st_prof, 40 + g);
+        F2_STAMP(st_out, 40 + g);
     }
     for (int i = tid; i < kb * kW; i += kPT) {
         const int t = i / kW, k = i % kW;
         if (k < ntw) A.w[ldi(pmap + L.r0 + t) * A.stride + rw0 + k] = X[i];
+        st_out->uleaf[t][k] = X[i];
     }
 }
 
-// One 512-row tile below the pivots (positions r0 + kb + ty*kRows ...).
-__device__ void update_tile(const Mat& A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap,
-                            const LeafInfo& L, int ty, const uint64_t* X, const uint64_t* F, uint64_t* tabs,
-                            uint64_t* cbuf, int64_t* pbuf, const PlsState* st_prof) {
+// Worker preparation for one leaf (every CTA, after the barrier): one round of
+// loads of what CTA 0 published -- pivot columns, the finalize basis and the solved
+// pivot rows -- then the finalize tables F[g][v] (xor of the basis over v's bits) and
+// the sixteen 4-bit tables T4[g][e] = xor of the solved pivot rows at the pivot
+// columns of e's bits in nibble g (word 0 of every entry, the leaf column, is 0).
+__device__ void worker_prep(const PlsState* st, LeafInfo& L, uint64_t* X, uint64_t* F, uint64_t* T4) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        L.kb = static_cast<int>(ldi(&st->leaf_kb));
+        L.r0 = ldi(&st->leaf_r);
+        L.pmap_hi = ldi(&st->pmap_hi);
+    }
+    if (tid < 64) {
+        L.fb[tid] = ldw(&st->fbasis[tid]);
+        L.q[tid] = __ldcg(&st->q[tid]);
+        L.pos[tid] = -1;
+    }
+    for (int i = tid; i < 64 * kW; i += kPT) {
+        const int t = i >> 4, w = i & 15;
+        X[i] = w == 0 ? 0ull : ldw(&st->uleaf[t][w - 1]);
+    }
+    __syncthreads();
+    if (tid < L.kb) L.pos[L.q[tid]] = tid;
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t f = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if ((v >> b) & 1) f ^= L.fb[8 * g + b];
+        F[i] = f;
+    }
+    __syncthreads();
+    {  // thread = (nibble group g4, entry e, 4-word quarter wq)
+        const int g4 = tid >> 6, e = (tid >> 2) & 15, wq = tid & 3;
+        uint64_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = L.pos[4 * g4 + b];
+            if (((e >> b) & 1) && r >= 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] ^= X[r * kW + 4 * wq + k];
+            }
+        }
+        uint64_t* d = T4 + (g4 * 16 + e) * kW + 4 * wq;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[k] = v[k];
+    }
+    __syncthreads();
+}
+
+// One 512-row tile below the pivots (positions r0 + kb + ty*kRows ...): every row's
+// panel words wl..pw1 in one load (8 lanes x 2 words per row), the leaf word
+// finalised into the L coefficients (the gauss_pls chain of gauss.cpp:47-49 through
+// the linear tables F), then 16 nibble lookups add the combination of the solved
+// pivot rows (add_rows_from_table, m4ri.cpp:28-38), one store.
+__device__ void update_tile(const Mat& A, int64_t wl, int64_t pw1, const int64_t* pmap, const LeafInfo& L, int ty,
+                            const uint64_t* F, const uint64_t* T4, const PlsState* st) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kb = L.kb;
-    const int64_t row_base = L.r0 + kb + static_cast<int64_t>(ty) * kRows;
+    const int64_t row_base = L.r0 + L.kb + static_cast<int64_t>(ty) * kRows;
     const int64_t nr64 = A.m - row_base;
     const int nrows = nr64 <= 0 ? 0 : (nr64 < kRows ? static_cast<int>(nr64) : kRows);
-    const int ntw = rw1 > rw0 ? static_cast<int>(rw1 - rw0) : 0;
-
-    // finalise the leaf word -> L coefficients
-    for (int i = tid; i < nrows; i += kPT) {
-        const int64_t phys = ldi(pmap + row_base + i);
-        uint64_t w = ldw(A.w + phys * A.stride + wl);
-#pragma unroll
-        for (int g = 0; g < 8; ++g) w ^= F[g * 256 + ((w >> (8 * g)) & 0xffu)];
-        cbuf[i] = w;
-        pbuf[i] = phys;
-        A.w[phys * A.stride + wl] = w;
-    }
-    if (ntw == 0) return;
-    __syncthreads();
-    F2_STAMP(st_prof, 50);
-
+    const int nw = static_cast<int>(pw1 - wl);  // 1..16 words from the leaf word on
     const int rq = lane >> 3, wp = lane & 7;
-    uint64_t acc0[4], acc1[4], cw[4];
+    const bool h0 = 2 * wp < nw, h1 = 2 * wp + 1 < nw;
+    uint64_t w0[4], w1[4];
+    int64_t ph[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int i = warp * 16 + rq + 4 * j;
-        acc0[j] = acc1[j] = 0;
-        cw[j] = i < nrows ? cbuf[i] : 0ull;
-        if (i < nrows) {
-            const uint64_t* cr = A.w + pbuf[i] * A.stride + rw0;
-            if (2 * wp < ntw) acc0[j] = ldw(cr + 2 * wp);
-            if (2 * wp + 1 < ntw) acc1[j] = ldw(cr + 2 * wp + 1);
-        }
-    }
-    F2_STAMP(st_prof, 51);
-    for (int h = 0; h < 2; ++h) {
-        // tables of groups 4h..4h+3 over the solved pivot rows, indexed by the raw
-        // coefficient byte: thread = (group gg, walk half hh, low nibble el, word pair wp)
-        {
-            const int gg = tid >> 8, hh = (tid >> 7) & 1, el = (tid >> 3) & 15, tw = tid & 7;
-            const int g = 4 * h + gg;
-            uint64_t v0[8], v1[8];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int r = L.pos[8 * g + b];
-                v0[b] = r >= 0 ? X[r * kW + 2 * tw] : 0ull;
-                v1[b] = r >= 0 ? X[r * kW + 2 * tw + 1] : 0ull;
-            }
-            uint64_t l0 = 0, l1 = 0, h0 = 0, h1 = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((el >> b) & 1) {
-                    l0 ^= v0[b];
-                    l1 ^= v1[b];
-                }
-            const int k0 = 8 * hh;
-            const int e0 = k0 ^ (k0 >> 1);
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((e0 >> b) & 1) {
-                    h0 ^= v0[4 + b];
-                    h1 ^= v1[4 + b];
-                }
-            uint64_t* tg = tabs + gg * kTab;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int kk = k0 + k;
-                if (k) {
-                    const int b = __ffs(kk) - 1;  // Gray code step flips bit ctz(kk)
-                    h0 ^= b == 0 ? v0[4] : b == 1 ? v0[5] : b == 2 ? v0[6] : v0[7];
-                    h1 ^= b == 0 ? v1[4] : b == 1 ? v1[5] : b == 2 ? v1[6] : v1[7];
-                }
-                const int eh = kk ^ (kk >> 1);
-                uint64_t* e = tg + (eh * 16 + el) * kW + 2 * tw;
-                e[0] = l0 ^ h0;
-                e[1] = l1 ^ h1;
-            }
-        }
-        __syncthreads();
-        F2_STAMP(st_prof, 52 + 2 * h);
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-            const int sh = 8 * (4 * h + gg);
-            const uint64_t* tg = tabs + gg * kTab;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned idx = static_cast<unsigned>(cw[j] >> sh) & 0xffu;
-                const uint4 v = lds128(tg + idx * kW + 2 * wp);
-                acc0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
-                acc1[j] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
-            }
-        }
-        __syncthreads();
-        F2_STAMP(st_prof, 53 + 2 * h);
+        const int64_t pos = row_base + i;
+        ph[j] = i < nrows ? (pos < L.pmap_hi ? ldi(pmap + pos) : pos) : -1;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int i = warp * 16 + rq + 4 * j;
-        if (i < nrows) {
-            uint64_t* cr = A.w + pbuf[i] * A.stride + rw0;
-            if (2 * wp < ntw) cr[2 * wp] = acc0[j];
-            if (2 * wp + 1 < ntw) cr[2 * wp + 1] = acc1[j];
+        const uint64_t* rp = A.w + ph[j] * A.stride + wl + 2 * wp;
+        w0[j] = ph[j] >= 0 && h0 ? ldw(rp) : 0ull;
+        w1[j] = ph[j] >= 0 && h1 ? ldw(rp + 1) : 0ull;
+    }
+    F2_STAMP(st, 50);
+    // finalise: lane x < 16 takes row (rq = x & 3, j = x >> 2), whose leaf word sits
+    // on lane 8 * rq (wp == 0) in w0[j]; the coefficient words go back to the groups
+    uint64_t c[4];
+    {
+        const int xr = lane & 3, xj = (lane >> 2) & 3;
+        uint64_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t t = __shfl_sync(FULL_MASK, w0[j], 8 * xr);
+            v = xj == j ? t : v;
         }
+        if (lane < 16) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) v ^= F[g * 256 + ((v >> (8 * g)) & 0xffu)];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = __shfl_sync(FULL_MASK, v, rq + 4 * j);
+    }
+    if (wp == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w0[j] = c[j];
+    }
+    F2_STAMP(st, 51);
+#pragma unroll
+    for (int g4 = 0; g4 < 16; ++g4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned e = static_cast<unsigned>(c[j] >> (4 * g4)) & 15u;
+            const uint4 v = lds128(T4 + (g4 * 16 + e) * kW + 2 * wp);
+            w0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
+            w1[j] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
+        }
+    }
+    F2_STAMP(st, 52);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (ph[j] < 0) continue;
+        uint64_t* rp = A.w + ph[j] * A.stride + wl + 2 * wp;
+        if (h0) rp[0] = w0[j];
+        if (h1) rp[1] = w1[j];
     }
 }
 
@@ -319,11 +342,9 @@ k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t
                int64_t* pmap, int64_t qcol_off, unsigned* bar) {
     extern __shared__ __align__(16) uint64_t dsm[];
     __shared__ LeafInfo L;
-    uint64_t* tabs = dsm;
-    uint64_t* X = tabs + 4 * kTab;
+    uint64_t* tab = dsm;  // CTA 0's fallback solve table, or T4
+    uint64_t* X = tab + kTab;
     uint64_t* F = X + 64 * kW;
-    uint64_t* cbuf = F + 8 * 256;
-    int64_t* pbuf = reinterpret_cast<int64_t*>(cbuf + kRows);
     const int nleaves = (width + 63) / 64;
     unsigned target = 0;
     for (int j = 0; j < nleaves; ++j) {
@@ -335,42 +356,24 @@ k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t
 #endif
         F2_STAMP(st, 0);
         if (blockIdx.x == 0) {
-            const bool solved = leaf_pivot_body(A, wl, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1);
+            const bool solved = leaf_pivot_body(A, wl, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1, dsm);
             __syncthreads();
             F2_STAMP(st, 1);
-            if (!solved) {
+            if (!solved) {  // the general search ran: basis and solve here
                 load_leaf(st, L);
-                solve_pivot_rows(A, wl + 1, pw1, pmap, L, X, tabs, st);
+                if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];
+                solve_pivot_rows(A, wl + 1, pw1, pmap, L, X, tab, st);
             }
             F2_STAMP(st, 2);
         }
         grid_barrier(bar, target);
         F2_STAMP(st, 3);
-        load_leaf(st, L);
-        if (L.kb) {
-            // finalize tables F[g][v] = xor of the basis over v's bits
-            for (int i = threadIdx.x; i < 8 * 256; i += kPT) {
-                const int g = i >> 8, v = i & 255;
-                uint64_t f = 0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-                    if ((v >> b) & 1) f ^= L.fb[8 * g + b];
-                F[i] = f;
-            }
-            // solved pivot rows (written by CTA 0 before the barrier)
-            const int ntw = pw1 > wl + 1 ? static_cast<int>(pw1 - wl - 1) : 0;
-            for (int i = threadIdx.x; i < L.kb * kW; i += kPT) {
-                const int t = i / kW, k = i % kW;
-                X[i] = k < ntw ? ldw(A.w + ldi(pmap + L.r0 + t) * A.stride + wl + 1 + k) : 0ull;
-            }
-            __syncthreads();
+        if (__ldcg(reinterpret_cast<const long long*>(&st->leaf_kb)) != 0) {
+            worker_prep(st, L, X, F, tab);
             F2_STAMP(st, 4);
             const int64_t rows = A.m - (L.r0 + L.kb);
             const int ntiles = rows > 0 ? static_cast<int>((rows + kRows - 1) / kRows) : 0;
-            for (int ty = blockIdx.x; ty < ntiles; ty += gridDim.x) {
-                update_tile(A, wl, wl + 1, pw1, pmap, L, ty, X, F, tabs, cbuf, pbuf, st);
-                __syncthreads();
-            }
+            for (int ty = blockIdx.x; ty < ntiles; ty += gridDim.x) update_tile(A, wl, pw1, pmap, L, ty, F, tab, st);
         }
         F2_STAMP(st, 5);
 #ifdef F2_PANEL_PROFILE

@@ -11,13 +11,13 @@ L = f2.load_library("tools/libf2gpu_prof.so")
 L.f2_debug_prof.argtypes = [C.POINTER(C.c_longlong), C.c_int]
 names = {0: "leaf start", 10: "k1 window loaded", 11: "k1 outputs start", 12: "k1 st written", 1: "pivot done",
          2: "solve done", 3: "barrier 1 passed", 4: "update prep done", 5: "update done (CTA 0)",
-         50: "tile finalized", 51: "tile acc loaded", 52: "round 0 tables", 53: "round 0 lookups",
-         54: "round 1 tables", 55: "round 1 lookups"}
+         50: "tile rows loaded", 51: "tile finalized", 52: "tile lookups done"}
 names.update({40 + g: f"solve group {g}" for g in range(8)})
 names.update({15: "fast window loaded", 16: "fast transposed", 17: "fast loop done", 18: "fast rows out",
               19: "fast outputs done"})
 names.update({15: "fast phys loaded", 16: "fast transposed", 17: "fast loop done", 18: "fast replay joined",
-              19: "fast src done", 20: "fast outputs done"})
+              19: "fast src done", 20: "fast outputs done", 21: "fast pivot rows written",
+              22: "fast U computed (t0)", 23: "fast U sync"})
 for m, n in [(65536, 2048)]:
     a = f2.DeviceMatrix(m, n)
     a.randomize(0.5, 7)
