@@ -297,8 +297,10 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         if (pw1 < nw) {
             {
                 LaunchTimer t(2, 0, 0);
-                launch_panel_lmaps(s, A, pw0, nleaves, g.st);
-                ++g.launches;
+                if (!g.fused) {  // the panel kernel leaves the maps behind
+                    launch_panel_lmaps(s, A, pw0, nleaves, g.st);
+                    ++g.launches;
+                }
                 launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
             }
             TableApply ta{};

@@ -122,6 +122,8 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
 struct FastSmem {
     uint32_t colw[64 * 4];       // leaf columns: 4 x 32 slots each
     uint64_t linv[64];           // rows of L11^{-1} over pivot indices
+    uint64_t rraw[64];           // the same rows in raw leaf-column coordinates
+    int posc[64];                // leaf column -> pivot index, -1
     int64_t phys[128];           // pre-leaf physical row of each slot
     int step_p[64], step_c[64];  // pivot steps
     int src[128];                // slot s now holds the pre-leaf content of slot src[s]
@@ -221,7 +223,7 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
             const uint64_t u1 = r10 | (static_cast<uint64_t>(r11) << 32);
             F.uf[lane] = u0;
             F.uf[lane + 32] = u1;
-            if (nrest) {
+            if (scratch) {
                 // L11^{-1}: row l = e_l + sum over t < l with L bit of l at q_t of row t
                 __syncwarp();
                 uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
@@ -275,6 +277,20 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
             }
         }
         st->fbasis[e] = corr;
+    } else if (scratch && tid >= 320 && tid < 384) {
+        // rows of L11^{-1} in raw leaf-column coordinates (pivot index t -> column q_t)
+        const int l = tid - 320;
+        uint64_t r = 0;
+        if (l < kb) {
+            uint64_t lv = F.linv[l];
+            while (lv) {
+                const int tt = __ffsll(static_cast<long long>(lv)) - 1;
+                lv &= lv - 1;
+                r |= 1ull << F.step_c[tt];
+            }
+        }
+        F.rraw[l] = r;
+        F.posc[l] = -1;
     } else if (tid >= 256 && tid < 320) {
         const int l = tid - 256;
         const bool in = l < kb;
@@ -287,6 +303,22 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
         for (int i = tid; i < panel_bits; i += blockDim.x) st->brow[i] = -1;
     __syncthreads();
     F2_STAMP(st, 19);
+    if (scratch) {
+        // the panel TRSM's bytewise map c -> c * L11^{-1} for this leaf (see trsm.cu):
+        // lmap[g][v] = xor over bits b of v of the L11^{-1} row of the pivot at column 8g+b
+        if (tid < kb) F.posc[F.step_c[tid]] = tid;
+        __syncthreads();
+        for (int i = tid; i < 8 * 256; i += blockDim.x) {
+            const int g = i >> 8, v = i & 255;
+            uint64_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int l = F.posc[8 * g + b];
+                if (((v >> b) & 1) && l >= 0) x ^= F.rraw[l];
+            }
+            st->lmap[leaf_in_panel][g][v] = x;
+        }
+    }
     const int mv0 = first_in_panel ? 0 : static_cast<int>(st->nmoved);
     const int64_t pkb = first_in_panel ? 0 : st->panel_kb;
     // re-mapped positions (pre-leaf pmap values are in F.phys)

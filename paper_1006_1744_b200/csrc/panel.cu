@@ -148,6 +148,46 @@ __device__ __forceinline__ unsigned mgroup(const LeafInfo& L, int g, unsigned e)
     return m;
 }
 
+// CTA 0 after a general-path leaf: the panel TRSM's bytewise map of L11^{-1}
+// (st->lmap[leaf], see trsm.cu), computed from the pivot words.  Scratch: 128 words.
+__device__ void leaf_lmap(PlsState* st, const LeafInfo& L, int leaf, uint64_t* scratch) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint64_t* rraw = scratch;
+    if (tid < 32) {
+        const int kb = L.kb;
+        uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);  // rows over pivot indices
+        for (int tt = 0; tt < kb; ++tt) {
+            const int qt = L.q[tt];
+            const uint64_t Rt = __shfl_sync(FULL_MASK, tt < 32 ? R0 : R1, tt & 31);
+            if (lane > tt && ((L.uf[lane] >> qt) & 1ull)) R0 ^= Rt;
+            if (lane + 32 > tt && lane + 32 < kb && ((L.uf[lane + 32] >> qt) & 1ull)) R1 ^= Rt;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int l = lane + 32 * h;
+            uint64_t lv = l < kb ? (h ? R1 : R0) : 0ull, r = 0;
+            while (lv) {
+                const int tt = __ffsll(static_cast<long long>(lv)) - 1;
+                lv &= lv - 1;
+                r |= 1ull << L.q[tt];
+            }
+            rraw[l] = r;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t x = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int l = L.pos[8 * g + b];
+            if (((v >> b) & 1) && l >= 0) x ^= rraw[l];
+        }
+        st->lmap[leaf][g][v] = x;
+    }
+    __syncthreads();
+}
+
 // CTA 0, after the pivot search: U = L11^{-1} A12 on the pivot rows' words [rw0, rw1),
 // written back in place (the pivot rows sit at positions r0 .. r0+kb via pmap).
 __device__ void solve_pivot_rows(const Mat& A, int64_t rw0, int64_t rw1, const int64_t* pmap, const LeafInfo& L,
@@ -359,9 +399,10 @@ k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t
             const bool solved = leaf_pivot_body(A, wl, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1, dsm);
             __syncthreads();
             F2_STAMP(st, 1);
-            if (!solved) {  // the general search ran: basis and solve here
+            if (!solved) {  // the general search ran: basis, panel-TRSM map and solve here
                 load_leaf(st, L);
                 if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];
+                leaf_lmap(st, L, j, X);
                 solve_pivot_rows(A, wl + 1, pw1, pmap, L, X, tab, st);
             }
             F2_STAMP(st, 2);
