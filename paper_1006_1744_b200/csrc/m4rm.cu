@@ -34,12 +34,25 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kRPT = 16;                         // rows per thread
 constexpr int kTNW = 16;                         // 64-bit words per tile row (1024 bits)
 constexpr int kTM = kWarps * 4 * kRPT;           // 1024 rows per CTA (4 rows per warp instruction)
-constexpr int kStages = 4;                       // B-row ring depth
+#ifndef F2_SCHUR_SINGLE
+#define F2_SCHUR_PAIRS 1
+#endif
+#ifdef F2_SCHUR_PAIRS
+constexpr int kStages = 8;                       // B-row ring depth (chunks)
+constexpr int kTabs = 4;                         // table buffers: two chunks built while two are read
+#else
+constexpr int kStages = 4;
+constexpr int kTabs = 2;
+#endif
 constexpr int kMaxMap = kMaxPanelBits;           // K bits held in the SMEM row map
+#ifndef F2_BUILD_WARPS
+#define F2_BUILD_WARPS 4
+#endif
+constexpr int kBuildWarps = F2_BUILD_WARPS;      // warps building each chunk's table (4, 8 or 16)
 
 // shared memory carve-up (bytes)
-constexpr size_t kOffT = 0;                                   // [2][256][kTNW] u64   64 KB
-constexpr size_t kOffRing = kOffT + 2 * 256 * kTNW * 8;        // [kStages][8][kTNW]    4 KB
+constexpr size_t kOffT = 0;                                   // [kTabs][256][kTNW] u64
+constexpr size_t kOffRing = kOffT + kTabs * 256 * kTNW * 8;    // [kStages][8][kTNW]
 constexpr size_t kOffA = kOffRing + kStages * 8 * kTNW * 8;    // [2][kTM] u64          16 KB
 constexpr size_t kOffMap = kOffA + 2 * kTM * 8;                // [kMaxMap] i32         8 KB
 constexpr size_t kOffLive = kOffMap + kMaxMap * 4;             // [kMaxMap/8/32] u32
@@ -145,23 +158,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     // built by warps 0..3 only (fewer ring reads): thread = (16-byte column chunk wp,
     // low nibble el of the entry); the high nibble is walked in Gray order
     auto build = [&](int c) {
-        if (warp >= 4) return;
+#ifdef F2_EXP_NOBUILD
+        return;
+#endif
+        if (warp >= kBuildWarps) return;
         const uint64_t* rs = ring + (c % kStages) * 8 * kTNW + 2 * wp;
-        const int el = tid >> 3;  // 0..15
-        uint4 lo = make_uint4(0, 0, 0, 0);
+        const int el = (tid >> 3) & 15;                    // low nibble of the entry
+        constexpr int kSeg = 16 / (kBuildWarps / 4);       // Gray steps per thread
+        const int k0 = (tid >> 7) * kSeg;                  // first step of this thread's segment
+        uint4 x = make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const uint4 v = lds128(rs + b * kTNW);
-            if ((el >> b) & 1) lo = xor4(lo, v);
+            if ((el >> b) & 1) x = xor4(x, v);
         }
         uint4 hv[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) hv[b] = lds128(rs + (4 + b) * kTNW);
-        uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
-        uint4 x = lo;
+        const int g0 = k0 ^ (k0 >> 1);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if (k) x = xor4(x, hv[(k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3))]);
+        for (int b = 0; b < 4; ++b)
+            if ((g0 >> b) & 1) x = xor4(x, hv[b]);
+        uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
+#pragma unroll
+        for (int s = 0; s < kSeg; ++s) {
+            const int k = k0 + s;
+            if (s) {
+                const int b = __ffs(k) - 1;  // the Gray step k-1 -> k flips bit ctz(k)
+                x = xor4(x, b == 0 ? hv[0] : b == 1 ? hv[1] : b == 2 ? hv[2] : hv[3]);
+            }
             const int eh = k ^ (k >> 1);
             sts128(tb + (eh * 16 + el) * kTNW, x);
         }
@@ -177,6 +202,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         acc1[i] = (rv && vb) ? cr[cwb] : 0ull;
     }
 
+#ifdef F2_SCHUR_PAIRS
+    // Two chunks per barrier: while every warp reads tables c, c+1, warps 0-3 build
+    // table c+2 and warps 4-7 table c+3, so there is one CTA barrier per 16
+    // coefficient bits and each builder warp builds one table per two chunks read.
+    // table c by warps 4*grp .. 4*grp+3: thread = (16-byte column chunk wp, low nibble
+    // el of the entry); the high nibble walked in Gray order (16 steps)
+    auto build_half = [&](int c, int grp) {
+        if ((warp >> 2) != grp || c >= nch || !live(c)) return;
+        const uint64_t* rs = ring + (c % kStages) * 8 * kTNW + 2 * wp;
+        const int el = (tid >> 3) & 15;
+        uint4 x = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint4 v = lds128(rs + b * kTNW);
+            if ((el >> b) & 1) x = xor4(x, v);
+        }
+        uint4 hv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) hv[b] = lds128(rs + (4 + b) * kTNW);
+        uint64_t* tb = Tb + (c % kTabs) * 256 * kTNW + 2 * wp;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (k) x = xor4(x, hv[(k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3))]);
+            const int eh = k ^ (k >> 1);
+            sts128(tb + (eh * 16 + el) * kTNW, x);
+        }
+    };
+    auto lookups = [&](int c, const uint32_t (&aw)[kRPT]) {
+        if (c >= nch || !live(c)) return;
+        const uint64_t* tb = Tb + (c % kTabs) * 256 * kTNW + 2 * wp;
+        const int sh = 8 * (c & 3);
+#pragma unroll
+        for (int i = 0; i < kRPT; ++i) {
+            const unsigned idx = (aw[i] >> sh) & 0xffu;
+            const uint4 t = lds128(tb + idx * kTNW);
+            acc0[i] ^= static_cast<uint64_t>(t.x) | (static_cast<uint64_t>(t.y) << 32);
+            acc1[i] ^= static_cast<uint64_t>(t.z) | (static_cast<uint64_t>(t.w) << 32);
+        }
+    };
+    issue_a(0);
+    for (int c = 0; c < 6; c += 2) {  // chunks 0-1, 2-3, 4-5: one group each
+        if (c < nch) issue_b(c);
+        if (c + 1 < nch) issue_b(c + 1);
+        cp_async_commit();
+    }
+    cp_async_wait<2>();
+    __syncthreads();
+    build_half(0, 0);
+    build_half(1, 1);
+    uint32_t aw[kRPT];
+    const int npairs = (nch + 1) / 2;
+    for (int pi = 0; pi < npairs; ++pi) {
+        const int c = 2 * pi;
+        cp_async_wait<1>();
+        __syncthreads();
+        if ((c & 7) == 0 || (c & 7) == 4) {  // coefficient bits of chunks c .. c+3
+            const int g = c >> 3;
+            const uint32_t* ab =
+                reinterpret_cast<const uint32_t*>(abuf + (g & 1) * kTM + warp * 64 + rq) + ((c & 7) >> 2);
+#pragma unroll
+            for (int i = 0; i < kRPT; ++i) aw[i] = ab[8 * i];
+        }
+        build_half(c + 2, 0);
+        build_half(c + 3, 1);
+        if (c + 6 < nch) issue_b(c + 6);
+        if (c + 7 < nch) issue_b(c + 7);
+        if ((c & 7) == 0 && (c >> 3) + 1 < p.kw && (c >> 3) + 1 < (nch + 7) / 8) issue_a((c >> 3) + 1);
+        cp_async_commit();
+#ifndef F2_EXP_NOLOOKUP
+        lookups(c, aw);
+        lookups(c + 1, aw);
+#endif
+    }
+#else
     issue_a(0);
     for (int c = 0; c < 3; ++c) {
         if (c < nch) issue_b(c);
@@ -204,7 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
                     for (int i = 0; i < kRPT; ++i) aw[i] = ab[8 * i];
                 }
                 if (c + 1 < nch && live(c + 1)) build(c + 1);
+#ifdef F2_EXP_NOLOOKUP
+                if (false) {
+#else
                 if (live(c)) {
+#endif
                     const uint64_t* tb = Tb + (c & 1) * 256 * kTNW + 2 * wp;
 #pragma unroll
                     for (int i = 0; i < kRPT; ++i) {
@@ -217,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
             }
         }
     }
+#endif
     cp_async_wait<0>();
 
 #pragma unroll
