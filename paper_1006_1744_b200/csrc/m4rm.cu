@@ -136,9 +136,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     auto live = [&](int c) -> bool { return mapped ? ((livebits[c >> 5] >> (c & 31)) & 1u) : c < nch; };
 
     // B rows of chunk c -> ring stage c % kStages (threads 0..63, one word each)
+    // (threads 256..383: warps that never build in the paired schedule)
     auto issue_b = [&](int c) {
-        if (tid < 8 * kTNW) {
-            const int b = tid >> 4, k = tid & 15;
+        const int tb0 = kThreads - 2 * 8 * kTNW;
+        if (tid >= tb0 && tid < tb0 + 8 * kTNW) {
+            const int b = (tid - tb0) >> 4, k = (tid - tb0) & 15;
             const int64_t br = brow_of(c * 8 + b);
             const int64_t wcol = tile_w0 + k;
             const bool ok = br >= 0 && wcol < p.cw1;
