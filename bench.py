@@ -220,6 +220,19 @@ def run_ours(args):
                 "share_of_step": schur["ms"] / total_fam_ms if total_fam_ms else None,
                 "launches": schur["launches"], "avg_launch_ms": schur["ms"] / max(schur["launches"], 1),
                 "traffic": None}
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (first Schur launch of config 3: C 64512 x 64512 ^= A 64512 x 1024 * B 1024 x 64512)
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_schur_config3_raw.json")
+    if os.path.exists(prof):
+        raw = json.load(open(prof))
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tb = sum(float(raw[k][0]) * scale.get(raw[k][1], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        rows_, cw_, kb_ = 64512, 1008, 1024
+        algo = rows_ * (2 * cw_ * 8 + kb_ // 8) + kb_ * cw_ * 8
+        roofline["traffic"] = tb
+        roofline["traffic_note"] = ("dram read+write bytes of one captured launch (the first, largest Schur launch of "
+                                    "config 3, profiles/r1_ncu_schur_config3_raw.json); that launch's algorithmic "
+                                    f"bytes are {algo:.4g}")
 
     # --- MMPF table-apply over a 1 GiB trailing matrix: the HBM-bound kernel of the flat MMPF
     table_apply = {}
