@@ -49,6 +49,14 @@ struct Ctx {
     int device = -1;
     int nsm = 148;
     cudaStream_t stream = nullptr;
+    // streamed download of finished pivot rows (host-buffer entry points): when set,
+    // the engine copies rows [pW, (p+1)W) to dl_host on dl_stream right after panel
+    // p's TRSM -- final there whenever panels 0..p each found W pivots (checked after)
+    cudaStream_t dl_stream = nullptr;
+    cudaEvent_t dl_ev = nullptr, dl_join = nullptr;
+    uint64_t* dl_host = nullptr;
+    size_t dl_pitch = 0;    // words
+    int64_t dl_done = -1;   // rows [0, dl_done) downloaded by the last engine run
     // engine workspace
     PlsState* st = nullptr;
     int64_t* P = nullptr;
@@ -103,6 +111,9 @@ int ensure_init() {
     if (prop.major < 10) return fail(F2_NO_DEVICE, "kernels are built for sm_100a (B200)");
     g.nsm = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g.dl_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g.dl_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.dl_join, cudaEventDisableTiming));
     CK(cudaMalloc(&g.st, sizeof(PlsState)));
     CK(cudaMalloc(&g.d_digest, sizeof(unsigned long long)));
     setup_leaf_kernels();
@@ -247,13 +258,27 @@ void replay_q(size_t m, size_t n, uint64_t cutoff, const int64_t* piv, size_t np
 // ---- the engine -------------------------------------------------------------
 struct EngineOut {
     int64_t rank = 0;
+    int64_t dl_rows = -1;  // rows [0, dl_rows) already in g.dl_host (streamed download), -1: none
     std::vector<int64_t> P;   // P[0..rank)
     std::vector<int64_t> Qp;  // pivot columns
 };
 
+// Speculative D2H of rows [c, c+W) (see Ctx::dl_host) on the download stream.
+int enqueue_download(const Mat& A, int64_t c, unsigned W, cudaStream_t s) {
+    if (!g.dl_host || c >= A.m) return F2_OK;
+    const int64_t rows = std::min<int64_t>(W, A.m - c);
+    const int64_t nw = (A.n + 63) / 64;
+    CK(cudaEventRecord(g.dl_ev, s));
+    CK(cudaStreamWaitEvent(g.dl_stream, g.dl_ev, 0));
+    CK(cudaMemcpy2DAsync(g.dl_host + c * g.dl_pitch, g.dl_pitch * 8, A.w + c * A.stride, A.stride * 8, nw * 8, rows,
+                         cudaMemcpyDeviceToHost, g.dl_stream));
+    return F2_OK;
+}
+
 // One right-looking PLS pass, enqueued on `s`.  poll = snapshot r after every panel
 // and stop enqueueing once every row is a pivot (not usable inside a graph capture).
 int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
+    int rc = F2_OK;
     const int64_t m = A.m, n = A.n;
     const int64_t nw = (n + 63) / 64;
     const int64_t npanels = (n + W - 1) / W;
@@ -303,6 +328,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 }
                 launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
             }
+            if ((rc = enqueue_download(A, c, W, s))) return rc;
             TableApply ta{};
             ta.C = A;
             ta.c_r1 = m;
@@ -321,6 +347,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             LaunchTimer t(0, static_cast<double>(pi), -1.0);
             launch_table_apply(s, ta, g.nsm);
         }
+        if (pw1 >= nw && (rc = enqueue_download(A, c, W, s))) return rc;  // last panel: final after the gather
         if (poll) {  // early exit once every row is a pivot: snapshot r without blocking
             CK(cudaMemcpyAsync(g.h_r + pi, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
             cudaEvent_t ev;
@@ -332,6 +359,10 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 ++checked;
             }
         }
+    }
+    if (g.dl_host) {  // join the download stream back into s
+        CK(cudaEventRecord(g.dl_join, g.dl_stream));
+        CK(cudaStreamWaitEvent(s, g.dl_join, 0));
     }
     CK(cudaGetLastError());
     if (poll) {
@@ -346,6 +377,8 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
 // (per-launch overhead of ~3300 small launches at 64K^2 drops to graph-node cost).
 struct GraphCache {
     uint64_t* w = nullptr;
+    uint64_t* dl_host = nullptr;
+    size_t dl_pitch = 0;
     int64_t m = 0, n = 0, stride = 0;
     unsigned W = 0;
     uint64_t gen = 0;
@@ -369,7 +402,8 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && !std::getenv("F2_NO_GRAPH");
     if (use_graph) {
         const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
-                         g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen;
+                         g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen &&
+                         g_graph.dl_host == g.dl_host && g_graph.dl_pitch == g.dl_pitch;
         if (!hit) {
             if (g_graph.exec) cudaGraphExecDestroy(g_graph.exec);
             g_graph.exec = nullptr;
@@ -385,6 +419,8 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
             g_graph.w = A.w;
+            g_graph.dl_host = g.dl_host;
+            g_graph.dl_pitch = g.dl_pitch;
             g_graph.m = m;
             g_graph.n = n;
             g_graph.stride = A.stride;
@@ -415,6 +451,25 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     if (!ident) {
         LaunchTimer t(3, 0, 0);
         launch_compress(s, A, r, g.Qp, g.nsm);
+    }
+    if (g.dl_host) {
+        // the speculative copies of panels 0..p are valid while every panel found W pivots
+        out.dl_rows = 0;
+        if (ident) {
+            int64_t t = 0;
+            for (int64_t pi = 0; pi < npanels; ++pi) {
+                const int64_t c = pi * W, hi = std::min<int64_t>(c + W, m);
+                if (c >= m) break;
+                int64_t kb = 0;
+                while (t < r && out.Qp[t] < c + W) {
+                    ++kb;
+                    ++t;
+                }
+                if (kb != hi - c) break;
+                out.dl_rows = hi;
+            }
+        }
+        g.dl_done = out.dl_rows;
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -737,12 +792,34 @@ static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols,
     }
     f2_matrix* a = g_host_mat;
     rc = f2_matrix_upload(a, words, stride_words);
+    // pinned host buffer: finished pivot rows stream back while later panels compute
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, words) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        nrows > 0 && ncols > 0;
+    cudaGetLastError();
     if (!rc) {
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            g.dl_host = pinned ? words : nullptr;
+            g.dl_pitch = stride_words;
+            g.dl_done = -1;
+        }
         f2_window w{0, 0, nrows, ncols};
         rc = recursive ? f2_pls_recursive(a, w, p, nrows, q, ncols, cfg, rank)
                        : f2_mmpf_pls(a, w, p, nrows, q, ncols, k, rank);
+        std::lock_guard<std::mutex> lk(g_mu);
+        g.dl_host = nullptr;
     }
-    if (!rc) rc = f2_matrix_download(a, words, stride_words);
+    if (!rc) {
+        const int64_t done = g.dl_done < 0 ? 0 : g.dl_done;
+        if (done < static_cast<int64_t>(nrows)) {  // the rest (non-pivot rows, or every row after a fallback)
+            std::lock_guard<std::mutex> lk(g_mu);
+            const size_t nw = (ncols + 63) / 64;
+            CK(cudaMemcpy2DAsync(words + done * stride_words, stride_words * 8, a->d + done * a->stride, a->stride * 8,
+                                 nw * 8, nrows - done, cudaMemcpyDeviceToHost, g.stream));
+            CK(cudaStreamSynchronize(g.stream));
+        }
+    }
     return rc;
 }
 

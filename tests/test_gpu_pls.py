@@ -179,3 +179,31 @@ def test_windows(f2, oracle):
         outside = bits.copy()
         outside[r0:r1, c0:c1] = gb[r0:r1, c0:c1]
         assert (gb == outside).all(), "bits outside the window changed"
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_entry_points_streamed_download(f2, oracle, pinned):
+    """f2_*_host: upload, decompose, download.  With a pinned buffer the finished
+    pivot rows stream back during the factorisation (valid while every panel is
+    full rank, redone otherwise): full-rank, rank-deficient, tall and wide inputs."""
+    cases = [(3000, 3000, 0.5, None), (2500, 2600, 0.5, 300), (4100, 1500, 0.5, None), (1200, 5000, 0.5, None),
+             (2048, 2048, 0.02, None)]
+    for (m, n, d, inner) in cases:
+        if inner:
+            x = oracle.randomize(m, inner, 0.5, 5)
+            y = oracle.randomize(inner, n, 0.5, 6)
+            a = oracle.mul(x, inner, y, n)
+        else:
+            a = oracle.randomize(m, n, d, m + n)
+        w, p, q, r = oracle.gauss_pls(a, n)
+        for recursive in (True, False):
+            h = f2.pinned_empty(a.shape) if pinned else np.empty_like(a)
+            np.copyto(h, a)
+            if recursive:
+                res = f2.pls_recursive_host(h, n, f2.EliminationConfig(cutoff_bytes=4096))
+                qq = oracle.recursive_q(m, n, 4096, q[:r])
+            else:
+                res = f2.mmpf_pls_host(h, n)
+                qq = q
+            assert res.rank == r and (res.P == p).all() and (res.Q == qq).all(), (m, n, recursive)
+            assert (h == w).all(), (m, n, recursive, "packed")
