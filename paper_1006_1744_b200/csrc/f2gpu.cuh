@@ -51,6 +51,15 @@ struct PlsState {
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
     int64_t brow[kMaxPanelBits];        // panel raw column -> pivot row position, -1 if none
     int64_t moved[kMaxMoved];           // positions with pmap[x] != x (may repeat)
+    // what CTA 0 of the panel kernel publishes for the row-tile workers, double
+    // buffered so the pipelined schedule can write leaf j's while leaf j-1's is read
+    struct Packet {
+        int64_t r0, kb, lo, pmap_hi;  // pivots at positions r0..r0+kb; workers update positions >= lo
+        int32_t q[64];                // pivot bit positions in the leaf word
+        uint64_t fb[64];              // finalize basis
+        uint64_t u[64][16];           // solved pivot rows over the rest of the panel (word 0 = leaf word + 1)
+    } pk[2];
+    int64_t ctl[4];                     // pipelined panel kernel: next iteration's control word
     uint64_t uleaf[64][16];             // the current leaf's solved pivot rows over the rest of the panel
     uint64_t fbasis[64];                // the current leaf's finalize basis (see panel.cu)
     long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)

@@ -132,47 +132,17 @@ struct FastSmem {
     int final_kb;                // -1: fell back
 };
 
-static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, int lw, int first_in_panel,
-                                                    int leaf_in_panel, int panel_bits, PlsState* st, int64_t* P,
-                                                    int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1,
-                                                    uint64_t* scratch) {
-    constexpr int kFW = 128;
-    __shared__ FastSmem F;
-    // scratch (dynamic smem, >= (128 + 256) * 15 words when solving): window rows'
-    // pre-leaf rest words (row form), then the 4-bit tables over the pivot rows' ones
-    uint64_t* const Frest = scratch;
-    uint64_t* const Ft16 = scratch + 128 * 15;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t m = A.m, stride = A.stride;
-    const int64_t base = st->r;
-    const int64_t span = m - base;
-    const int nrest = (scratch && rw1 > wl + 1) ? static_cast<int>(rw1 - wl - 1) : 0;  // <= 15
-
-    if (tid < kFW) F.phys[tid] = tid < span ? ldi(pmap + base + tid) : -1;
-    __syncthreads();
-    F2_STAMP(st, 15);
-    if (warp < 8) {  // leaf word -> column form: task = (slot block rb, column half h)
-        const int rb = warp & 3, h = warp >> 2;
-        const int64_t ph = F.phys[rb * 32 + lane];
-        const uint64_t w = ph >= 0 ? ldw(A.w + ph * stride + wl) : 0ull;
-        F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
-    }
-    for (int i = tid; i < kFW * nrest; i += blockDim.x) {  // rest of the panel, row form
-        const int sl = i / nrest, k = i - sl * nrest;
-        const int64_t ph = F.phys[sl];
-        Frest[sl * 15 + k] = ph >= 0 ? ldw(A.w + ph * stride + wl + 1 + k) : 0ull;
-    }
-    __syncthreads();
-    F2_STAMP(st, 16);
-
-    if (warp == 0) {
+// Warp 0: the column-form pivot rule on F.colw (leaf columns as 128-slot masks).
+// Fills step_p/step_c, final_kb (-1: a column needs rows past the window), the pivot
+// rows' final leaf words uf and, with want_linv, the rows of L11^{-1}.
+__device__ __forceinline__ void warp0_pivots(FastSmem& F, int lw, bool more, bool want_linv, PlsState* st) {
+    const int lane = threadIdx.x & 31;
         U128 C0, C1;
         C0.lo = F.colw[lane * 4] | (static_cast<uint64_t>(F.colw[lane * 4 + 1]) << 32);
         C0.hi = F.colw[lane * 4 + 2] | (static_cast<uint64_t>(F.colw[lane * 4 + 3]) << 32);
         C1.lo = F.colw[(lane + 32) * 4] | (static_cast<uint64_t>(F.colw[(lane + 32) * 4 + 1]) << 32);
         C1.hi = F.colw[(lane + 32) * 4 + 2] | (static_cast<uint64_t>(F.colw[(lane + 32) * 4 + 3]) << 32);
-        const bool more = base + kFW < m;
-        int t = 0;
+                int t = 0;
         bool ok = true;
         for (int c = 0; c < lw; ++c) {
             const uint64_t srclo = c < 32 ? C0.lo : C1.lo, srchi = c < 32 ? C0.hi : C1.hi;
@@ -223,7 +193,7 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
             const uint64_t u1 = r10 | (static_cast<uint64_t>(r11) << 32);
             F.uf[lane] = u0;
             F.uf[lane + 32] = u1;
-            if (scratch) {
+            if (want_linv) {
                 // L11^{-1}: row l = e_l + sum over t < l with L bit of l at q_t of row t
                 __syncwarp();
                 uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
@@ -238,6 +208,41 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
             }
         }
     }
+
+static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, int lw, int first_in_panel,
+                                                    int leaf_in_panel, int panel_bits, PlsState* st, int64_t* P,
+                                                    int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1,
+                                                    uint64_t* scratch) {
+    constexpr int kFW = 128;
+    __shared__ FastSmem F;
+    // scratch (dynamic smem, >= (128 + 256) * 15 words when solving): window rows'
+    // pre-leaf rest words (row form), then the 4-bit tables over the pivot rows' ones
+    uint64_t* const Frest = scratch;
+    uint64_t* const Ft16 = scratch + 128 * 15;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m = A.m, stride = A.stride;
+    const int64_t base = st->r;
+    const int64_t span = m - base;
+    const int nrest = (scratch && rw1 > wl + 1) ? static_cast<int>(rw1 - wl - 1) : 0;  // <= 15
+
+    if (tid < kFW) F.phys[tid] = tid < span ? ldi(pmap + base + tid) : -1;
+    __syncthreads();
+    F2_STAMP(st, 15);
+    if (warp < 8) {  // leaf word -> column form: task = (slot block rb, column half h)
+        const int rb = warp & 3, h = warp >> 2;
+        const int64_t ph = F.phys[rb * 32 + lane];
+        const uint64_t w = ph >= 0 ? ldw(A.w + ph * stride + wl) : 0ull;
+        F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
+    }
+    for (int i = tid; i < kFW * nrest; i += blockDim.x) {  // rest of the panel, row form
+        const int sl = i / nrest, k = i - sl * nrest;
+        const int64_t ph = F.phys[sl];
+        Frest[sl * 15 + k] = ph >= 0 ? ldw(A.w + ph * stride + wl + 1 + k) : 0ull;
+    }
+    __syncthreads();
+    F2_STAMP(st, 16);
+
+    if (warp == 0) warp0_pivots(F, lw, base + kFW < m, scratch != nullptr, st);
     __syncthreads();
     F2_STAMP(st, 18);
     const int kb = F.final_kb;

@@ -79,6 +79,7 @@ struct LeafInfo {
     int kb;
     int64_t r0;
     int64_t pmap_hi;  // positions >= pmap_hi are not re-mapped
+    int64_t lo;       // first position a worker updates
 };
 
 // Loads the current leaf's pivots (st written by CTA 0 before the barrier) and
@@ -258,21 +259,22 @@ __device__ void solve_pivot_rows(const Mat& A, int64_t rw0, int64_t rw1, const i
 // pivot rows -- then the finalize tables F[g][v] (xor of the basis over v's bits) and
 // the sixteen 4-bit tables T4[g][e] = xor of the solved pivot rows at the pivot
 // columns of e's bits in nibble g (word 0 of every entry, the leaf column, is 0).
-__device__ void worker_prep(const PlsState* st, LeafInfo& L, uint64_t* X, uint64_t* F, uint64_t* T4) {
+__device__ void worker_prep(const PlsState::Packet* pk, LeafInfo& L, uint64_t* X, uint64_t* F, uint64_t* T4) {
     const int tid = threadIdx.x;
     if (tid == 0) {
-        L.kb = static_cast<int>(ldi(&st->leaf_kb));
-        L.r0 = ldi(&st->leaf_r);
-        L.pmap_hi = ldi(&st->pmap_hi);
+        L.kb = static_cast<int>(ldi(&pk->kb));
+        L.r0 = ldi(&pk->r0);
+        L.pmap_hi = ldi(&pk->pmap_hi);
+        L.lo = ldi(&pk->lo);
     }
     if (tid < 64) {
-        L.fb[tid] = ldw(&st->fbasis[tid]);
-        L.q[tid] = __ldcg(&st->q[tid]);
+        L.fb[tid] = ldw(&pk->fb[tid]);
+        L.q[tid] = __ldcg(&pk->q[tid]);
         L.pos[tid] = -1;
     }
     for (int i = tid; i < 64 * kW; i += kPT) {
         const int t = i >> 4, w = i & 15;
-        X[i] = w == 0 ? 0ull : ldw(&st->uleaf[t][w - 1]);
+        X[i] = w == 0 ? 0ull : ldw(&pk->u[t][w - 1]);
     }
     __syncthreads();
     if (tid < L.kb) L.pos[L.q[tid]] = tid;
@@ -311,7 +313,7 @@ __device__ void worker_prep(const PlsState* st, LeafInfo& L, uint64_t* X, uint64
 __device__ void update_tile(const Mat& A, int64_t wl, int64_t pw1, const int64_t* pmap, const LeafInfo& L, int ty,
                             const uint64_t* F, const uint64_t* T4, const PlsState* st) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t row_base = L.r0 + L.kb + static_cast<int64_t>(ty) * kRows;
+    const int64_t row_base = L.lo + static_cast<int64_t>(ty) * kRows;
     const int64_t nr64 = A.m - row_base;
     const int nrows = nr64 <= 0 ? 0 : (nr64 < kRows ? static_cast<int>(nr64) : kRows);
     const int nw = static_cast<int>(pw1 - wl);  // 1..16 words from the leaf word on
@@ -375,6 +377,23 @@ __device__ void update_tile(const Mat& A, int64_t wl, int64_t pw1, const int64_t
     }
 }
 
+// CTA 0 (non-pipelined schedule): the worker packet from the state the leaf left.
+__device__ void publish_from_state(const PlsState* st, PlsState::Packet* pk) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    if (tid == 0) {
+        pk->r0 = st->leaf_r;
+        pk->kb = st->leaf_kb;
+        pk->lo = st->leaf_r + st->leaf_kb;
+        pk->pmap_hi = st->pmap_hi;
+    }
+    if (tid < 64) {
+        pk->q[tid] = st->q[tid];
+        pk->fb[tid] = st->fbasis[tid];
+    }
+    for (int i = tid; i < 64 * 16; i += kPT) (&pk->u[0][0])[i] = (&st->uleaf[0][0])[i];
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kPT, 1)
@@ -406,13 +425,14 @@ k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t
                 solve_pivot_rows(A, wl + 1, pw1, pmap, L, X, tab, st);
             }
             F2_STAMP(st, 2);
+            publish_from_state(st, &st->pk[0]);
         }
         grid_barrier(bar, target);
         F2_STAMP(st, 3);
-        if (__ldcg(reinterpret_cast<const long long*>(&st->leaf_kb)) != 0) {
-            worker_prep(st, L, X, F, tab);
+        if (__ldcg(reinterpret_cast<const long long*>(&st->pk[0].kb)) != 0) {
+            worker_prep(&st->pk[0], L, X, F, tab);
             F2_STAMP(st, 4);
-            const int64_t rows = A.m - (L.r0 + L.kb);
+            const int64_t rows = A.m - L.lo;
             const int ntiles = rows > 0 ? static_cast<int>((rows + kRows - 1) / kRows) : 0;
             for (int ty = blockIdx.x; ty < ntiles; ty += gridDim.x) update_tile(A, wl, pw1, pmap, L, ty, F, tab, st);
         }

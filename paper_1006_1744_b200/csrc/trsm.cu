@@ -272,12 +272,36 @@ k_panel_trsm(Mat A, Mat Cf, int64_t coef_w0, int nleaves, int64_t tw0, int64_t t
     }
     __syncthreads();
 
+    // block j's inverse map and every row's coefficient word for the block, loaded
+    // into registers one block ahead (4 + 2 words per thread at 512 threads)
+    constexpr int kLmPer = 8 * 256 / 512, kCwPer = kMaxTrsmBits / 512;
+    uint64_t pf_lm[kLmPer], pf_cw[kCwPer];
+    auto prefetch = [&](int j) {
+        if (j >= nleaves) return;
+        const int t0 = bstart[j];
+#pragma unroll
+        for (int u = 0; u < kLmPer; ++u) pf_lm[u] = (&st->lmap[j][0][0])[tid + u * 512];
+#pragma unroll
+        for (int u = 0; u < kCwPer; ++u) {
+            const int t = t0 + tid + u * 512;
+            pf_cw[u] = t < nk ? Cf.w[(r0 + t) * Cf.stride + coef_w0 + j] : 0ull;
+        }
+    };
+    prefetch(0);
     for (int j = 0; j < nleaves; ++j) {
         const int t0 = bstart[j], t1 = bstart[j + 1];
-        if (t0 == t1) continue;
-        // this block's inverse map and every row's coefficient word for the block
-        for (int i = tid; i < 8 * 256; i += nth) Lm[i] = (&st->lmap[j][0][0])[i];
-        for (int t = t0 + tid; t < nk; t += nth) cw[t] = Cf.w[(r0 + t) * Cf.stride + coef_w0 + j];
+        if (t0 == t1) {
+            prefetch(j + 1);
+            continue;
+        }
+#pragma unroll
+        for (int u = 0; u < kLmPer; ++u) Lm[tid + u * 512] = pf_lm[u];
+#pragma unroll
+        for (int u = 0; u < kCwPer; ++u) {
+            const int t = t0 + tid + u * 512;
+            if (t < nk) cw[t] = pf_cw[u];
+        }
+        prefetch(j + 1);
         // 8 tables over block j's rows as they are now: thread = (table g, word w, low nibble)
         {
             const int g = tid >> 6, w = (tid >> 4) & 3, el = tid & 15;
