@@ -64,6 +64,7 @@ struct Ctx {
     int64_t* pmap = nullptr;
     unsigned* bar = nullptr;  // grid barrier counter of k_panel_leaves
     bool fused = true;        // panel leaves in one persistent kernel (F2_UNFUSED=1: three launches per leaf)
+    bool pipe = true;         // pipelined panel kernel (F2_NO_PIPE=1: one leaf per barrier pair)
     uint64_t* scratch = nullptr;
     size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
@@ -125,6 +126,7 @@ int ensure_init() {
     setup_panel_kernels();
     CK(cudaMalloc(&g.bar, sizeof(unsigned)));
     g.fused = !(std::getenv("F2_UNFUSED") && std::getenv("F2_UNFUSED")[0] == '1');
+    g.pipe = !(std::getenv("F2_NO_PIPE") && std::getenv("F2_NO_PIPE")[0] == '1');
     CK(cudaGetLastError());
     g.init = true;
     return F2_OK;
@@ -295,7 +297,10 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         const int64_t pw0 = c / 64, pw1 = pw0 + nleaves;
         if (g.fused) {
             LaunchTimer t(1, 0, 0);
-            launch_panel_leaves(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
+            if (g.pipe)
+                launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
+            else
+                launch_panel_leaves(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         } else {
             for (int j = 0; j < nleaves; ++j) {
                 const int64_t wl = pw0 + j;

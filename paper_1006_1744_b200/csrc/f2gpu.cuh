@@ -59,7 +59,7 @@ struct PlsState {
         uint64_t fb[64];              // finalize basis
         uint64_t u[64][16];           // solved pivot rows over the rest of the panel (word 0 = leaf word + 1)
     } pk[2];
-    int64_t ctl[4];                     // pipelined panel kernel: next iteration's control word
+    int64_t ctl[2][4];                  // pipelined panel kernel: control word per iteration parity
     uint64_t uleaf[64][16];             // the current leaf's solved pivot rows over the rest of the panel
     uint64_t fbasis[64];                // the current leaf's finalize basis (see panel.cu)
     long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)

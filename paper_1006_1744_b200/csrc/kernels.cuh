@@ -70,6 +70,8 @@ void setup_misc_kernels();
 // panel.cu: all leaves of a panel in one cooperative persistent kernel
 void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st,
                          int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm);
+void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
+                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm);
 void setup_panel_kernels();
 void launch_rref_prepare(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp);
 void launch_rref_coeffs(cudaStream_t s, const Mat& S, int64_t rank, const int64_t* Qp, const Mat& Lrev, int nsm);

@@ -420,9 +420,9 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
 // rows over words wl+1..rw1); false after the general search.
 static __device__ __noinline__ bool leaf_pivot_body(const Mat& A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel,
                                 int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap,
-                                int64_t qcol_off, int64_t rw1, uint64_t* scratch) {
-    if (leaf_pivot_fast(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, rw1,
-                        scratch))
+                                int64_t qcol_off, int64_t rw1, uint64_t* scratch, bool try_fast = true) {
+    if (try_fast && leaf_pivot_fast(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off,
+                                    rw1, scratch))
         return true;
     __syncthreads();
     __shared__ uint64_t s_u[64];

@@ -444,6 +444,417 @@ k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t
     }
 }
 
+
+// ---- pipelined schedule (k_panel_pipe) --------------------------------------------------
+//
+// CTA 0 keeps the 128-row window of the current order in shared memory (row form,
+// the panel's 16 words per row) and carries it from leaf to leaf: after leaf j the
+// rows that did not become pivots stay, the leaf's pivots are replaced by the next
+// kb rows of the order, and CTA 0 itself applies leaf j's update to all 128.  So the
+// search for leaf j+1 needs nothing from the other CTAs, which meanwhile apply leaf
+// j to every row past the next window.  One grid barrier per leaf, and the row
+// updates run concurrently with the next pivot search.  A leaf the column-form search
+// cannot decide inside the window (rank-deficient / sparse inputs) falls back to the
+// general search on the global matrix: CTA 0 writes its window back, waits for the
+// workers, searches, then the workers update everything before a fresh window.
+namespace {
+
+constexpr int kPW = 128;  // window slots
+struct PipeSmem {
+    uint64_t win[2][kPW][16];  // window rows, panel words pw0 .. pw0+15 (double buffered)
+    uint64_t T[16 * 16 * kW];  // 4-bit tables over the last fast leaf's solved rows
+    uint64_t F[8 * 256];       // its finalize tables
+    uint64_t t16[256 * 15];    // solve scratch: 4-bit tables over the pivot rows' rest words
+    uint64_t U[64 * 16];       // this leaf's solved rows (word 0 = 0, 1.. = rest words)
+};
+constexpr size_t kPipeSmem = sizeof(PipeSmem) > kSmem ? sizeof(PipeSmem) : kSmem;
+
+enum PipeState : int64_t { S_FRESH = 0, S_CARRY = 1, S_GENERAL = 2, S_IDLE = 3, S_FINAL = 4, S_DONE = 5 };
+
+struct PipeStatic {  // CTA 0's persistent window bookkeeping
+    int64_t wphys[2][kPW];
+    int srcprev[kPW];
+    int cs[kPW];
+};
+
+// Window for leaf `leaf` into buffer `pb`: fresh from the global matrix (every leaf
+// before it applied there), or carried from buffer pb^1 (leaf-1's window, kbp pivots,
+// srcprev) plus new rows, with leaf-1's update applied by CTA 0.
+__device__ void pipe_build_window(const Mat& A, int64_t pw0, int nwp, const int64_t* pmap, PlsState* st,
+                                  PipeSmem& S, PipeStatic& Z, int pb, bool carry, int kbp, int leafp,
+                                  int64_t pmap_hi) {
+    const int tid = threadIdx.x;
+    const int64_t base = st->r;  // position of slot 0
+    const int64_t m = A.m;
+    // phase 0: sources (previous window slot or a global row) and physical rows
+    for (int i = tid; i < kPW * 16; i += kPT) {
+        const int sl = i >> 4, k = i & 15;
+        int64_t ph;
+        uint64_t v = 0;
+        if (carry && sl < kPW - kbp) {
+            const int ss = Z.srcprev[kbp + sl];
+            ph = Z.wphys[pb ^ 1][ss];
+            v = S.win[pb ^ 1][ss][k];
+        } else {
+            const int64_t pos = base + sl;
+            ph = pos < m ? (pos < pmap_hi ? ldi(pmap + pos) : pos) : -1;
+            v = (ph >= 0 && k < nwp) ? ldw(A.w + ph * A.stride + pw0 + k) : 0ull;
+        }
+        S.win[pb][sl][k] = v;
+        if (k == 0) Z.wphys[pb][sl] = ph;
+    }
+    if (!carry) {
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    // phase 1: leaf-1's word of every slot -> its L coefficients (finalize chain)
+    if (tid < kPW) {
+        uint64_t x = S.win[pb][tid][leafp];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) x ^= S.F[g * 256 + ((x >> (8 * g)) & 0xffu)];
+        S.win[pb][tid][leafp] = x;
+        Z.cs[tid] = 0;
+        reinterpret_cast<uint64_t*>(S.t16)[tid] = x;  // coefficient words (scratch)
+    }
+    __syncthreads();
+    // phase 2: the words right of leaf-1 add the combination of its solved rows
+    for (int i = tid; i < kPW * 16; i += kPT) {
+        const int sl = i >> 4, k = i & 15;
+        if (k <= leafp || k >= nwp) continue;
+        const uint64_t c = S.t16[sl];
+        uint64_t v = S.win[pb][sl][k];
+#pragma unroll
+        for (int g4 = 0; g4 < 16; ++g4) v ^= S.T[(g4 * 16 + ((c >> (4 * g4)) & 15u)) * kW + (k - leafp)];
+        S.win[pb][sl][k] = v;
+    }
+    __syncthreads();
+}
+
+__device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSmem& S, const PipeStatic& Z, int pb) {
+    for (int i = threadIdx.x; i < kPW * 16; i += kPT) {
+        const int sl = i >> 4, k = i & 15;
+        const int64_t ph = Z.wphys[pb][sl];
+        if (ph >= 0 && k < nwp) A.w[ph * A.stride + pw0 + k] = S.win[pb][sl][k];
+    }
+}
+
+// Column-form search of leaf `leaf` on window buffer pb; on success publishes every
+// output (P, Q, pmap moves, pivot rows' slices, state, panel-TRSM map, worker packet)
+// and the carry tables, and returns kb; -1 when the window cannot decide a column.
+__device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int lw, PlsState* st, int64_t* P,
+                              int64_t* Qp, int64_t* pmap, int64_t qcol_off, PipeSmem& S, PipeStatic& Z, int pb,
+                              PlsState::Packet* pk, int nleaves) {
+    __shared__ FastSmem F;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m = A.m, stride = A.stride;
+    const int64_t base = st->r;
+    const int64_t span = m - base;
+    const int nrest = nwp - leaf - 1;  // rest words right of the leaf
+    const bool first = leaf == 0;
+    const int64_t wl = pw0 + leaf;
+    if (warp < 8) {  // leaf word -> column form
+        const int rb = warp & 3, h = warp >> 2;
+        const uint64_t w = S.win[pb][rb * 32 + lane][leaf];
+        F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
+    }
+    __syncthreads();
+    if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
+    __syncthreads();
+    const int kb = F.final_kb;
+    if (kb < 0) return -1;
+
+    if (tid < kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
+        int x = tid;
+        for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
+            int pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pv[i] = F.step_p[u0 + i];
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                const int u = u0 + i;
+                if (u < kb) x = x == u ? pv[i] : (x == pv[i] ? u : x);
+            }
+        }
+        F.src[tid] = x;
+    } else if (tid < kPW + 64) {  // finalize basis
+        const int e = tid - kPW, g = e >> 3, b = e & 7;
+        int lo = 0, hi = kb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (F.step_c[mid] < 8 * g) lo = mid + 1;
+            else hi = mid;
+        }
+        uint64_t x = 1ull << (8 * g + b), corr = 0;
+        for (int l = lo; l < kb && F.step_c[l] < 8 * g + 8; ++l) {
+            const int q = F.step_c[l];
+            if ((x >> q) & 1ull) {
+                const uint64_t ul = F.uf[l] & above(q);
+                x ^= ul;
+                corr ^= ul;
+            }
+        }
+        pk->fb[e] = corr;
+        F.rraw[e] = corr;  // also the carry tables' basis (rraw reused below)
+    } else if (tid >= 256 && tid < 320) {
+        const int l = tid - 256;
+        const bool in = l < kb;
+        const int q = in ? F.step_c[l] : 64;
+        st->ustrict[l] = in ? F.uf[l] & above(q) : 0ull;
+        st->ufull[l] = in ? F.uf[l] : 0ull;
+        st->q[l] = q;
+        pk->q[l] = q;
+        F.posc[l] = -1;
+    }
+    if (first)
+        for (int i = tid; i < nleaves * 64; i += kPT) st->brow[i] = -1;
+    __syncthreads();
+    // carry finalize tables from the basis; posc; L11^-1 rows in raw columns (for lmap)
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t f = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if ((v >> b) & 1) f ^= F.rraw[8 * g + b];
+        S.F[i] = f;
+    }
+    if (tid < kb) F.posc[F.step_c[tid]] = tid;
+    __syncthreads();
+    if (tid < 64) {
+        uint64_t r = 0;
+        if (tid < kb) {
+            uint64_t lv = F.linv[tid];
+            while (lv) {
+                const int tt = __ffsll(static_cast<long long>(lv)) - 1;
+                lv &= lv - 1;
+                r |= 1ull << F.step_c[tt];
+            }
+        }
+        F.rraw[tid] = r;
+    }
+    // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order)
+    for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
+        const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
+        uint64_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
+        S.t16[ge * 15 + k] = v;
+    }
+    __syncthreads();
+    // panel-TRSM map of this leaf
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t x = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int l = F.posc[8 * g + b];
+            if (((v >> b) & 1) && l >= 0) x ^= F.rraw[l];
+        }
+        st->lmap[leaf][g][v] = x;
+    }
+    // solved rest words U_l = sum over t of Linv[l][t] A12_t
+    for (int i = tid; i < 64 * 16; i += kPT) {
+        const int l = i >> 4, k = i & 15;
+        uint64_t acc = 0;
+        if (l < kb && k >= 1 && k - 1 < nrest) {
+            const uint64_t lv = F.linv[l];
+#pragma unroll
+            for (int g = 0; g < 16; ++g) acc ^= S.t16[((g << 4) | static_cast<int>((lv >> (4 * g)) & 15u)) * 15 + k - 1];
+        }
+        S.U[i] = acc;
+        if (k >= 1) pk->u[l][k - 1] = acc;
+    }
+    const int mv0 = first ? 0 : static_cast<int>(st->nmoved);
+    const int64_t pkb = first ? 0 : st->panel_kb;
+    int moved = 0, off = 0;
+    if (warp < 4) {
+        const int sl = tid;
+        moved = sl < span && F.src[sl] != sl;
+        const unsigned bm = __ballot_sync(FULL_MASK, moved);
+        off = __popc(bm & ((1u << lane) - 1));
+        if (lane == 0) F.wcount[warp] = __popc(bm);
+    }
+    for (int l = tid; l < kb; l += kPT) {
+        P[base + l] = base + F.step_p[l];
+        Qp[base + l] = qcol_off + wl * 64 + F.step_c[l];
+        st->panel_q[pkb + l] = leaf * 64 + F.step_c[l];
+        st->brow[leaf * 64 + F.step_c[l]] = base + l;
+    }
+    __syncthreads();
+    // pivot rows' slices: earlier leaf words as carried, the final leaf word, U
+    for (int i = tid; i < kb * 16; i += kPT) {
+        const int l = i >> 4, k = i & 15;
+        if (k >= nwp) continue;
+        const int ss = F.src[l];
+        const uint64_t v = k < leaf ? S.win[pb][ss][k] : (k == leaf ? F.uf[l] : S.U[l * 16 + k - leaf]);
+        A.w[Z.wphys[pb][ss] * stride + pw0 + k] = v;
+    }
+    if (warp < 4 && moved) {
+        int o = off;
+        for (int w2 = 0; w2 < warp; ++w2) o += F.wcount[w2];
+        pmap[base + tid] = Z.wphys[pb][F.src[tid]];
+        st->moved[mv0 + o] = base + tid;
+    }
+    if (tid < kPW) Z.srcprev[tid] = F.src[tid];
+    // carry tables T[g4][e] over the solved rows (word index relative to the leaf word)
+    {
+        const int g4 = tid >> 6, e = (tid >> 2) & 15, wq = tid & 3;
+        uint64_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = F.posc[4 * g4 + b];
+            if (((e >> b) & 1) && r >= 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] ^= S.U[r * 16 + 4 * wq + k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) S.T[(g4 * 16 + e) * kW + 4 * wq + k] = v[k];
+    }
+    if (warp == 0) {
+        uint64_t mk = 0;
+        for (int l = lane; l < kb; l += 32) mk |= 1ull << F.step_c[l];
+        mk = warp_or64(mk);
+        int nm = 0, hi = -1;
+        for (int w2 = 0; w2 < 4; ++w2) nm += F.wcount[w2];
+        for (int w2 = 3; w2 >= 0 && hi < 0; --w2)
+            if (F.wcount[w2]) hi = w2;
+        if (lane == 0) {
+            st->leaf_mask = mk;
+            st->nmoved = mv0 + nm;
+            const int64_t h = hi < 0 ? 0 : base + 32 * (hi + 1);
+            const int64_t prev = first ? 0 : st->pmap_hi;
+            const int64_t ph = h > prev ? h : prev;
+            st->pmap_hi = ph;
+            st->leaf_r = base;
+            st->leaf_kb = kb;
+            st->r = base + kb;
+            if (first) st->panel_r = base;
+            st->panel_kb = pkb + kb;
+            pk->r0 = base;
+            pk->kb = kb;
+            pk->lo = base + kb + kPW;
+            pk->pmap_hi = ph;
+        }
+    }
+    __syncthreads();
+    return kb;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kPT, 1)
+k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap,
+             int64_t qcol_off, unsigned* bar) {
+    extern __shared__ __align__(16) uint64_t dsm[];
+    __shared__ LeafInfo L;
+    __shared__ PipeStatic Z;
+    __shared__ int64_t s_ctl[4];
+    PipeSmem& S = *reinterpret_cast<PipeSmem*>(dsm);
+    uint64_t* tab = dsm;  // workers / fallback: T4 or the 8-bit solve table
+    uint64_t* X = tab + kTab;
+    uint64_t* Fw = X + 64 * kW;
+    const int nleaves = (width + 63) / 64;
+    const int nwp = static_cast<int>(pw1 - pw0);
+    unsigned target = 0;
+    int kbprev = 0, pkc = 0;  // CTA 0's carry state (uniform across its threads)
+    int64_t state = S_FRESH, leaf = 0, wpk = -1, wleaf = 0;
+    for (int it = 0;; ++it) {
+        if (it > 0) {
+            if (threadIdx.x < 4) s_ctl[threadIdx.x] = ldi(&st->ctl[it & 1][threadIdx.x]);
+            __syncthreads();
+            state = s_ctl[0];
+            leaf = s_ctl[1];
+            wpk = s_ctl[2];
+            wleaf = s_ctl[3];
+            __syncthreads();
+        }
+        if (state == S_DONE) break;
+        if (blockIdx.x == 0) {
+            int64_t nstate = S_DONE, nleaf = leaf, nwpk = -1, nwleaf = 0;
+            const int j = static_cast<int>(leaf);
+            const int pb = j & 1;
+            if (state == S_FRESH || state == S_CARRY || state == S_FINAL) {
+                pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
+                                  j == 0 ? 0 : st->pmap_hi);
+                if (state == S_FINAL) {
+                    pipe_write_back(A, pw0, nwp, S, Z, pb);
+                    nstate = S_DONE;
+                } else {
+                    const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
+                    PlsState::Packet* pk = &st->pk[pkc & 1];
+                    const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves);
+                    if (kb >= 0) {
+                        kbprev = kb;
+                        nwpk = pkc & 1;
+                        nwleaf = j;
+                        ++pkc;
+                        nstate = j + 1 < nleaves ? S_CARRY : S_FINAL;
+                        nleaf = j + 1;
+                    } else {  // undecidable in the window: hand the window back, search globally
+                        pipe_write_back(A, pw0, nwp, S, Z, pb);
+                        nstate = S_GENERAL;
+                        nleaf = j;
+                    }
+                }
+            } else if (state == S_GENERAL) {
+                const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
+                leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1, nullptr,
+                                false);
+                __syncthreads();
+                load_leaf(st, L);
+                if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];
+                leaf_lmap(st, L, j, X);
+                solve_pivot_rows(A, pw0 + j + 1, pw1, pmap, L, X, tab, st);
+                publish_from_state(st, &st->pk[pkc & 1]);
+                nwpk = pkc & 1;
+                nwleaf = j;
+                ++pkc;
+                nstate = S_IDLE;
+                nleaf = j + 1;
+            } else if (state == S_IDLE) {
+                nstate = j < nleaves ? S_FRESH : S_DONE;
+                nleaf = j;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {  // read by every CTA after the barrier (parity: a late
+                int64_t* c = st->ctl[(it + 1) & 1];  // reader of this iteration's word is never overtaken)
+                c[0] = nstate;
+                c[1] = nleaf;
+                c[2] = nwpk;
+                c[3] = nwleaf;
+            }
+        } else if (wpk >= 0) {
+            const PlsState::Packet* pk = &st->pk[wpk];
+            if (ldi(&pk->kb) != 0) {
+                worker_prep(pk, L, X, Fw, tab);
+                const int64_t rows = A.m - L.lo;
+                const int ntiles = rows > 0 ? static_cast<int>((rows + kRows - 1) / kRows) : 0;
+                for (int ty = blockIdx.x - 1; ty < ntiles; ty += gridDim.x - 1)
+                    update_tile(A, pw0 + wleaf, pw1, pmap, L, ty, Fw, tab, st);
+            }
+        }
+        grid_barrier(bar, target);
+    }
+}
+
+void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
+                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm) {
+    cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(nsm));
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = kPipeSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_panel_pipe, A, pw0, width, pw1, st, P, Qp, pmap, qcol_off, bar);
+}
+
 void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st,
                          int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm) {
     cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
@@ -462,6 +873,7 @@ void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, i
 
 void setup_panel_kernels() {
     cudaFuncSetAttribute(k_panel_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+    cudaFuncSetAttribute(k_panel_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem));
 }
 
 }  // namespace f2g
