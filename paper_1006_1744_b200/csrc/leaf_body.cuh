@@ -130,6 +130,12 @@ struct FastSmem {
     uint64_t uf[64];             // pivot rows' final leaf words
     int wcount[4];
     int final_kb;                // -1: fell back
+    // two-warp search: published steps (the selecting warp writes, the other replays)
+    uint64_t step_e[64][2];
+    uint32_t ufl[64], ufh[64];   // pivot rows' leaf words, columns 0-31 / 32-63
+    uint64_t fbas[64];           // finalize basis
+    volatile int q_n;            // steps published
+    volatile int q_done[2];      // warp w finished selecting: its final step count, -1 when undecidable
 };
 
 // Warp 0: the column-form pivot rule on F.colw (leaf columns as 128-slot masks).
@@ -209,6 +215,137 @@ __device__ __forceinline__ void warp0_pivots(FastSmem& F, int lw, bool more, boo
         }
     }
 
+
+// One warp: rows of L11^{-1} over pivot indices from the pivot rows' leaf words:
+// row l = e_l + sum over t < l with the L bit of l at column q_t of row t.
+__device__ __forceinline__ void warp_linv(FastSmem& F, int kb) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t u0 = F.uf[lane], u1 = F.uf[lane + 32];
+    uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
+    for (int tt = 0; tt < kb; ++tt) {
+        const int qt = F.step_c[tt];
+        const uint64_t Rt = __shfl_sync(FULL, tt < 32 ? R0 : R1, tt & 31);
+        if (lane > tt && ((u0 >> qt) & 1ull)) R0 ^= Rt;
+        if (lane + 32 > tt && ((u1 >> qt) & 1ull)) R1 ^= Rt;
+    }
+    F.linv[lane] = R0;
+    F.linv[lane + 32] = R1;
+}
+
+// Warps 0 and 1: the same pivot rule with the columns split, lane l of warp w owning
+// column 32w + l.  Warp 0 selects the pivots of columns 0-31 while warp 1 replays each
+// published step (slot swap + masked XOR) on its columns; then warp 1 selects columns
+// 32-63 while warp 0 replays the swaps.  Each selecting step touches one column mask
+// per lane instead of two.  Same outputs as warp0_pivots.
+__device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, bool want_linv) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int col = 32 * w + lane;
+    U128 C;
+    C.lo = F.colw[col * 4] | (static_cast<uint64_t>(F.colw[col * 4 + 1]) << 32);
+    C.hi = F.colw[col * 4 + 2] | (static_cast<uint64_t>(F.colw[col * 4 + 3]) << 32);
+    if (threadIdx.x == 0) {
+        F.q_n = 0;
+        F.q_done[0] = -2;
+        F.q_done[1] = -2;
+    }
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    auto apply = [&](int t, int p, uint64_t elo, uint64_t ehi, bool xr) {
+        const uint64_t tb = 1ull << t;
+        const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
+        const uint64_t d = (((C.lo & tb) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
+        C.lo ^= d & (tb | plo);
+        C.hi ^= d & phi;
+        const bool a = xr && (C.lo & tb);
+        C.lo ^= a ? elo : 0ull;
+        C.hi ^= a ? ehi : 0ull;
+    };
+    int t = 0;
+    bool ok = true;
+    for (int phase = 0; phase < 2; ++phase) {
+        const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32;
+        if (w == phase) {
+            // select the pivots of columns c0 .. c1-1
+            for (int c = c0; c < c1; ++c) {
+                const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
+                const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
+                const uint64_t clo = mlo & (~0ull << t);
+                if ((clo | mhi) == 0) {
+                    if (more) {
+                        ok = false;
+                        break;
+                    }
+                    continue;
+                }
+                const int p = clo ? __ffsll(static_cast<long long>(clo)) - 1 : 63 + __ffsll(static_cast<long long>(mhi));
+                const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
+                const uint64_t elo = (mlo & ~plo) & (t == 63 ? 0ull : (~0ull << (t + 1)));
+                const uint64_t ehi = mhi & ~phi;
+                apply(t, p, elo, ehi, col > c);
+                F.step_p[t] = p;
+                F.step_c[t] = c;
+                F.step_e[t][0] = elo;
+                F.step_e[t][1] = ehi;
+                ++t;
+                __syncwarp();
+#ifdef F2_PUB_FENCE
+                if (lane == 0) {
+                    __threadfence_block();
+                    F.q_n = t;
+                }
+#else
+                if (lane == 0) asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
+#endif
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                F.q_done[phase] = ok ? t : -1;
+            }
+        } else if (c0 < lw) {
+            // replay the other warp's steps as they are published
+            while (true) {
+                int n;
+                asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(n) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
+                const int dn = F.q_done[phase];
+                __threadfence_block();
+                for (; t < n; ++t)
+                    apply(t, F.step_p[t], F.step_e[t][0], F.step_e[t][1], w > phase);
+                if (dn != -2) {
+                    if (dn < 0) ok = false;
+                    else
+                        for (; t < dn; ++t) apply(t, F.step_p[t], F.step_e[t][0], F.step_e[t][1], w > phase);
+                    break;
+                }
+#ifdef F2_PUB_SLEEP
+                __nanosleep(20);
+#endif
+            }
+        }
+        if (!ok) break;
+    }
+    if (lane == 0 && w == 0) F.final_kb = ok ? t : -1;
+    if (ok) {
+        // pivot rows' final leaf words (slots 0..63), this warp's 32 columns
+        const uint32_t r0 = warp_transpose32(static_cast<uint32_t>(C.lo), lane);
+        const uint32_t r1 = warp_transpose32(static_cast<uint32_t>(C.lo >> 32), lane);
+        if (w == 0) {
+            F.ufl[lane] = r0;
+            F.ufl[lane + 32] = r1;
+        } else {
+            F.ufh[lane] = r0;
+            F.ufh[lane + 32] = r1;
+        }
+    }
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    if (ok && w == 0) {
+        const uint64_t u0 = F.ufl[lane] | (static_cast<uint64_t>(F.ufh[lane]) << 32);
+        const uint64_t u1 = F.ufl[lane + 32] | (static_cast<uint64_t>(F.ufh[lane + 32]) << 32);
+        F.uf[lane] = u0;
+        F.uf[lane + 32] = u1;
+        if (want_linv) warp_linv(F, t);
+    }
+}
+
 static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, int lw, int first_in_panel,
                                                     int leaf_in_panel, int panel_bits, PlsState* st, int64_t* P,
                                                     int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1,
@@ -242,7 +379,11 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
     __syncthreads();
     F2_STAMP(st, 16);
 
+#ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kFW < m, scratch != nullptr, st);
+#else
+    if (warp < 2) two_warp_pivots(F, lw, base + kFW < m, scratch != nullptr);
+#endif
     __syncthreads();
     F2_STAMP(st, 18);
     const int kb = F.final_kb;

@@ -559,13 +559,27 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
     }
     __syncthreads();
+    F2_STAMP(st, 16);
+    const bool clk = pw0 == 0 && leaf == 2 && tid == 0;
+    long long c0 = clock64();
+#ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
+#else
+    if (warp < 2) two_warp_pivots(F, lw, base + kPW < m, false);
+#endif
     __syncthreads();
+    if (clk) st->dbg[20] = clock64() - c0;
+    F2_STAMP(st, 18);
     const int kb = F.final_kb;
     if (kb < 0) return -1;
 
-    if (tid < kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
-        int x = tid;
+    // warp 0: L11^-1 while the others derive everything that does not need it
+#ifndef F2_ONE_WARP_PIVOTS
+    if (warp == 0) warp_linv(F, kb);
+#endif
+    if (tid >= 32 && tid < 32 + kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
+        const int sl = tid - 32;
+        int x = sl;
         for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
             int pv[8];
 #pragma unroll
@@ -576,9 +590,9 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
                 if (u < kb) x = x == u ? pv[i] : (x == pv[i] ? u : x);
             }
         }
-        F.src[tid] = x;
-    } else if (tid < kPW + 64) {  // finalize basis
-        const int e = tid - kPW, g = e >> 3, b = e & 7;
+        F.src[sl] = x;
+    } else if (tid >= 32 + kPW && tid < 32 + kPW + 64) {  // finalize basis
+        const int e = tid - 32 - kPW, g = e >> 3, b = e & 7;
         int lo = 0, hi = kb;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -595,7 +609,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
             }
         }
         pk->fb[e] = corr;
-        F.rraw[e] = corr;  // also the carry tables' basis (rraw reused below)
+        F.fbas[e] = corr;
     } else if (tid >= 256 && tid < 320) {
         const int l = tid - 256;
         const bool in = l < kb;
@@ -609,28 +623,29 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     if (first)
         for (int i = tid; i < nleaves * 64; i += kPT) st->brow[i] = -1;
     __syncthreads();
+    F2_STAMP(st, 19);
     // carry finalize tables from the basis; posc; L11^-1 rows in raw columns (for lmap)
     for (int i = tid; i < 8 * 256; i += kPT) {
         const int g = i >> 8, v = i & 255;
         uint64_t f = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b)
-            if ((v >> b) & 1) f ^= F.rraw[8 * g + b];
+            if ((v >> b) & 1) f ^= F.fbas[8 * g + b];
         S.F[i] = f;
     }
     if (tid < kb) F.posc[F.step_c[tid]] = tid;
-    __syncthreads();
-    if (tid < 64) {
+    if (tid >= 960) {
+        const int l = tid - 960;
         uint64_t r = 0;
-        if (tid < kb) {
-            uint64_t lv = F.linv[tid];
+        if (l < kb) {
+            uint64_t lv = F.linv[l];
             while (lv) {
                 const int tt = __ffsll(static_cast<long long>(lv)) - 1;
                 lv &= lv - 1;
                 r |= 1ull << F.step_c[tt];
             }
         }
-        F.rraw[tid] = r;
+        F.rraw[l] = r;
     }
     // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order)
     for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
@@ -642,6 +657,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         S.t16[ge * 15 + k] = v;
     }
     __syncthreads();
+    F2_STAMP(st, 21);
     // panel-TRSM map of this leaf
     for (int i = tid; i < 8 * 256; i += kPT) {
         const int g = i >> 8, v = i & 255;
@@ -682,6 +698,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->brow[leaf * 64 + F.step_c[l]] = base + l;
     }
     __syncthreads();
+    F2_STAMP(st, 22);
     // pivot rows' slices: earlier leaf words as carried, the final leaf word, U
     for (int i = tid; i < kb * 16; i += kPT) {
         const int l = i >> 4, k = i & 15;
@@ -739,6 +756,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         }
     }
     __syncthreads();
+    if (clk) st->dbg[21] = clock64() - c0;
     return kb;
 }
 
@@ -771,13 +789,21 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
             __syncthreads();
         }
         if (state == S_DONE) break;
+#ifdef F2_PANEL_PROFILE
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = (pw0 == 0 && leaf == 2 && state == S_CARRY);
+        __syncthreads();
+#endif
+        F2_STAMP(st, 0);
         if (blockIdx.x == 0) {
             int64_t nstate = S_DONE, nleaf = leaf, nwpk = -1, nwleaf = 0;
             const int j = static_cast<int>(leaf);
             const int pb = j & 1;
             if (state == S_FRESH || state == S_CARRY || state == S_FINAL) {
+                const long long cb = clock64();
                 pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
                                   j == 0 ? 0 : st->pmap_hi);
+                if (pw0 == 0 && j == 2 && threadIdx.x == 0) st->dbg[22] = clock64() - cb;
+                F2_STAMP(st, 1);
                 if (state == S_FINAL) {
                     pipe_write_back(A, pw0, nwp, S, Z, pb);
                     nstate = S_DONE;
@@ -785,6 +811,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                     const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
                     PlsState::Packet* pk = &st->pk[pkc & 1];
                     const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves);
+                    F2_STAMP(st, 2);
                     if (kb >= 0) {
                         kbprev = kb;
                         nwpk = pkc & 1;
@@ -835,7 +862,14 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                     update_tile(A, pw0 + wleaf, pw1, pmap, L, ty, Fw, tab, st);
             }
         }
+        F2_STAMP(st, 3);
+#ifdef F2_PANEL_PROFILE
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = 0;
+#endif
+        const long long cbar = clock64();
         grid_barrier(bar, target);
+        if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 0) st->dbg[23] = clock64() - cbar;
+        if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 1) st->dbg[24] = clock64() - cbar;
     }
 }
 

@@ -9,7 +9,9 @@ import paper_1006_1744_b200 as f2
 
 L = f2.load_library("tools/libf2gpu_prof.so")
 L.f2_debug_prof.argtypes = [C.POINTER(C.c_longlong), C.c_int]
-names = {0: "leaf start", 10: "k1 window loaded", 11: "k1 outputs start", 12: "k1 st written", 1: "pivot done",
+names = {0: "iteration start", 1: "window built", 2: "fast leaf done", 3: "ctl written", 16: "transposed",
+         18: "pivot loop + uf/linv", 19: "src/basis", 21: "tables/t16", 22: "lmap/U/P", 17: "loop done"}
+names_old = {0: "leaf start", 10: "k1 window loaded", 11: "k1 outputs start", 12: "k1 st written", 1: "pivot done",
          2: "solve done", 3: "barrier 1 passed", 4: "update prep done", 5: "update done (CTA 0)",
          50: "tile rows loaded", 51: "tile finalized", 52: "tile lookups done"}
 names.update({40 + g: f"solve group {g}" for g in range(8)})
