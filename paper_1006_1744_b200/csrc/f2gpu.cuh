@@ -58,6 +58,8 @@ struct PlsState {
         int32_t q[64];                // pivot bit positions in the leaf word
         uint64_t fb[64];              // finalize basis
         uint64_t u[64][16];           // solved pivot rows over the rest of the panel (word 0 = leaf word + 1)
+        uint64_t linv[64];            // rows of L11^{-1} over pivot indices (pipelined kernel: lmap by a worker)
+        int64_t leaf;                 // leaf index within the panel
     } pk[2];
     int64_t ctl[2][4];                  // pipelined panel kernel: control word per iteration parity
     uint64_t uleaf[64][16];             // the current leaf's solved pivot rows over the rest of the panel

@@ -531,6 +531,44 @@ __device__ void pipe_build_window(const Mat& A, int64_t pw0, int nwp, const int6
     __syncthreads();
 }
 
+// A worker CTA: the panel TRSM's bytewise L11^{-1} map of the packet's leaf (trsm.cu),
+// lmap[g][v] = xor over bits b of v of the L11^{-1} row of the pivot at column 8g+b.
+__device__ void pipe_worker_lmap(PlsState* st, const PlsState::Packet* pk, uint64_t* scratch) {
+    const int tid = threadIdx.x;
+    uint64_t* rraw = scratch;                                  // [64]
+    int* posc = reinterpret_cast<int*>(scratch + 64);          // [64]
+    int* q = posc + 64;                                        // [64]
+    const int kb = static_cast<int>(ldi(&pk->kb));
+    const int leaf = static_cast<int>(ldi(&pk->leaf));
+    if (tid < 64) {
+        q[tid] = __ldcg(&pk->q[tid]);
+        posc[tid] = -1;
+    }
+    __syncthreads();
+    if (tid < 64) {
+        uint64_t lv = tid < kb ? ldw(&pk->linv[tid]) : 0ull, r = 0;
+        while (lv) {
+            const int tt = __ffsll(static_cast<long long>(lv)) - 1;
+            lv &= lv - 1;
+            r |= 1ull << q[tt];
+        }
+        rraw[tid] = r;
+        if (tid < kb) posc[q[tid]] = tid;
+    }
+    __syncthreads();
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t x = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int l = posc[8 * g + b];
+            if (((v >> b) & 1) && l >= 0) x ^= rraw[l];
+        }
+        st->lmap[leaf][g][v] = x;
+    }
+    __syncthreads();
+}
+
 __device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSmem& S, const PipeStatic& Z, int pb) {
     for (int i = threadIdx.x; i < kPW * 16; i += kPT) {
         const int sl = i >> 4, k = i & 15;
@@ -623,6 +661,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     if (first)
         for (int i = tid; i < nleaves * 64; i += kPT) st->brow[i] = -1;
     __syncthreads();
+    if (clk) st->dbg[25] = clock64() - c0;
     F2_STAMP(st, 19);
     // carry finalize tables from the basis; posc; L11^-1 rows in raw columns (for lmap)
     for (int i = tid; i < 8 * 256; i += kPT) {
@@ -634,19 +673,8 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         S.F[i] = f;
     }
     if (tid < kb) F.posc[F.step_c[tid]] = tid;
-    if (tid >= 960) {
-        const int l = tid - 960;
-        uint64_t r = 0;
-        if (l < kb) {
-            uint64_t lv = F.linv[l];
-            while (lv) {
-                const int tt = __ffsll(static_cast<long long>(lv)) - 1;
-                lv &= lv - 1;
-                r |= 1ull << F.step_c[tt];
-            }
-        }
-        F.rraw[l] = r;
-    }
+    if (tid >= 960) pk->linv[tid - 960] = F.linv[tid - 960];  // the lmap is a worker's job
+    if (tid == 0) pk->leaf = leaf;
     // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order)
     for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
         const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
@@ -657,18 +685,8 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         S.t16[ge * 15 + k] = v;
     }
     __syncthreads();
+    if (clk) st->dbg[26] = clock64() - c0;
     F2_STAMP(st, 21);
-    // panel-TRSM map of this leaf
-    for (int i = tid; i < 8 * 256; i += kPT) {
-        const int g = i >> 8, v = i & 255;
-        uint64_t x = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const int l = F.posc[8 * g + b];
-            if (((v >> b) & 1) && l >= 0) x ^= F.rraw[l];
-        }
-        st->lmap[leaf][g][v] = x;
-    }
     // solved rest words U_l = sum over t of Linv[l][t] A12_t
     for (int i = tid; i < 64 * 16; i += kPT) {
         const int l = i >> 4, k = i & 15;
@@ -698,6 +716,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->brow[leaf * 64 + F.step_c[l]] = base + l;
     }
     __syncthreads();
+    if (clk) st->dbg[27] = clock64() - c0;
     F2_STAMP(st, 22);
     // pivot rows' slices: earlier leaf words as carried, the final leaf word, U
     for (int i = tid; i < kb * 16; i += kPT) {
@@ -854,6 +873,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
             }
         } else if (wpk >= 0) {
             const PlsState::Packet* pk = &st->pk[wpk];
+            if (blockIdx.x == 1 && s_ctl[0] != S_IDLE) pipe_worker_lmap(st, pk, X);
             if (ldi(&pk->kb) != 0) {
                 worker_prep(pk, L, X, Fw, tab);
                 const int64_t rows = A.m - L.lo;

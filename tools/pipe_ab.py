@@ -21,5 +21,6 @@ for lib in sys.argv[1:]:
     out = (C.c_longlong * 32)()
     L.f2_debug_clocks(out, 32)
     v = list(out)
-    print(f"{lib}: {best:.2f} ms; leaf2: window {v[22]} loop+uf/linv {v[20]} leaf {v[21]} clk", flush=True)
+    print(f"{lib}: {best:.2f} ms; leaf2 (cumulative clk from the search start): window {v[22]} | loop+uf {v[20]} "
+          f"| src/fb {v[25]} | tables/t16 {v[26]} | lmap/U {v[27]} | leaf {v[21]}", flush=True)
     del a0, a
