@@ -221,12 +221,27 @@ __device__ __forceinline__ void warp0_pivots(FastSmem& F, int lw, bool more, boo
 __device__ __forceinline__ void warp_linv(FastSmem& F, int kb) {
     const int lane = threadIdx.x & 31;
     const uint64_t u0 = F.uf[lane], u1 = F.uf[lane + 32];
-    uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
+    // the L bits of rows lane and lane+32 gathered into pivot-index order first, so the
+    // 64-step chain is one shuffle and two masked XORs per step
+    uint64_t c0 = 0, c1 = 0;
     for (int tt = 0; tt < kb; ++tt) {
         const int qt = F.step_c[tt];
-        const uint64_t Rt = __shfl_sync(FULL, tt < 32 ? R0 : R1, tt & 31);
-        if (lane > tt && ((u0 >> qt) & 1ull)) R0 ^= Rt;
-        if (lane + 32 > tt && ((u1 >> qt) & 1ull)) R1 ^= Rt;
+        c0 |= ((u0 >> qt) & 1ull) << tt;
+        c1 |= ((u1 >> qt) & 1ull) << tt;
+    }
+    c0 &= lane == 0 ? 0ull : (~0ull >> (64 - lane));  // strictly below the row's own index
+    uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
+#pragma unroll 4
+    for (int tt = 0; tt < 32; ++tt) {
+        const uint64_t Rt = __shfl_sync(FULL, R0, tt);
+        R0 ^= ((c0 >> tt) & 1ull) ? Rt : 0ull;
+        R1 ^= ((c1 >> tt) & 1ull) ? Rt : 0ull;
+    }
+    c1 &= lane == 0 ? ~0ull >> 32 : (~0ull >> (32 - lane));  // t < lane + 32
+#pragma unroll 4
+    for (int tt = 32; tt < 64; ++tt) {
+        const uint64_t Rt = __shfl_sync(FULL, R1, tt - 32);
+        R1 ^= ((c1 >> tt) & 1ull) ? Rt : 0ull;
     }
     F.linv[lane] = R0;
     F.linv[lane + 32] = R1;

@@ -614,6 +614,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     // warp 0: L11^-1 while the others derive everything that does not need it
 #ifndef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp_linv(F, kb);
+    if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;
 #endif
     if (tid >= 32 && tid < 32 + kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
         const int sl = tid - 32;
@@ -629,6 +630,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
             }
         }
         F.src[sl] = x;
+        if (pw0 == 0 && leaf == 2 && tid == 32) st->dbg[29] = clock64() - c0;
     } else if (tid >= 32 + kPW && tid < 32 + kPW + 64) {  // finalize basis
         const int e = tid - 32 - kPW, g = e >> 3, b = e & 7;
         int lo = 0, hi = kb;
@@ -648,6 +650,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         }
         pk->fb[e] = corr;
         F.fbas[e] = corr;
+        if (pw0 == 0 && leaf == 2 && e == 63) st->dbg[30] = clock64() - c0;
     } else if (tid >= 256 && tid < 320) {
         const int l = tid - 256;
         const bool in = l < kb;

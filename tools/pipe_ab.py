@@ -22,5 +22,5 @@ for lib in sys.argv[1:]:
     L.f2_debug_clocks(out, 32)
     v = list(out)
     print(f"{lib}: {best:.2f} ms; leaf2 (cumulative clk from the search start): window {v[22]} | loop+uf {v[20]} "
-          f"| src/fb {v[25]} | tables/t16 {v[26]} | lmap/U {v[27]} | leaf {v[21]}", flush=True)
+          f"| src/fb {v[25]} (linv {v[28]} src {v[29]} fb {v[30]}) | tables/t16 {v[26]} | lmap/U {v[27]} | leaf {v[21]}", flush=True)
     del a0, a
