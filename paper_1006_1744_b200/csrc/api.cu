@@ -350,7 +350,8 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             ta.st = g.st;
             // work is data dependent; filled in from the pivots after the call
             LaunchTimer t(0, static_cast<double>(pi), -1.0);
-            launch_table_apply(s, ta, g.nsm);
+            // expected rows below the panel's pivots if every panel so far had full rank
+            launch_table_apply(s, ta, g.nsm, m - std::min<int64_t>(m, c + cw));
         }
         if (pw1 >= nw && (rc = enqueue_download(A, c, W, s))) return rc;  // last panel: final after the gather
         if (poll) {  // early exit once every row is a pivot: snapshot r without blocking
@@ -957,7 +958,7 @@ void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0
     const double abytes = 8.0 * static_cast<double>((s + 63) / 64);
     LaunchTimer t(0, static_cast<double>(p) * (2.0 * cbytes + abytes) + static_cast<double>(s) * cbytes,
                   2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
-    launch_table_apply(g.stream, ta, g.nsm);
+    launch_table_apply(g.stream, ta, g.nsm, p);
 }
 
 // B <- L^{-1} B for L = Lm rows/cols [o, o+r) (o % 64 == 0) and B = Bm rows [o, o+r)

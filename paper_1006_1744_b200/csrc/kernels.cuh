@@ -53,8 +53,9 @@ struct TableApply {
     const int64_t* brow;
     int row_mode;          // RowMode: static / after leaf / after panel (c_r0 = a_r0 from state)
     const PlsState* st;
+    int64_t row_tile0;     // first 1024-row tile of this launch (set by launch_table_apply)
 };
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm);
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0);
 void setup_m4rm_kernels();
 
 // misc.cu

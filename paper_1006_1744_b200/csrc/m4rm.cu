@@ -21,6 +21,7 @@
 // The coefficient words of the tile's rows are staged in SMEM one K-word ahead.
 // SMEM bandwidth bounds it: per chunk 1024 lookups x 128 B + 256 table rows x 128 B.
 #include <cstdint>
+#include <cstdlib>
 
 #include "f2gpu.cuh"
 #include "kernels.cuh"
@@ -97,8 +98,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         if (p.st->panel_kb == 0) return;
         c_r0 = a_r0 = p.st->panel_r + p.st->panel_kb;
     }
-    const int64_t row_base = c_r0 + static_cast<int64_t>(blockIdx.y) * kTM;
+    const int64_t row_base = c_r0 + (p.row_tile0 + static_cast<int64_t>(blockIdx.y)) * kTM;
     if (row_base >= p.c_r1) return;
+    // K split (gridDim.z > 1): this CTA takes coefficient words [kw0, kw0 + kwn) and
+    // XORs its partial product into C atomically (GF(2) addition is order-free)
+    const int wps = (p.kw + static_cast<int>(gridDim.z) - 1) / static_cast<int>(gridDim.z);
+    const int kw0 = static_cast<int>(blockIdx.z) * wps;
+    if (kw0 >= p.kw) return;
+    const int kwn = p.kw - kw0 < wps ? p.kw - kw0 : wps;
+    const int64_t kbits_l = p.kbits - 64 * kw0 < 64 * kwn ? p.kbits - 64 * kw0 : 64 * kwn;
+    if (kbits_l <= 0) return;
+    const int64_t aw0_l = p.aw0 + kw0;
+    const int64_t* brow_l = p.brow ? p.brow + 64 * kw0 : nullptr;
+    const int64_t b_r0_l = p.b_r0 + 64 * kw0;
+    const bool split = gridDim.z > 1;
     const int64_t tile_w0 = p.cw0 + static_cast<int64_t>(blockIdx.x) * kTNW;
     const int64_t arow_base = a_r0 + (row_base - c_r0);
     const int64_t nrows = p.c_r1 - row_base < kTM ? p.c_r1 - row_base : kTM;
@@ -107,13 +120,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     const int rq = lane >> 3, wp = lane & 7;
     const int64_t cwa = tile_w0 + 2 * wp, cwb = cwa + 1;
     const bool va = cwa < p.cw1, vb = cwb < p.cw1;
-    const int nch = static_cast<int>((p.kbits + 7) / 8);
-    const bool mapped = p.brow != nullptr;
+    const int nch = static_cast<int>((kbits_l + 7) / 8);
+    const bool mapped = brow_l != nullptr;
 
     // B row map and live-chunk mask for the whole K range
     if (mapped) {
         for (int j = tid; j < nch * 8; j += kThreads) {
-            int64_t r = j < p.kbits ? p.brow[j] : -1;
+            int64_t r = j < kbits_l ? brow_l[j] : -1;
             bmap[j] = static_cast<int32_t>(r);
         }
         __syncthreads();
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
 
     auto brow_of = [&](int j) -> int64_t {
         if (mapped) return bmap[j];
-        return j < p.kbits ? p.b_r0 + j : -1;
+        return j < kbits_l ? b_r0_l + j : -1;
     };
     auto live = [&](int c) -> bool { return mapped ? ((livebits[c >> 5] >> (c & 31)) & 1u) : c < nch; };
 
@@ -152,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
     auto issue_a = [&](int g) {
         for (int r = tid; r < kTM; r += kThreads) {
             const bool ok = r < nrows;
-            const uint64_t* src = ok ? p.A.w + (arow_base + r) * p.A.stride + p.aw0 + g : p.A.w;
+            const uint64_t* src = ok ? p.A.w + (arow_base + r) * p.A.stride + aw0_l + g : p.A.w;
             cp_async8(abuf + (g & 1) * kTM + r, src, ok);
         }
     };
@@ -200,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         const int64_t row = row_base + warp * 64 + rq + 4 * i;
         const bool rv = row < p.c_r1;
         const uint64_t* cr = p.C.w + row * p.C.stride;
-        acc0[i] = (rv && va) ? cr[cwa] : 0ull;
-        acc1[i] = (rv && vb) ? cr[cwb] : 0ull;
+        acc0[i] = (rv && va && !split) ? cr[cwa] : 0ull;
+        acc1[i] = (rv && vb && !split) ? cr[cwb] : 0ull;
     }
 
 #ifdef F2_SCHUR_PAIRS
@@ -270,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         build_half(c + 3, 1);
         if (c + 6 < nch) issue_b(c + 6);
         if (c + 7 < nch) issue_b(c + 7);
-        if ((c & 7) == 0 && (c >> 3) + 1 < p.kw && (c >> 3) + 1 < (nch + 7) / 8) issue_a((c >> 3) + 1);
+        if ((c & 7) == 0 && (c >> 3) + 1 < kwn && (c >> 3) + 1 < (nch + 7) / 8) issue_a((c >> 3) + 1);
         cp_async_commit();
 #ifndef F2_EXP_NOLOOKUP
         lookups(c, aw);
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
             const int c = g * 8 + j;
             if (c < nch) {
                 if (c + 3 < nch) issue_b(c + 3);
-                if (j == 0 && g + 1 < p.kw && g + 1 < ngroups) issue_a(g + 1);
+                if (j == 0 && g + 1 < kwn && g + 1 < ngroups) issue_a(g + 1);
                 cp_async_commit();
                 cp_async_wait<2>();
                 __syncthreads();
@@ -330,22 +343,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         const int64_t row = row_base + warp * 64 + rq + 4 * i;
         if (row < p.c_r1) {
             uint64_t* cr = p.C.w + row * p.C.stride;
-            if (va) cr[cwa] = acc0[i];
-            if (vb) cr[cwb] = acc1[i];
+            if (split) {
+                if (va) atomicXor(reinterpret_cast<unsigned long long*>(cr + cwa), acc0[i]);
+                if (vb) atomicXor(reinterpret_cast<unsigned long long*>(cr + cwb), acc1[i]);
+            } else {
+                if (va) cr[cwa] = acc0[i];
+                if (vb) cr[cwb] = acc1[i];
+            }
         }
     }
 }
 
 static size_t table_apply_smem() { return kSmem; }
 
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm) {
-    (void)nsm;
+// One launch over all row tiles, or -- when the tile count leaves a partial last wave
+// -- the rows that fill whole waves first, then the remaining row tiles with K split
+// across gridDim.z CTAs (atomic XOR into C) so the tail wave is short.  expect_rows
+// (the caller's estimate of the device-side row count; <= 0: unknown) only steers
+// the split; correctness never depends on it.
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows) {
     if (t.cw1 <= t.cw0 || t.kbits <= 0) return;
     const int64_t lo = t.row_mode == ROWS_STATIC ? t.c_r0 : 0;
     const int64_t rows = t.c_r1 - lo;
     if (rows <= 0) return;
-    dim3 grid(static_cast<unsigned>((t.cw1 - t.cw0 + kTNW - 1) / kTNW), static_cast<unsigned>((rows + kTM - 1) / kTM));
-    k_table_apply<<<grid, kThreads, table_apply_smem(), s>>>(t);
+    const int64_t nct = (t.cw1 - t.cw0 + kTNW - 1) / kTNW;
+    const int64_t nrt = (rows + kTM - 1) / kTM;
+    int64_t y0 = nrt;
+    int splitk = 1;
+    if (expect_rows > 0 && nsm > 0 && t.kw >= 2 && !std::getenv("F2_NO_KSPLIT")) {
+        const int64_t ert = (expect_rows + kTM - 1) / kTM;  // expected row tiles
+        const int64_t tiles = ert * nct;
+        const int64_t full_waves = tiles / nsm;
+        const int64_t ya = full_waves * nsm / nct;  // row tiles that fit whole waves
+        const int64_t tail = (ert - ya) * nct;
+        if (ya < ert && tail > 0) {
+            int sk = static_cast<int>(nsm / tail);
+            if (sk > t.kw) sk = t.kw;
+            if (sk >= 2) {
+                y0 = ya;
+                splitk = sk;
+            }
+        }
+    }
+    if (y0 > 0) {
+        TableApply a = t;
+        a.row_tile0 = 0;
+        k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(y0), 1), kThreads, table_apply_smem(),
+                        s>>>(a);
+    }
+    if (y0 < nrt) {
+        TableApply b = t;
+        b.row_tile0 = y0;
+        k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(nrt - y0), static_cast<unsigned>(splitk)),
+                        kThreads, table_apply_smem(), s>>>(b);
+    }
 }
 
 void setup_m4rm_kernels() {
