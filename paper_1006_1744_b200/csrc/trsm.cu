@@ -18,6 +18,7 @@
 // them are prepared up front in parallel; each group then costs one table build
 // and one lookup pass (two barriers) and no serial in-group solve.
 #include <cstdint>
+#include <cstdlib>
 
 #include "f2gpu.cuh"
 #include "kernels.cuh"
@@ -355,14 +356,163 @@ static size_t panel_trsm_smem(int nleaves) {
            sizeof(int16_t) * rows + sizeof(int32_t) * (nleaves + 8);
 }
 
+
+// The same panel TRSM on 512-bit column strips (kPTW8 = 8 words): one wave of CTAs
+// at 64K columns, and every table entry / row slice is 64 B read by 4 lanes with
+// 16-byte accesses (the 4-word version's 32-B entries read by single lanes conflict).
+namespace {
+constexpr int kPTW8 = 8;
+}
+
+__global__ void __launch_bounds__(512, 1)
+k_panel_trsm8(Mat A, Mat Cf, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1, const PlsState* st) {
+    extern __shared__ __align__(16) uint64_t smem[];
+    const int rows_cap = nleaves * 64;
+    uint64_t* X = smem;                                               // [rows_cap][8]
+    uint64_t* T = X + rows_cap * kPTW8;                               // [8][256][8]
+    uint64_t* Lm = T + 8 * 256 * kPTW8;                               // [8][256]
+    uint64_t* cw = Lm + 8 * 256;                                      // [rows_cap]
+    int32_t* sq = reinterpret_cast<int32_t*>(cw + rows_cap);          // [rows_cap]
+    int16_t* posrow = reinterpret_cast<int16_t*>(sq + rows_cap);      // [rows_cap]
+    int32_t* bstart = reinterpret_cast<int32_t*>(posrow + rows_cap);  // [nleaves + 1]
+
+    const int nk = static_cast<int>(st->panel_kb);
+    const int64_t r0 = st->panel_r;
+    if (nk <= 1) return;
+    const int64_t tb = tw0 + static_cast<int64_t>(blockIdx.x) * kPTW8;
+    if (tb >= tw1) return;
+    const int ntw = static_cast<int>(tw1 - tb < kPTW8 ? tw1 - tb : kPTW8);
+    const int tid = threadIdx.x;
+
+    for (int t = tid; t < nk; t += 512) sq[t] = st->panel_q[t];
+    for (int i = tid; i < rows_cap; i += 512) posrow[i] = -1;
+    for (int i = tid; i < nk * kPTW8; i += 512) {
+        const int t = i >> 3, j = i & 7;
+        X[i] = j < ntw ? A.w[(r0 + t) * A.stride + tb + j] : 0ull;
+    }
+    __syncthreads();
+    for (int t = tid; t < nk; t += 512) posrow[sq[t]] = static_cast<int16_t>(t);
+    for (int j = tid; j <= nleaves; j += 512) {
+        int lo = 0, hi = nk;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sq[mid] < 64 * j) lo = mid + 1;
+            else hi = mid;
+        }
+        bstart[j] = lo;
+    }
+    __syncthreads();
+
+    constexpr int kLmPer = 8 * 256 / 512, kCwPer = kMaxTrsmBits / 512;
+    uint64_t pf_lm[kLmPer], pf_cw[kCwPer];
+    auto prefetch = [&](int j) {
+        if (j >= nleaves) return;
+        const int t0 = bstart[j];
+#pragma unroll
+        for (int u = 0; u < kLmPer; ++u) pf_lm[u] = (&st->lmap[j][0][0])[tid + u * 512];
+#pragma unroll
+        for (int u = 0; u < kCwPer; ++u) {
+            const int t = t0 + tid + u * 512;
+            pf_cw[u] = t < nk ? Cf.w[(r0 + t) * Cf.stride + coef_w0 + j] : 0ull;
+        }
+    };
+    prefetch(0);
+    const int sub = tid & 3, grp = tid >> 2;  // update: 4 lanes per row, 16 B each
+    for (int j = 0; j < nleaves; ++j) {
+        const int t0 = bstart[j], t1 = bstart[j + 1];
+        if (t0 == t1) {
+            prefetch(j + 1);
+            continue;
+        }
+#pragma unroll
+        for (int u = 0; u < kLmPer; ++u) Lm[tid + u * 512] = pf_lm[u];
+#pragma unroll
+        for (int u = 0; u < kCwPer; ++u) {
+            const int t = t0 + tid + u * 512;
+            if (t < nk) cw[t] = pf_cw[u];
+        }
+        prefetch(j + 1);
+        // 8 tables over block j's rows as they are now: thread = (table g, 16-B chunk wc,
+        // low nibble el); a warp covers 8 consecutive entries x 64 B (conflict-free)
+        {
+            const int g = tid >> 6, wc = tid & 3, el = (tid >> 2) & 15;
+            uint4 v[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int l = posrow[64 * j + 8 * g + b];
+                v[b] = l >= 0 ? *reinterpret_cast<const uint4*>(X + l * kPTW8 + 2 * wc) : make_uint4(0, 0, 0, 0);
+            }
+            uint4 x = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if ((el >> b) & 1) {
+                    x.x ^= v[b].x;
+                    x.y ^= v[b].y;
+                    x.z ^= v[b].z;
+                    x.w ^= v[b].w;
+                }
+            uint64_t* tg = T + g * 256 * kPTW8 + 2 * wc;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k) {
+                    const uint4 h = v[4 + ((k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3)))];
+                    x.x ^= h.x;
+                    x.y ^= h.y;
+                    x.z ^= h.z;
+                    x.w ^= h.w;
+                }
+                const int eh = k ^ (k >> 1);
+                *reinterpret_cast<uint4*>(tg + (eh * 16 + el) * kPTW8) = x;
+            }
+        }
+        __syncthreads();
+        for (int t = t0 + grp; t < nk; t += 128) {
+            uint64_t c = cw[t];
+            if (t < t1) c &= (1ull << (sq[t] - 64 * j)) - 1ull;
+            uint64_t M = 0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) M ^= Lm[g * 256 + ((c >> (8 * g)) & 0xffu)];
+            uint4 a = *reinterpret_cast<const uint4*>(X + t * kPTW8 + 2 * sub);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const uint4 b = *reinterpret_cast<const uint4*>(T + (g * 256 + ((M >> (8 * g)) & 0xffu)) * kPTW8 + 2 * sub);
+                a.x ^= b.x;
+                a.y ^= b.y;
+                a.z ^= b.z;
+                a.w ^= b.w;
+            }
+            *reinterpret_cast<uint4*>(X + t * kPTW8 + 2 * sub) = a;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < nk * kPTW8; i += 512) {
+        const int t = i >> 3, jj = i & 7;
+        if (jj < ntw) A.w[(r0 + t) * A.stride + tb + jj] = X[i];
+    }
+}
+
+static size_t panel_trsm8_smem(int nleaves) {
+    const size_t rows = static_cast<size_t>(nleaves) * 64;
+    return sizeof(uint64_t) * (rows * kPTW8 + 8 * 256 * kPTW8 + 8 * 256 + rows) + sizeof(int32_t) * rows +
+           sizeof(int16_t) * rows + sizeof(int32_t) * (nleaves + 8);
+}
+
 void launch_panel_trsm(cudaStream_t s, const Mat& A, const Mat& Cf, int64_t coef_w0, int nleaves, int64_t tw0,
                        int64_t tw1, const PlsState* st) {
     if (tw1 <= tw0) return;
-    const int grid = static_cast<int>((tw1 - tw0 + kPTW - 1) / kPTW);
-    k_panel_trsm<<<grid, 512, panel_trsm_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
+    static const bool narrow = std::getenv("F2_TRSM4") != nullptr;
+    if (narrow) {
+        const int grid = static_cast<int>((tw1 - tw0 + kPTW - 1) / kPTW);
+        k_panel_trsm<<<grid, 512, panel_trsm_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
+    } else {
+        const int grid = static_cast<int>((tw1 - tw0 + kPTW8 - 1) / kPTW8);
+        k_panel_trsm8<<<grid, 512, panel_trsm8_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
+    }
 }
 
 void setup_trsm_kernels() {
+    cudaFuncSetAttribute(k_panel_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(panel_trsm8_smem(kMaxTrsmBits / 64)));
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(panel_trsm_smem(kMaxTrsmBits / 64)));
     cudaFuncSetAttribute(k_pivot_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
