@@ -134,6 +134,8 @@ struct FastSmem {
     uint64_t step_e[64][2];
     uint32_t ufl[64], ufh[64];   // pivot rows' leaf words, columns 0-31 / 32-63
     uint64_t fbas[64];           // finalize basis
+    uint64_t cfin[64];           // post-search column masks, slots 0..63 (bit l = row l's bit in column c)
+    uint32_t ainv[32], brows[32];
     volatile int q_n;            // steps published
     volatile int q_done[2];      // warp w finished selecting: its final step count, -1 when undecidable
 };
@@ -247,6 +249,51 @@ __device__ __forceinline__ void warp_linv(FastSmem& F, int kb) {
     F.linv[lane + 32] = R1;
 }
 
+// Warps 0 and 1: rows of L11^{-1} (pivot-index coordinates) from the post-search
+// column masks.  Column q_t's mask holds, in bit l, row l's bit at that column, so
+// one transpose gives every row's L bits in pivot order; then L11 = [A 0; B C] in
+// 32x32 blocks: A^{-1} (warp 0) and C^{-1} (warp 1) by 32-step shuffle chains in
+// parallel, and the off-diagonal block C^{-1} B A^{-1} by two independent passes.
+__device__ __forceinline__ void pair_linv(FastSmem& F, int kb) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int tt = 32 * w + lane;
+    const uint64_t vt = tt < kb ? F.cfin[F.step_c[tt]] : 0ull;  // bit l: L[l][tt] (for l > tt)
+    uint32_t rows, rowsb = 0;
+    if (w == 0) {
+        rows = warp_transpose32(static_cast<uint32_t>(vt), lane) & ((1u << lane) - 1u);  // A rows
+        rowsb = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane);                 // B rows
+    } else {
+        (void)warp_transpose32(static_cast<uint32_t>(vt), lane);
+        rows = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane) & ((1u << lane) - 1u);  // C rows
+    }
+    uint32_t R = 1u << lane;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+        const uint32_t Rt = __shfl_sync(FULL, R, t);
+        R ^= ((rows >> t) & 1u) ? Rt : 0u;
+    }
+    if (w == 0) {
+        F.ainv[lane] = R;
+        F.brows[lane] = rowsb;
+    }
+    asm volatile("bar.sync 2, 64;\n" ::: "memory");
+    if (w == 0) {
+        F.linv[lane] = R;
+    } else {
+        const uint32_t b = F.brows[lane];
+        uint32_t y = 0;  // (B A^{-1}) row
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) y ^= ((b >> t) & 1u) ? F.ainv[t] : 0u;
+        uint32_t z = 0;  // (C^{-1} B A^{-1}) row
+#pragma unroll 8
+        for (int sidx = 0; sidx < 32; ++sidx) {
+            const uint32_t ys = __shfl_sync(FULL, y, sidx);
+            z ^= ((R >> sidx) & 1u) ? ys : 0u;
+        }
+        F.linv[32 + lane] = static_cast<uint64_t>(z) | (static_cast<uint64_t>(R) << 32);
+    }
+}
+
 // Warps 0 and 1: the same pivot rule with the columns split, lane l of warp w owning
 // column 32w + l.  Warp 0 selects the pivots of columns 0-31 while warp 1 replays each
 // published step (slot swap + masked XOR) on its columns; then warp 1 selects columns
@@ -256,14 +303,24 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int col = 32 * w + lane;
     U128 C;
-    C.lo = F.colw[col * 4] | (static_cast<uint64_t>(F.colw[col * 4 + 1]) << 32);
-    C.hi = F.colw[col * 4 + 2] | (static_cast<uint64_t>(F.colw[col * 4 + 3]) << 32);
+    if (w < 2) {
+        C.lo = F.colw[col * 4] | (static_cast<uint64_t>(F.colw[col * 4 + 1]) << 32);
+        C.hi = F.colw[col * 4 + 2] | (static_cast<uint64_t>(F.colw[col * 4 + 3]) << 32);
+    } else {
+        // warp 2 tracks the slot permutation: lane b < 7 holds the mask of slots whose
+        // pre-leaf index has bit b set; it replays every swap, so at the end bit b of
+        // slot s's source index sits in bit s of mask b
+        const uint64_t pat[6] = {0xAAAAAAAAAAAAAAAAull, 0xCCCCCCCCCCCCCCCCull, 0xF0F0F0F0F0F0F0F0ull,
+                                 0xFF00FF00FF00FF00ull, 0xFFFF0000FFFF0000ull, 0xFFFFFFFF00000000ull};
+        C.lo = lane < 6 ? pat[lane] : 0ull;
+        C.hi = lane < 6 ? pat[lane] : (lane == 6 ? ~0ull : 0ull);
+    }
     if (threadIdx.x == 0) {
         F.q_n = 0;
         F.q_done[0] = -2;
         F.q_done[1] = -2;
     }
-    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    asm volatile("bar.sync 1, 96;\n" ::: "memory");
     auto apply = [&](int t, int p, uint64_t elo, uint64_t ehi, bool xr) {
         const uint64_t tb = 1ull << t;
         const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
@@ -276,6 +333,32 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     };
     int t = 0;
     bool ok = true;
+    if (w == 2) {
+        for (int phase = 0; phase < 2 && ok; ++phase) {
+            if (32 * phase >= lw) break;
+            while (true) {
+                int n;
+                asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(n) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
+                const int dn = F.q_done[phase];
+                __threadfence_block();
+                for (; t < n; ++t) apply(t, F.step_p[t], 0ull, 0ull, false);
+                if (dn != -2) {
+                    if (dn < 0) ok = false;
+                    else
+                        for (; t < dn; ++t) apply(t, F.step_p[t], 0ull, 0ull, false);
+                    break;
+                }
+            }
+        }
+        if (ok) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t m = k < 2 ? C.lo : C.hi;
+                const uint32_t piece = static_cast<uint32_t>(m >> (32 * (k & 1)));
+                F.src[32 * k + lane] = static_cast<int>(warp_transpose32(piece, lane) & 127u);
+            }
+        }
+    } else
     for (int phase = 0; phase < 2; ++phase) {
         const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32;
         if (w == phase) {
@@ -339,7 +422,8 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
         if (!ok) break;
     }
     if (lane == 0 && w == 0) F.final_kb = ok ? t : -1;
-    if (ok) {
+    if (w < 2) F.cfin[col] = C.lo;
+    if (ok && w < 2) {
         // pivot rows' final leaf words (slots 0..63), this warp's 32 columns
         const uint32_t r0 = warp_transpose32(static_cast<uint32_t>(C.lo), lane);
         const uint32_t r1 = warp_transpose32(static_cast<uint32_t>(C.lo >> 32), lane);
@@ -351,7 +435,7 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
             F.ufh[lane + 32] = r1;
         }
     }
-    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    asm volatile("bar.sync 1, 96;\n" ::: "memory");
     if (ok && w == 0) {
         const uint64_t u0 = F.ufl[lane] | (static_cast<uint64_t>(F.ufh[lane]) << 32);
         const uint64_t u1 = F.ufl[lane + 32] | (static_cast<uint64_t>(F.ufh[lane + 32]) << 32);
@@ -397,14 +481,18 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
 #ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kFW < m, scratch != nullptr, st);
 #else
-    if (warp < 2) two_warp_pivots(F, lw, base + kFW < m, scratch != nullptr);
+    if (warp < 3) two_warp_pivots(F, lw, base + kFW < m, scratch != nullptr);
 #endif
     __syncthreads();
     F2_STAMP(st, 18);
     const int kb = F.final_kb;
     if (kb < 0) return false;
 
+#ifdef F2_ONE_WARP_PIVOTS
     if (tid < kFW) {
+#else
+    if (false) {
+#endif
         // slot sources: walk the transpositions backwards (LAPACK order, perm.cpp:8-16)
         int x = tid;
         for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {

@@ -603,7 +603,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
 #ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
 #else
-    if (warp < 2) two_warp_pivots(F, lw, base + kPW < m, false);
+    if (warp < 3) two_warp_pivots(F, lw, base + kPW < m, false);
 #endif
     __syncthreads();
     if (clk) st->dbg[20] = clock64() - c0;
@@ -613,10 +613,12 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
 
     // warp 0: L11^-1 while the others derive everything that does not need it
 #ifndef F2_ONE_WARP_PIVOTS
-    if (warp == 0) warp_linv(F, kb);
+    if (warp < 2) pair_linv(F, kb);
     if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;
-#endif
+    if (false) {  // slot sources come from the search's tracker warp
+#else
     if (tid >= 32 && tid < 32 + kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
+#endif
         const int sl = tid - 32;
         int x = sl;
         for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
