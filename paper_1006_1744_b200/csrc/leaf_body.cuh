@@ -348,6 +348,9 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                         for (; t < dn; ++t) apply(t, F.step_p[t], 0ull, 0ull, false);
                     break;
                 }
+#ifdef F2_POLL_SLEEP
+                __nanosleep(F2_POLL_SLEEP);
+#endif
             }
         }
         if (ok) {
@@ -384,15 +387,8 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 F.step_e[t][0] = elo;
                 F.step_e[t][1] = ehi;
                 ++t;
-                __syncwarp();
-#ifdef F2_PUB_FENCE
-                if (lane == 0) {
-                    __threadfence_block();
-                    F.q_n = t;
-                }
-#else
-                if (lane == 0) asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
-#endif
+                // every lane stored the same step and releases the same count: no branch
+                asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
             }
             __syncwarp();
             if (lane == 0) {
@@ -414,8 +410,8 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                         for (; t < dn; ++t) apply(t, F.step_p[t], F.step_e[t][0], F.step_e[t][1], w > phase);
                     break;
                 }
-#ifdef F2_PUB_SLEEP
-                __nanosleep(20);
+#ifdef F2_POLL_SLEEP
+                __nanosleep(F2_POLL_SLEEP);
 #endif
             }
         }
