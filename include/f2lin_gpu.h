@@ -182,6 +182,8 @@ uint64_t f2_last_launch_count(void);
 int f2_debug_clocks(long long* out, int n);
 /* globaltimer stamps of the panel kernel (only builds compiled with -DF2_PANEL_PROFILE fill them) */
 int f2_debug_prof(long long* out, int n);
+/* per-panel start/end stamps of the panel kernel and the Schur (only -DF2_TIMELINE builds fill them) */
+int f2_debug_timeline(unsigned long long* out, int n);
 /* engine tuning (panel width in bits for pls_recursive; 0 = default) */
 int f2_set_panel_bits(unsigned bits);
 

@@ -65,6 +65,13 @@ struct Ctx {
     unsigned* bar = nullptr;  // grid barrier counter of k_panel_leaves
     bool fused = true;        // panel leaves in one persistent kernel (F2_UNFUSED=1: three launches per leaf)
     bool pipe = true;         // pipelined panel kernel (F2_NO_PIPE=1: one leaf per barrier pair)
+    // look-ahead: panel p+1's kernel runs on a high-priority side stream with side_ctas
+    // CTAs while the Schur update of panel p covers the columns right of panel p+1
+    bool lookahead = true;    // F2_NO_LOOKAHEAD=1 disables
+    int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
+    cudaStream_t side = nullptr;
+    cudaEvent_t la_fork = nullptr, la_join = nullptr;
+    int64_t* snap = nullptr;  // [2][2 + kMaxPanelBits]
     uint64_t* scratch = nullptr;
     size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
@@ -127,6 +134,19 @@ int ensure_init() {
     CK(cudaMalloc(&g.bar, sizeof(unsigned)));
     g.fused = !(std::getenv("F2_UNFUSED") && std::getenv("F2_UNFUSED")[0] == '1');
     g.pipe = !(std::getenv("F2_NO_PIPE") && std::getenv("F2_NO_PIPE")[0] == '1');
+    g.lookahead = !(std::getenv("F2_NO_LOOKAHEAD") && std::getenv("F2_NO_LOOKAHEAD")[0] == '1');
+    if (const char* e = std::getenv("F2_SIDE_CTAS")) {
+        const int v = std::atoi(e);
+        if (v >= 2 && v <= g.nsm) g.side_ctas = v;
+    }
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&g.side, cudaStreamNonBlocking, hi));
+        CK(cudaEventCreateWithFlags(&g.la_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.la_join, cudaEventDisableTiming));
+        CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * (2 + kMaxPanelBits)));
+    }
     CK(cudaGetLastError());
     g.init = true;
     return F2_OK;
@@ -285,17 +305,33 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
     const int64_t nw = (n + 63) / 64;
     const int64_t npanels = (n + W - 1) / W;
     CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), s));
+#ifdef F2_TIMELINE
+    CK(cudaMemsetAsync(&g.st->tl[0][0], 0xff, sizeof(g.st->tl[0]), s));  // min slots
+    CK(cudaMemsetAsync(&g.st->tl[2][0], 0xff, sizeof(g.st->tl[2]), s));
+#endif
     launch_pmap_init(s, g.pmap, m);
     std::vector<cudaEvent_t> evs;
     int64_t checked = 0;
     bool stop = false;
+
+    const bool la = g.lookahead && g.fused && g.pipe && !g.stats && npanels > 1;
+    // the side kernel is launched cooperatively too: the scheduler then places all its
+    // CTAs next to the running Schur update at once (plain launches waited for it to drain)
+    auto panel_kernel = [&](cudaStream_t st_, int64_t pi_, int ctas) {
+        const int64_t c_ = pi_ * W, cw_ = std::min<int64_t>(W, n - c_);
+        const int64_t pw0_ = c_ / 64, pw1_ = pw0_ + (cw_ + 63) / 64;
+        launch_panel_pipe(st_, A, pw0_, static_cast<int>(cw_), pw1_, g.st, g.P, g.Qp, g.pmap, 0, g.bar, ctas, true);
+    };
+    if (la) panel_kernel(s, 0, g.nsm);
 
     for (int64_t pi = 0; pi < npanels && !stop; ++pi) {
         const int64_t c = pi * W;
         const int64_t cw = std::min<int64_t>(W, n - c);
         const int nleaves = static_cast<int>((cw + 63) / 64);
         const int64_t pw0 = c / 64, pw1 = pw0 + nleaves;
-        if (g.fused) {
+        if (la) {
+            // panel pi's kernel ran ahead (panel 0: above; others: on the side stream)
+        } else if (g.fused) {
             LaunchTimer t(1, 0, 0);
             if (g.pipe)
                 launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
@@ -348,10 +384,34 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             ta.brow = g.st->brow;
             ta.row_mode = ROWS_AFTER_PANEL;
             ta.st = g.st;
-            // work is data dependent; filled in from the pivots after the call
-            LaunchTimer t(0, static_cast<double>(pi), -1.0);
-            // expected rows below the panel's pivots if every panel so far had full rank
-            launch_table_apply(s, ta, g.nsm, m - std::min<int64_t>(m, c + cw));
+            const int64_t erows = m - std::min<int64_t>(m, c + cw);  // rows below the pivots at full rank
+            if (la) {
+                // Schur of panel pi on panel pi+1's columns, then panel pi+1's kernel on the
+                // side stream while the Schur covers the columns right of it
+                int64_t* snap = g.snap + (pi & 1) * (2 + kMaxPanelBits);
+                launch_panel_snapshot(s, g.st, snap, nleaves * 64);
+                ta.brow = snap + 2;
+                ta.rk = snap;
+                const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
+                TableApply t1 = ta;
+                t1.cw1 = npw1;
+                launch_table_apply(s, t1, g.nsm, erows);
+                CK(cudaEventRecord(g.la_fork, s));
+                CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
+                panel_kernel(g.side, pi + 1, g.side_ctas);
+                CK(cudaEventRecord(g.la_join, g.side));
+                if (npw1 < nw) {
+                    TableApply t2 = ta;
+                    t2.cw0 = npw1;
+                    t2.bw0 = npw1;
+                    launch_table_apply(s, t2, g.nsm - g.side_ctas, erows);
+                }
+                CK(cudaStreamWaitEvent(s, g.la_join, 0));
+            } else {
+                // work is data dependent; filled in from the pivots after the call
+                LaunchTimer t(0, static_cast<double>(pi), -1.0);
+                launch_table_apply(s, ta, g.nsm, erows);
+            }
         }
         if (pw1 >= nw && (rc = enqueue_download(A, c, W, s))) return rc;  // last panel: final after the gather
         if (poll) {  // early exit once every row is a pivot: snapshot r without blocking
@@ -888,6 +948,14 @@ int f2_timer_stop(double* ms) {
 }
 
 // phase clocks recorded by builds compiled with -DF2_LEAF_PROFILE (development aid)
+int f2_debug_timeline(unsigned long long* out, int n) {
+    if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
+    static unsigned long long tmp[4 * 128];
+    CK(cudaMemcpy(tmp, &g.st->tl[0][0], sizeof(tmp), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 4 * 128; ++i) out[i] = tmp[i];
+    return F2_OK;
+}
+
 int f2_debug_prof(long long* out, int n) {
     if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
     long long tmp[64];

@@ -66,6 +66,7 @@ struct PlsState {
     uint64_t fbasis[64];                // the current leaf's finalize basis (see panel.cu)
     long long dbg[32];                  // phase clocks (F2_LEAF_PROFILE builds only)
     long long prof[64];                 // globaltimer stamps (F2_PANEL_PROFILE builds only)
+    unsigned long long tl[4][128];      // F2_TIMELINE builds: per panel start/end of the panel kernel and the Schur
 };
 
 // Leaf update geometry (leafupd.cu): kLuRPT rows per quarter-warp lane group, 1024-bit
@@ -99,6 +100,12 @@ static __device__ int g_prof_on = 0;
     do {                 \
     } while (0)
 #endif
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // How a table-apply launch finds its C/A rows (device-side offsets).
 enum RowMode : int { ROWS_STATIC = 0, ROWS_AFTER_LEAF = 1, ROWS_AFTER_PANEL = 2 };

@@ -54,7 +54,11 @@ struct TableApply {
     int row_mode;          // RowMode: static / after leaf / after panel (c_r0 = a_r0 from state)
     const PlsState* st;
     int64_t row_tile0;     // first 1024-row tile of this launch (set by launch_table_apply)
+    const int64_t* rk;     // ROWS_AFTER_PANEL from a snapshot {panel_r, panel_kb} instead of st (look-ahead)
 };
+// snapshot of a finished panel's row range and raw-column -> pivot-row map, so its Schur
+// update can run while the next panel's kernel rewrites the state
+void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int panel_bits);
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0);
 void setup_m4rm_kernels();
 
@@ -72,7 +76,7 @@ void setup_misc_kernels();
 void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st,
                          int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm);
 void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
-                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm);
+                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm, bool cooperative = true);
 void setup_panel_kernels();
 void launch_rref_prepare(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp);
 void launch_rref_coeffs(cudaStream_t s, const Mat& S, int64_t rank, const int64_t* Qp, const Mat& Lrev, int nsm);

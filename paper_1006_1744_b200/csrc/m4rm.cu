@@ -95,10 +95,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         if (p.st->leaf_kb == 0) return;
         c_r0 = a_r0 = p.st->leaf_r + p.st->leaf_kb;
     } else if (p.row_mode == ROWS_AFTER_PANEL) {
-        if (p.st->panel_kb == 0) return;
-        c_r0 = a_r0 = p.st->panel_r + p.st->panel_kb;
+        const int64_t pr = p.rk ? p.rk[0] : p.st->panel_r, pk = p.rk ? p.rk[1] : p.st->panel_kb;
+        if (pk == 0) return;
+        c_r0 = a_r0 = pr + pk;
     }
     const int64_t row_base = c_r0 + (p.row_tile0 + static_cast<int64_t>(blockIdx.y)) * kTM;
+#ifdef F2_TIMELINE
+    const int tl_slot = p.st ? static_cast<int>((p.aw0 / 16) & 127) : -1;  // panel index (W = 1024)
+    if (tl_slot >= 0 && threadIdx.x == 0 && p.cw1 - p.cw0 > 16) atomicMin(&const_cast<PlsState*>(p.st)->tl[2][tl_slot], gtimer());
+#endif
     if (row_base >= p.c_r1) return;
     // K split (gridDim.z > 1): this CTA takes coefficient words [kw0, kw0 + kwn) and
     // XORs its partial product into C atomically (GF(2) addition is order-free)
@@ -352,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
             }
         }
     }
+#ifdef F2_TIMELINE
+    if (tl_slot >= 0 && threadIdx.x == 0 && p.cw1 - p.cw0 > 16) atomicMax(&const_cast<PlsState*>(p.st)->tl[3][tl_slot], gtimer());
+#endif
 }
 
 static size_t table_apply_smem() { return kSmem; }

@@ -306,4 +306,18 @@ void setup_rref_kernels() {
     cudaFuncSetAttribute(k_rref_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+
+__global__ void k_panel_snapshot(const PlsState* st, int64_t* snap, int panel_bits) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid == 0) {
+        snap[0] = st->panel_r;
+        snap[1] = st->panel_kb;
+    }
+    for (int i = tid; i < panel_bits; i += gridDim.x * blockDim.x) snap[2 + i] = st->brow[i];
+}
+
+void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int panel_bits) {
+    k_panel_snapshot<<<2, 512, 0, s>>>(st, snap, panel_bits);
+}
+
 }  // namespace f2g

@@ -800,6 +800,9 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
     const int nleaves = (width + 63) / 64;
     const int nwp = static_cast<int>(pw1 - pw0);
     unsigned target = 0;
+#ifdef F2_TIMELINE
+    if (threadIdx.x == 0) atomicMin(&st->tl[0][(pw0 / 16) & 127], gtimer());
+#endif
     int kbprev = 0, pkc = 0;  // CTA 0's carry state (uniform across its threads)
     int64_t state = S_FRESH, leaf = 0, wpk = -1, wleaf = 0;
     for (int it = 0;; ++it) {
@@ -896,10 +899,17 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
         if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 0) st->dbg[23] = clock64() - cbar;
         if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 1) st->dbg[24] = clock64() - cbar;
     }
+#ifdef F2_TIMELINE
+    if (threadIdx.x == 0) atomicMax(&st->tl[1][(pw0 / 16) & 127], gtimer());
+#endif
 }
 
 void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
-                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm) {
+                       int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm, bool cooperative) {
+    // Non-cooperative launches (the look-ahead side stream, next to a running Schur
+    // update) rely on every CTA becoming resident eventually: the only other work on
+    // the device is the Schur kernel, whose CTAs never wait, and the grid (<= SMs)
+    // fits one CTA per SM.
     cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nsm));
@@ -908,7 +918,7 @@ void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    attr[0].val.cooperative = cooperative ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_panel_pipe, A, pw0, width, pw1, st, P, Qp, pmap, qcol_off, bar);
