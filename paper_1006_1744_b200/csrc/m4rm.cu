@@ -54,8 +54,8 @@ constexpr int kBuildWarps = F2_BUILD_WARPS;      // warps building each chunk's 
 // shared memory carve-up (bytes)
 constexpr size_t kOffT = 0;                                   // [kTabs][256][kTNW] u64
 constexpr size_t kOffRing = kOffT + kTabs * 256 * kTNW * 8;    // [kStages][8][kTNW]
-constexpr size_t kOffA = kOffRing + kStages * 8 * kTNW * 8;    // [2][kTM] u64          16 KB
-constexpr size_t kOffMap = kOffA + 2 * kTM * 8;                // [kMaxMap] i32         8 KB
+constexpr size_t kOffA = kOffRing + kStages * 8 * kTNW * 8;    // [2][kTM][2] u64       32 KB (K-word pairs)
+constexpr size_t kOffMap = kOffA + 2 * kTM * 8 * 2;            // [kMaxMap] i32         8 KB
 constexpr size_t kOffLive = kOffMap + kMaxMap * 4;             // [kMaxMap/8/32] u32
 constexpr size_t kSmem = kOffLive + (kMaxMap / 8 / 32) * 4;
 
@@ -63,6 +63,10 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool
     const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     const int n = valid ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -166,6 +170,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
             cp_async8(ring + ((c % kStages) * 8 + b) * kTNW + k, src, ok);
         }
     };
+    // coefficient words 2gg, 2gg+1 of every row of the tile -> abuf[gg & 1][row][0..1]:
+    // one 16-byte copy per row (the rows are a stride apart, so every copy is its own
+    // global sector either way; pairs halve the copies)
+    auto issue_a2 = [&](int gg) {
+        const bool al = (aw0_l & 1) == 0;
+        const int rem = kwn - 2 * gg;  // valid words in this pair (>= 1)
+        for (int r = tid; r < kTM; r += kThreads) {
+            const bool ok = r < nrows;
+            uint64_t* dst = abuf + ((gg & 1) * kTM + r) * 2;
+            const uint64_t* src = p.A.w + (arow_base + r) * p.A.stride + aw0_l + 2 * gg;
+            if (al) {
+                cp_async16(dst, ok ? src : p.A.w, ok ? (rem >= 2 ? 16 : 8) : 0);
+            } else {
+                cp_async8(dst, ok ? src : p.A.w, ok);
+                cp_async8(dst + 1, ok && rem >= 2 ? src + 1 : p.A.w, ok && rem >= 2);
+            }
+        }
+    };
     // coefficient word g of every row of the tile -> abuf[g & 1]
     auto issue_a = [&](int g) {
         for (int r = tid; r < kTM; r += kThreads) {
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
             acc1[i] ^= static_cast<uint64_t>(t.z) | (static_cast<uint64_t>(t.w) << 32);
         }
     };
-    issue_a(0);
+    issue_a2(0);
     for (int c = 0; c < 6; c += 2) {  // chunks 0-1, 2-3, 4-5: one group each
         if (c < nch) issue_b(c);
         if (c + 1 < nch) issue_b(c + 1);
@@ -277,18 +299,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         const int c = 2 * pi;
         cp_async_wait<1>();
         __syncthreads();
-        if ((c & 7) == 0 || (c & 7) == 4) {  // coefficient bits of chunks c .. c+3
-            const int g = c >> 3;
-            const uint32_t* ab =
-                reinterpret_cast<const uint32_t*>(abuf + (g & 1) * kTM + warp * 64 + rq) + ((c & 7) >> 2);
+        if ((c & 3) == 0) {  // coefficient bits of chunks c .. c+3
+            const int gg = c >> 4;
+            const uint32_t* ab = reinterpret_cast<const uint32_t*>(abuf + ((gg & 1) * kTM + warp * 64 + rq) * 2) +
+                                 ((c >> 3) & 1) * 2 + ((c >> 2) & 1);
 #pragma unroll
-            for (int i = 0; i < kRPT; ++i) aw[i] = ab[8 * i];
+            for (int i = 0; i < kRPT; ++i) aw[i] = ab[16 * i];
         }
         build_half(c + 2, 0);
         build_half(c + 3, 1);
         if (c + 6 < nch) issue_b(c + 6);
         if (c + 7 < nch) issue_b(c + 7);
-        if ((c & 7) == 0 && (c >> 3) + 1 < kwn && (c >> 3) + 1 < (nch + 7) / 8) issue_a((c >> 3) + 1);
+        if ((c & 15) == 0 && 2 * ((c >> 4) + 1) < kwn && 2 * ((c >> 4) + 1) < (nch + 7) / 8) issue_a2((c >> 4) + 1);
         cp_async_commit();
 #ifndef F2_EXP_NOLOOKUP
         lookups(c, aw);
