@@ -71,7 +71,7 @@ struct Ctx {
     int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
-    int64_t* snap = nullptr;  // [2][2 + kMaxPanelBits]
+    int64_t* snap = nullptr;  // [2][kSnapWords]
     uint64_t* scratch = nullptr;
     size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
@@ -145,7 +145,7 @@ int ensure_init() {
         CK(cudaStreamCreateWithPriority(&g.side, cudaStreamNonBlocking, hi));
         CK(cudaEventCreateWithFlags(&g.la_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.la_join, cudaEventDisableTiming));
-        CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * (2 + kMaxPanelBits)));
+        CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
     }
     CK(cudaGetLastError());
     g.init = true;
@@ -361,15 +361,6 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             ++g.launches;  // save + put
         }
         if (pw1 < nw) {
-            {
-                LaunchTimer t(2, 0, 0);
-                if (!g.fused) {  // the panel kernel leaves the maps behind
-                    launch_panel_lmaps(s, A, pw0, nleaves, g.st);
-                    ++g.launches;
-                }
-                launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
-            }
-            if ((rc = enqueue_download(A, c, W, s))) return rc;
             TableApply ta{};
             ta.C = A;
             ta.c_r1 = m;
@@ -385,14 +376,16 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             ta.row_mode = ROWS_AFTER_PANEL;
             ta.st = g.st;
             const int64_t erows = m - std::min<int64_t>(m, c + cw);  // rows below the pivots at full rank
-            if (la) {
-                // Schur of panel pi on panel pi+1's columns, then panel pi+1's kernel on the
-                // side stream while the Schur covers the columns right of it
-                int64_t* snap = g.snap + (pi & 1) * (2 + kMaxPanelBits);
-                launch_panel_snapshot(s, g.st, snap, nleaves * 64);
-                ta.brow = snap + 2;
-                ta.rk = snap;
+            if (la && nleaves * 64 <= 1024) {
+                // snapshot the finished panel (rows, pivots, solve words), solve panel pi+1's
+                // columns narrow and fast, their Schur update, then panel pi+1's kernel on the
+                // side stream while the main stream solves and updates the columns right of it
+                int64_t* snap = g.snap + (pi & 1) * kSnapWords;
+                launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
                 const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
+                launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
+                ta.brow = snap + kSnapBrow;
+                ta.rk = snap;
                 TableApply t1 = ta;
                 t1.cw1 = npw1;
                 launch_table_apply(s, t1, g.nsm, erows);
@@ -400,6 +393,8 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
                 panel_kernel(g.side, pi + 1, g.side_ctas);
                 CK(cudaEventRecord(g.la_join, g.side));
+                launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
+                if ((rc = enqueue_download(A, c, W, s))) return rc;
                 if (npw1 < nw) {
                     TableApply t2 = ta;
                     t2.cw0 = npw1;
@@ -408,9 +403,40 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 }
                 CK(cudaStreamWaitEvent(s, g.la_join, 0));
             } else {
-                // work is data dependent; filled in from the pivots after the call
-                LaunchTimer t(0, static_cast<double>(pi), -1.0);
-                launch_table_apply(s, ta, g.nsm, erows);
+                {
+                    LaunchTimer t(2, 0, 0);
+                    if (!g.fused) {  // the panel kernel leaves the maps behind
+                        launch_panel_lmaps(s, A, pw0, nleaves, g.st);
+                        ++g.launches;
+                    }
+                    launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
+                }
+                if ((rc = enqueue_download(A, c, W, s))) return rc;
+                if (la) {  // look-ahead without the snapshot TRSM (panels wider than 1024)
+                    int64_t* snap = g.snap + (pi & 1) * kSnapWords;
+                    launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
+                    ta.brow = snap + kSnapBrow;
+                    ta.rk = snap;
+                    const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
+                    TableApply t1 = ta;
+                    t1.cw1 = npw1;
+                    launch_table_apply(s, t1, g.nsm, erows);
+                    CK(cudaEventRecord(g.la_fork, s));
+                    CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
+                    panel_kernel(g.side, pi + 1, g.side_ctas);
+                    CK(cudaEventRecord(g.la_join, g.side));
+                    if (npw1 < nw) {
+                        TableApply t2 = ta;
+                        t2.cw0 = npw1;
+                        t2.bw0 = npw1;
+                        launch_table_apply(s, t2, g.nsm - g.side_ctas, erows, g.side_ctas);
+                    }
+                    CK(cudaStreamWaitEvent(s, g.la_join, 0));
+                } else {
+                    // work is data dependent; filled in from the pivots after the call
+                    LaunchTimer t(0, static_cast<double>(pi), -1.0);
+                    launch_table_apply(s, ta, g.nsm, erows);
+                }
             }
         }
         if (pw1 >= nw && (rc = enqueue_download(A, c, W, s))) return rc;  // last panel: final after the gather

@@ -55,11 +55,30 @@ struct TableApply {
     const PlsState* st;
     int64_t row_tile0;     // first 1024-row tile of this launch (set by launch_table_apply)
     const int64_t* rk;     // ROWS_AFTER_PANEL from a snapshot {panel_r, panel_kb} instead of st (look-ahead)
+    int idle_ctas;         // > 0: grid rows with row_tile0 + y < 0 are placeholders; their first
+    int64_t idle_ns;       // idle_ctas CTAs hold their SM for idle_ns, then exit
 };
 // snapshot of a finished panel's row range and raw-column -> pivot-row map, so its Schur
 // update can run while the next panel's kernel rewrites the state
-void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int panel_bits);
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0);
+// Layout (int64 words): [0] panel_r, [1] panel_kb, brow, q (pivot columns, -1 past kb),
+// bstart (first pivot index of each leaf), and per leaf j and pivot index t >= bstart[j]
+// the solve word M[j][t] = (row t's leaf-j coefficients, masked below its own pivot in
+// leaf j) * L_jj^{-1}, i.e. the combination of leaf j's pivot rows as they are before
+// leaf j's solve step that row t adds (the panel lmap applied once, not per TRSM CTA).
+// Cf words coef_w0 + j of the gathered rows r0 + t hold the coefficients.
+constexpr int64_t kSnapBrow = 2, kSnapQ = kSnapBrow + kMaxPanelBits, kSnapBstart = kSnapQ + kMaxPanelBits,
+                  kSnapM = kSnapBstart + kMaxPanelBits / 64 + 8,
+                  kSnapWords = kSnapM + static_cast<int64_t>(kMaxPanelBits / 64) * kMaxPanelBits;
+void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int nleaves, const Mat& Cf,
+                           int64_t coef_w0);
+// U <- L11^{-1} U on words [tw0, tw1) of the panel's pivot rows, from a snapshot only
+// (the next panel's kernel may be rewriting the state); strip = words per CTA (1 or 8)
+void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, int nleaves, int64_t tw0, int64_t tw1,
+                            int strip);
+// idle_ctas > 0: the first idle_ctas CTAs of the launch hold their SMs for ~15 us and
+// exit, so a high-priority kernel launched next to this one (the look-ahead panel
+// kernel) is placed at once instead of after the first wave of tiles
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0, int idle_ctas = 0);
 void setup_m4rm_kernels();
 
 // misc.cu

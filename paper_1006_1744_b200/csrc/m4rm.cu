@@ -103,6 +103,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         if (pk == 0) return;
         c_r0 = a_r0 = pr + pk;
     }
+    if (p.idle_ctas > 0 && p.row_tile0 + static_cast<int64_t>(blockIdx.y) < 0) {  // placeholder rows: keep
+        if (static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) < p.idle_ctas) {  // the SM until the side kernel is queued
+            const unsigned long long t0 = gtimer();
+            while (gtimer() - t0 < static_cast<unsigned long long>(p.idle_ns)) __nanosleep(1000);
+        }
+        return;
+    }
     const int64_t row_base = c_r0 + (p.row_tile0 + static_cast<int64_t>(blockIdx.y)) * kTM;
 #ifdef F2_TIMELINE
     const int tl_slot = p.st ? static_cast<int>((p.aw0 / 16) & 127) : -1;  // panel index (W = 1024)
@@ -391,7 +398,7 @@ static size_t table_apply_smem() { return kSmem; }
 // across gridDim.z CTAs (atomic XOR into C) so the tail wave is short.  expect_rows
 // (the caller's estimate of the device-side row count; <= 0: unknown) only steers
 // the split; correctness never depends on it.
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows) {
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows, int idle_ctas) {
     if (t.cw1 <= t.cw0 || t.kbits <= 0) return;
     const int64_t lo = t.row_mode == ROWS_STATIC ? t.c_r0 : 0;
     const int64_t rows = t.c_r1 - lo;
@@ -418,12 +425,23 @@ void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t ex
     if (y0 > 0) {
         TableApply a = t;
         a.row_tile0 = 0;
-        k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(y0), 1), kThreads, table_apply_smem(),
-                        s>>>(a);
+        a.idle_ctas = 0;
+        static const int64_t idle_ns = [] {
+            const char* e = std::getenv("F2_IDLE_NS");
+            return e ? std::atoll(e) : 15000ll;
+        }();
+        if (idle_ctas > 0 && idle_ns > 0) {  // extra leading grid rows of placeholders
+            a.row_tile0 = -((idle_ctas + nct - 1) / nct);
+            a.idle_ctas = idle_ctas;
+            a.idle_ns = idle_ns;
+        }
+        k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(y0 - a.row_tile0), 1), kThreads,
+                        table_apply_smem(), s>>>(a);
     }
     if (y0 < nrt) {
         TableApply b = t;
         b.row_tile0 = y0;
+        b.idle_ctas = 0;
         k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(nrt - y0), static_cast<unsigned>(splitk)),
                         kThreads, table_apply_smem(), s>>>(b);
     }

@@ -19,8 +19,13 @@ out = (C.c_ulonglong * 512)()
 L.f2_debug_timeline(out, 512)
 v = [list(out[i * 128:(i + 1) * 128]) for i in range(4)]
 t0 = v[0][0]
-print(f"total {ms:.2f} ms")
-for p in [0, 1, 40, 41, 56, 57, 58, 59, 60, 61, 62, 63]:
-    ps, pe, ss, se = v[0][p], v[1][p], v[2][p], v[3][p]
-    f = lambda x: (x - t0) / 1000 if 0 < x < (1 << 63) else float('nan')
-    print(f"panel {p:2d}: kernel {f(ps):9.1f} .. {f(pe):9.1f} ({(pe - ps) / 1000:6.1f})   schur {f(ss):9.1f} .. {f(se):9.1f}")
+f = lambda x: (x - t0) / 1000 if 0 < x < (1 << 63) else float('nan')
+print(f"total {ms:.2f} ms; engine span {f(max(v[1][:64])):.1f} us")
+tot_t2 = tot_k = tot_gap = 0.0
+for p in range(63):
+    ks, ke = f(v[0][p + 1]), f(v[1][p + 1])
+    ss, se = f(v[2][p]), f(v[3][p])
+    nxt = f(v[2][p + 1]) if p + 1 < 62 else f(v[0][p + 2]) if p + 2 < 64 else float('nan')
+    gap = (nxt - max(se, ke)) if nxt == nxt and se == se else float('nan')
+    if p % 6 == 0 or p > 56:
+        print(f"panel {p:2d}: schur t2 {ss:9.1f}..{se:9.1f} ({se - ss:6.1f})  kernel(p+1) {ks:9.1f}..{ke:9.1f} ({ke - ks:6.1f})  next-start gap {gap:6.1f}")
