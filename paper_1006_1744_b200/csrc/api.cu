@@ -72,6 +72,12 @@ struct Ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
     int64_t* snap = nullptr;  // [2][kSnapWords]
+    // tensor-core Schur of the look-ahead path (F2_SCHUR_M4RM=1: the SMEM table kernel)
+    bool f4 = true;
+    uint8_t* f4_ax = nullptr;
+    uint8_t* f4_bx = nullptr;
+    unsigned* f4_claim = nullptr;
+    size_t cap_f4a = 0, cap_f4b = 0;
     uint64_t* scratch = nullptr;
     size_t cap_m = 0, cap_q = 0, cap_scratch = 0;
     int64_t* h_r = nullptr;  // pinned ring of r snapshots (early exit)
@@ -128,6 +134,8 @@ int ensure_init() {
     setup_leafupd_kernels();
     setup_trsm_kernels();
     setup_m4rm_kernels();
+    setup_schur_f4_kernels();
+    if (std::getenv("F2_SCHUR_M4RM")) g.f4 = false;
     setup_misc_kernels();
     setup_rref_kernels();
     setup_panel_kernels();
@@ -177,6 +185,26 @@ int ensure_workspace(size_t m, size_t nq, size_t npanels, size_t scratch_words) 
         CK(cudaMallocHost(&g.h_r, sizeof(int64_t) * npanels));
         g.h_r_cap = npanels;
     }
+    return F2_OK;
+}
+
+// expanded operands of the tensor-core Schur: A for every row, B for the trailing
+// columns plus the next panel's (t1 and t2 of one panel use disjoint regions)
+int ensure_f4(size_t m, size_t nw) {
+    const size_t a = schur_f4_a_bytes(static_cast<int64_t>(m));
+    const size_t b = schur_f4_b_bytes(static_cast<int64_t>(nw)) + schur_f4_b_bytes(kMaxPanelBits / 64);
+    if (a > g.cap_f4a || b > g.cap_f4b) ++g_ws_gen;
+    if (a > g.cap_f4a) {
+        if (g.f4_ax) cudaFree(g.f4_ax);
+        CK(cudaMalloc(&g.f4_ax, a));
+        g.cap_f4a = a;
+    }
+    if (b > g.cap_f4b) {
+        if (g.f4_bx) cudaFree(g.f4_bx);
+        CK(cudaMalloc(&g.f4_bx, b));
+        g.cap_f4b = b;
+    }
+    if (!g.f4_claim) CK(cudaMalloc(&g.f4_claim, 4 * sizeof(unsigned)));
     return F2_OK;
 }
 
@@ -386,9 +414,15 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
                 ta.brow = snap + kSnapBrow;
                 ta.rk = snap;
-                TableApply t1 = ta;
-                t1.cw1 = npw1;
-                launch_table_apply(s, t1, g.nsm, erows);
+                const bool f4 = g.f4 && g.f4_ax;
+                if (f4) {
+                    launch_schur_f4_expand_a(s, A, pw0, cw, snap, g.f4_ax, g.nsm);
+                    launch_schur_f4(s, A, pw1, npw1, snap, snap + kSnapBrow, cw, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+                } else {
+                    TableApply t1 = ta;
+                    t1.cw1 = npw1;
+                    launch_table_apply(s, t1, g.nsm, erows);
+                }
                 CK(cudaEventRecord(g.la_fork, s));
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
                 panel_kernel(g.side, pi + 1, g.side_ctas);
@@ -396,10 +430,15 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
                 if (npw1 < nw) {
-                    TableApply t2 = ta;
-                    t2.cw0 = npw1;
-                    t2.bw0 = npw1;
-                    launch_table_apply(s, t2, g.nsm - g.side_ctas, erows);
+                    if (f4) {
+                        launch_schur_f4(s, A, npw1, nw, snap, snap + kSnapBrow, cw, g.f4_ax,
+                                        g.f4_bx + schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + 1, g.nsm);
+                    } else {
+                        TableApply t2 = ta;
+                        t2.cw0 = npw1;
+                        t2.bw0 = npw1;
+                        launch_table_apply(s, t2, g.nsm - g.side_ctas, erows);
+                    }
                 }
                 CK(cudaStreamWaitEvent(s, g.la_join, 0));
             } else {
@@ -490,6 +529,7 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
                               static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
     if (rc) return rc;
+    if (g.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw)))) return rc;
     cudaStream_t s = g.stream;
     const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && !std::getenv("F2_NO_GRAPH");
     if (use_graph) {

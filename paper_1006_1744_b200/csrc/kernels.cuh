@@ -81,6 +81,17 @@ void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, i
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0, int idle_ctas = 0);
 void setup_m4rm_kernels();
 
+// schur_f4.cu -- the look-ahead Schur update C ^= L21 * U12 (K <= 1024 raw columns)
+// on the tensor cores (tcgen05 kind::mxf4, parity of exact fp32 counts).  Rows from
+// rk[0] + rk[1] to C.m; Ax/Bx: expanded operands, claim: a zeroed work counter.
+size_t schur_f4_a_bytes(int64_t rows);
+size_t schur_f4_b_bytes(int64_t words);
+void launch_schur_f4_expand_a(cudaStream_t s, const Mat& A, int64_t aw0, int64_t kbits, const int64_t* rk, uint8_t* Ax,
+                              int nsm);
+void launch_schur_f4(cudaStream_t s, const Mat& C, int64_t cw0, int64_t cw1, const int64_t* rk, const int64_t* brow,
+                     int64_t kbits, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm);
+void setup_schur_f4_kernels();
+
 // misc.cu
 void launch_randomize(cudaStream_t s, const Mat& A, uint64_t threshold, uint64_t seed);
 void launch_digest(cudaStream_t s, const Mat& A, unsigned long long* out);
