@@ -325,6 +325,23 @@ int enqueue_download(const Mat& A, int64_t c, unsigned W, cudaStream_t s) {
     return F2_OK;
 }
 
+// The Schur update of one panel as a tensor-core job: rows below the panel's pivots
+// (rk = {panel_r, panel_kb} on the device), coefficient bits = the panel's L columns,
+// B rows = the pivot rows through the raw-column map, columns [cw0, cw1).
+F4Job pls_f4_job(const Mat& A, int64_t pw0, int64_t kbits, int64_t cw0, int64_t cw1, const int64_t* rk,
+                 const int64_t* brow) {
+    F4Job j{};
+    j.C = j.A = j.B = A;
+    j.cw0 = j.bw0 = cw0;
+    j.cw1 = cw1;
+    j.aw0 = pw0;
+    j.brow = brow;
+    j.rk = rk;
+    j.rows_end = A.m;
+    j.kbits = kbits;
+    return j;
+}
+
 // One right-looking PLS pass, enqueued on `s`.  poll = snapshot r after every panel
 // and stop enqueueing once every row is a pivot (not usable inside a graph capture).
 int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
@@ -414,10 +431,11 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
                 ta.brow = snap + kSnapBrow;
                 ta.rk = snap;
-                const bool f4 = g.f4 && g.f4_ax;
+                const bool f4 = g.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
+                const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
                 if (f4) {
-                    launch_schur_f4_expand_a(s, A, pw0, cw, snap, g.f4_ax, g.nsm);
-                    launch_schur_f4(s, A, pw1, npw1, snap, snap + kSnapBrow, cw, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+                    launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
+                    launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
                 } else {
                     TableApply t1 = ta;
                     t1.cw1 = npw1;
@@ -431,8 +449,15 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
                 if (npw1 < nw) {
                     if (f4) {
-                        launch_schur_f4(s, A, npw1, nw, snap, snap + kSnapBrow, cw, g.f4_ax,
-                                        g.f4_bx + schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + 1, g.nsm);
+                        unsigned long long* tl = nullptr;
+#ifdef F2_TIMELINE
+                        tl = &g.st->tl[2][pi & 127];
+#endif
+                        F4Job fw = fj;
+                        fw.cw0 = fw.bw0 = npw1;
+                        fw.cw1 = nw;
+                        launch_schur_f4(s, fw, g.f4_ax, g.f4_bx + schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + 1,
+                                        g.nsm, tl);
                     } else {
                         TableApply t2 = ta;
                         t2.cw0 = npw1;
@@ -474,7 +499,13 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 } else {
                     // work is data dependent; filled in from the pivots after the call
                     LaunchTimer t(0, static_cast<double>(pi), -1.0);
-                    launch_table_apply(s, ta, g.nsm, erows);
+                    if (g.f4 && g.f4_ax && cw >= 256 && cw <= 1024) {  // panel_r, panel_kb are adjacent
+                        const F4Job fj = pls_f4_job(A, pw0, cw, pw1, nw, &g.st->panel_r, g.st->brow);
+                        launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
+                        launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+                    } else {
+                        launch_table_apply(s, ta, g.nsm, erows);
+                    }
                 }
             }
         }
@@ -1092,6 +1123,29 @@ void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0
     const double abytes = 8.0 * static_cast<double>((s + 63) / 64);
     LaunchTimer t(0, static_cast<double>(p) * (2.0 * cbytes + abytes) + static_cast<double>(s) * cbytes,
                   2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
+    // tensor cores once the product is deep and wide enough to fill 128 x 256 x 1024 tiles
+    // (F2_SCHUR_M4RM=1 keeps the SMEM table kernel); K is cut into chunks of <= 1024
+    if (g.f4 && s >= 256 && p >= 128 && q >= 256 && ensure_f4(static_cast<size_t>(p), static_cast<size_t>(ta.cw1 - cw0)) == F2_OK) {
+        for (int64_t k0 = 0; k0 < s; k0 += kF4MaxK) {
+            F4Job j{};
+            j.C = C;
+            j.c_r0 = cr0;
+            j.cw0 = cw0;
+            j.cw1 = ta.cw1;
+            j.A = A;
+            j.a_r0 = ar0;
+            j.aw0 = aw0 + k0 / 64;
+            j.B = B;
+            j.b_r0 = br0 + k0;
+            j.bw0 = bw0;
+            j.rows_end = p;
+            j.kbits = std::min<int64_t>(kF4MaxK, s - k0);
+            launch_schur_f4_expand_a(g.stream, j, g.f4_ax, g.nsm);
+            launch_schur_f4(g.stream, j, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+            g.launches += 3;
+        }
+        return;
+    }
     launch_table_apply(g.stream, ta, g.nsm, p);
 }
 

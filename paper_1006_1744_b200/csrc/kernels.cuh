@@ -81,15 +81,31 @@ void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, i
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0, int idle_ctas = 0);
 void setup_m4rm_kernels();
 
-// schur_f4.cu -- the look-ahead Schur update C ^= L21 * U12 (K <= 1024 raw columns)
-// on the tensor cores (tcgen05 kind::mxf4, parity of exact fp32 counts).  Rows from
-// rk[0] + rk[1] to C.m; Ax/Bx: expanded operands, claim: a zeroed work counter.
+// schur_f4.cu -- C ^= A * B over GF(2) with K <= 1024 on the tensor cores (tcgen05
+// kind::mxf4, parity of exact fp32 counts): the Schur update of pls_recursive and the
+// GEMM of addmul/mul_m4rm/TRSM.  Rows are shifted by d = rk ? rk[0] + rk[1] : 0 (a
+// device-side pivot count, so PLS launches need no host sync): C row c_r0 + d + i,
+// A row a_r0 + d + i, i < rows_end - d.  B row j is brow ? brow[j] : b_r0 + j (brow
+// < 0: zero row); C word cw0 + x pairs with B word bw0 + x.
+struct F4Job {
+    Mat C;
+    int64_t c_r0, cw0, cw1;
+    Mat A;
+    int64_t a_r0, aw0;
+    Mat B;
+    int64_t b_r0, bw0;
+    const int64_t* brow;
+    const int64_t* rk;
+    int64_t rows_end;
+    int64_t kbits;
+};
+constexpr int64_t kF4MaxK = 1024;
 size_t schur_f4_a_bytes(int64_t rows);
 size_t schur_f4_b_bytes(int64_t words);
-void launch_schur_f4_expand_a(cudaStream_t s, const Mat& A, int64_t aw0, int64_t kbits, const int64_t* rk, uint8_t* Ax,
-                              int nsm);
-void launch_schur_f4(cudaStream_t s, const Mat& C, int64_t cw0, int64_t cw1, const int64_t* rk, const int64_t* brow,
-                     int64_t kbits, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm);
+void launch_schur_f4_expand_a(cudaStream_t s, const F4Job& jb, uint8_t* Ax, int nsm);
+// Ax: A expanded by launch_schur_f4_expand_a; Bx: scratch; claim: a work counter
+void launch_schur_f4(cudaStream_t s, const F4Job& jb, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm,
+                     unsigned long long* tl = nullptr);
 void setup_schur_f4_kernels();
 
 // misc.cu

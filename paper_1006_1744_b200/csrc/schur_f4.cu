@@ -5,7 +5,7 @@
 // integer count: a set bit becomes the E2M1 value 1.0 (nibble 0x2), a block-scaled
 // tcgen05.mma kind::mxf4 (all UE8M0 scales 2^0) accumulates the exact AND-count of
 // each C entry in fp32 (<= K = 1024 < 2^24), and the count's parity is the GF(2)
-// sum.  The accumulator starts at 2^23, so the parity is bit 0 of the fp32 word.
+// sum: bit 0 of the fp32 word of count + 2^23.
 //
 // Data flow per panel (all device-side, inside the PLS graph):
 //   k_f4_expand_a: the coefficient bits of every row below the panel's pivots (A =
@@ -21,9 +21,10 @@
 //     (cp.async.bulk + mbarrier transaction counts), one thread of warp 0 issues 4
 //     MMAs of 128x256x64 per stage into a 256-column TMEM accumulator, and 16
 //     epilogue warps (4 per TMEM lane quarter, 64 columns each) read the counts,
-//     re-arm the accumulator with 2^23, release it, pack 64 parities into a word by
-//     funnel shifts and XOR it into C.  Tiles and the chunk queue are data dependent
-//     (the row count comes from the panel snapshot), so no host sync is needed.
+//     release the accumulator (the next tile's first MMA overwrites it), pack 64
+//     parities into a word by funnel shifts and XOR it into C.  Tiles and the chunk
+//     queue are data dependent (the row count comes from the panel snapshot), so no
+//     host sync is needed.
 #include <cstdint>
 #include <cstdlib>
 
@@ -34,19 +35,20 @@ namespace f2g {
 
 namespace {
 
-constexpr int kFM = 128, kFN = 256, kFKS = 256;   // tile rows / cols, K elements per stage
+constexpr int kFM = 128, kFN = 224, kFKS = 256;   // tile rows / cols (7 half-words), K elements per stage
+constexpr int kFHW = kFN / 32;                    // 32-bit column groups per tile
 constexpr int kFAStage = kFM * kFKS / 2;          // 16 KB of nibbles
-constexpr int kFBStage = kFN * kFKS / 2;          // 32 KB
+constexpr int kFBStage = kFN * kFKS / 2;          // 28 KB
 constexpr int kFMaxStages = 4;                    // K <= 1024
-constexpr int kFRing = 4;                         // A stages in flight
+constexpr int kFRingMax = 6;                      // A stages in flight (template RING <= this)
 constexpr int kFChunk = 16;                       // tiles per claimed chunk
 constexpr int kFQ = 8;                            // chunk-id broadcast ring
-constexpr int kFThreads = 640;                    // warp 0 MMA, warp 1 loads, warps 4..19 epilogue
-constexpr int kFEpiWarps = 16;
-constexpr uint32_t kFSfCol = 256;                 // TMEM columns 256..319: scale factors (all 0x7F)
+// threads: warp 0 MMA, warp 1 loads, warps 2-3 idle, 4 * EPW epilogue warps from warp 4
+constexpr int f4_threads(int epw) { return 128 + 128 * epw; }
+constexpr uint32_t kFSfCol = 2 * kFN;             // TMEM: accumulators 0..447 (two tiles), scale factors 448..511
 constexpr uint32_t kFIdesc = (1u << 7) | (1u << 10) | (1u << 23) | (static_cast<uint32_t>(kFN >> 3) << 17) |
-                             (static_cast<uint32_t>(kFM >> 4) << 24);  // E2M1 x E2M1, UE8M0, K-major, 128x256
-constexpr size_t kFSmem = static_cast<size_t>(kFMaxStages) * kFBStage + static_cast<size_t>(kFRing) * kFAStage;
+                             (static_cast<uint32_t>(kFM >> 4) << 24);  // E2M1 x E2M1, UE8M0, K-major, 128x224
+constexpr size_t f4_smem(int ring) { return static_cast<size_t>(kFMaxStages) * kFBStage + static_cast<size_t>(ring) * kFAStage; }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -114,14 +116,16 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t v, int lane) {
 
 }  // namespace
 
-// A = coefficient bits [aw0*64, aw0*64 + kbits) of rows r0 + i, r0 = rk[0] + rk[1]
-__global__ void __launch_bounds__(256) k_f4_expand_a(Mat A, int64_t aw0, int64_t kbits, const int64_t* rk, int64_t m,
-                                                     uint8_t* __restrict__ Ax, int nst) {
-    const int64_t r0 = rk[0] + rk[1];
-    const int64_t rows = m - r0;
+__device__ __forceinline__ int64_t f4_row_shift(const F4Job& jb) { return jb.rk ? jb.rk[0] + jb.rk[1] : 0; }
+
+// A = coefficient bits [aw0*64, aw0*64 + kbits) of rows a_r0 + d + i
+__global__ void __launch_bounds__(256) k_f4_expand_a(F4Job jb, uint8_t* __restrict__ Ax, int nst) {
+    const int64_t d = f4_row_shift(jb);
+    const int64_t rows = jb.rows_end - d;
     if (rows <= 0) return;
     const int64_t nrt = (rows + kFM - 1) / kFM;
     const int64_t total = nrt * nst * 1024;  // 16-byte output chunks
+    const uint64_t* abase = jb.A.w + (jb.a_r0 + d) * jb.A.stride + jb.aw0;
     for (int64_t idx = blockIdx.x * 256ll + threadIdx.x; idx < total; idx += static_cast<int64_t>(gridDim.x) * 256) {
         const int r8 = static_cast<int>(idx & 7), kc = static_cast<int>((idx >> 3) & 7), rg = static_cast<int>((idx >> 6) & 15);
         const int64_t blk = idx >> 10;
@@ -130,59 +134,97 @@ __global__ void __launch_bounds__(256) k_f4_expand_a(Mat A, int64_t aw0, int64_t
         const int64_t row = rt * kFM + rg * 8 + r8;
         const int64_t j0 = static_cast<int64_t>(s) * kFKS + kc * 32;
         uint32_t x = 0;
-        if (row < rows && j0 < kbits) {
-            x = reinterpret_cast<const uint32_t*>(A.w + (r0 + row) * A.stride + aw0)[j0 >> 5];
-            if (kbits - j0 < 32) x &= (1u << (kbits - j0)) - 1u;
+        if (row < rows && j0 < jb.kbits) {
+            x = reinterpret_cast<const uint32_t*>(abase + row * jb.A.stride)[j0 >> 5];
+            if (jb.kbits - j0 < 32) x &= (1u << (jb.kbits - j0)) - 1u;
         }
         reinterpret_cast<uint4*>(Ax)[idx] = spread32(x);  // offset = ((rt*nst + s) * 1024 + rg*64 + kc*8 + r8) * 16
     }
 }
 
-// B^T: element (n, j) = bit (n) of pivot row brow[j] over words [cw0, cw1) of U
-__global__ void __launch_bounds__(256) k_f4_expand_b(Mat U, const int64_t* __restrict__ brow, int64_t kbits, int64_t cw0,
-                                                     int64_t cw1, uint8_t* __restrict__ Bx, int nst) {
+// B^T: element (n, j) = bit n of B row (brow ? brow[j] : b_r0 + j), columns from 32-bit
+// half-word 2*bw0 on; a tile is kFHW half-words of C starting at 2*cw0 + ct*kFHW
+__global__ void __launch_bounds__(256) k_f4_expand_b(F4Job jb, uint8_t* __restrict__ Bx, int nst) {
     const int lane = threadIdx.x & 31;
-    const int64_t nct = (cw1 - cw0 + 3) / 4;
-    const int64_t tasks = nct * nst * 8 * 4;  // (tile, stage, 32-K block, 64-column word)
+    const int64_t nhw = 2 * (jb.cw1 - jb.cw0);
+    const int64_t nct = (nhw + kFHW - 1) / kFHW;
+    const int64_t tasks = nct * nst * 8 * kFHW;  // (tile, stage, 32-K block, half-word)
     for (int64_t w = (blockIdx.x * 256ll + threadIdx.x) >> 5; w < tasks; w += (static_cast<int64_t>(gridDim.x) * 256) >> 5) {
-        const int wd = static_cast<int>(w & 3), kq = static_cast<int>((w >> 2) & 7);
-        const int64_t blk = w >> 5;
+        const int hw = static_cast<int>(w % kFHW);
+        const int64_t rest = w / kFHW;
+        const int kq = static_cast<int>(rest & 7);
+        const int64_t blk = rest >> 3;
         const int s = static_cast<int>(blk % nst);
         const int64_t ct = blk / nst;
         const int64_t j = static_cast<int64_t>(s) * kFKS + kq * 32 + lane;
-        const int64_t word = cw0 + ct * 4 + wd;
-        uint64_t v = 0;
-        if (j < kbits && word < cw1) {
-            const int64_t br = brow[j];
-            if (br >= 0) v = U.w[br * U.stride + word];
+        const int64_t x = ct * kFHW + hw;  // half-word within the column range
+        uint32_t v = 0;
+        if (j < jb.kbits && x < nhw) {
+            const int64_t br = jb.brow ? jb.brow[j] : jb.b_r0 + j;
+            if (br >= 0) v = reinterpret_cast<const uint32_t*>(jb.B.w + br * jb.B.stride + jb.bw0)[x];
         }
-        uint8_t* base = Bx + (ct * nst + s) * kFBStage + kq * 128;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t t = transpose32(static_cast<uint32_t>(v >> (32 * h)), lane);
-            const int n = wd * 64 + h * 32 + lane;  // column within the tile
-            *reinterpret_cast<uint4*>(base + (n >> 3) * 1024 + (n & 7) * 16) = spread32(t);
-        }
+        const uint32_t t = transpose32(v, lane);
+        const int n = hw * 32 + lane;  // column within the tile
+        *reinterpret_cast<uint4*>(Bx + (ct * nst + s) * kFBStage + kq * 128 + (n >> 3) * 1024 + (n & 7) * 16) = spread32(t);
     }
 }
 
-__global__ void __launch_bounds__(kFThreads, 1)
-k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int64_t m, const uint8_t* __restrict__ Ax,
-           const uint8_t* __restrict__ Bx, int nst, unsigned* __restrict__ claim) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* sB = smem;                               // [nst][32 KB]
-    uint8_t* sA = smem + kFMaxStages * kFBStage;      // ring [kFRing][16 KB]
-    __shared__ __align__(8) uint64_t a_full[kFRing], a_empty[kFRing], b_full[kFMaxStages], b_empty[kFMaxStages];
-    __shared__ __align__(8) uint64_t acc_full, acc_empty, q_full[kFQ], q_empty[kFQ];
+// One elected lane of a converged warp issues; the rest of the warp runs the same
+// uniform loop (operands stay in uniform registers, no per-MMA lane waterfall).
+__device__ __forceinline__ void f4_mma(uint32_t d, uint64_t da, uint64_t db, uint32_t sfa, uint32_t sfb, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %6, [%3], [%4], p;\n\t}\n" ::"r"(d),
+        "l"(da), "l"(db), "r"(sfa), "r"(sfb), "r"(accum), "n"(kFIdesc));
+}
+__device__ __forceinline__ void f4_commit(uint64_t* b) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(su32(b))
+        : "memory");
+}
+
+// Tile walk shared by the three roles: chunk ch covers tiles [16 ch, 16 ch + 16) of the
+// column-major tile order (row tile fastest), so consecutive tiles share the B tile.
+struct F4Walk {
+    int rt, ct, n;  // current tile, tiles left in the chunk
+    __device__ __forceinline__ F4Walk(int64_t ch, int nrt, int64_t T) {
+        const int64_t t = ch * kFChunk;
+        ct = static_cast<int>(t / nrt);
+        rt = static_cast<int>(t - static_cast<int64_t>(ct) * nrt);
+        n = static_cast<int>(T - t < kFChunk ? T - t : kFChunk);
+    }
+    __device__ __forceinline__ void next(int nrt) {
+        if (++rt == nrt) {
+            rt = 0;
+            ++ct;
+        }
+    }
+};
+
+// dbg (experiments only): bit 0 skips the C update, bit 2 the A stage copies, bit 3 the MMAs
+template <int kFRing, int EPW>
+__global__ void __launch_bounds__(f4_threads(EPW), 1)
+k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
+           unsigned long long* tl, int dbg) {
+    constexpr int NST = kFMaxStages;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sB = smem;                        // [NST][28 KB], the whole K of one column tile
+    uint8_t* sA = smem + NST * kFBStage;       // ring [kFRing][16 KB] of A stages
+    __shared__ __align__(8) uint64_t a_full[kFRing], a_empty[kFRing], b_full[NST], b_empty[NST];
+    __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2], q_full[kFQ], q_empty[kFQ];
     __shared__ int64_t q_chunk[kFQ];
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t r0 = rk[0] + rk[1];
-    const int64_t rows = m - r0;
+    const int64_t d = f4_row_shift(jb);
+    const int64_t rows = jb.rows_end - d;
+    const int64_t cw0 = jb.cw0, cw1 = jb.cw1;
     if (rows <= 0 || cw1 <= cw0) return;
-    const int64_t nrt = (rows + kFM - 1) / kFM, nct = (cw1 - cw0 + 3) / 4;
-    const int64_t T = nrt * nct;
+    if (tl && tid == 0) atomicMin(tl, gtimer());  // F2_TIMELINE builds: [start, end] of the launch
+    const int64_t nhw = 2 * (cw1 - cw0);
+    const int nrt = static_cast<int>((rows + kFM - 1) / kFM), nct = static_cast<int>((nhw + kFHW - 1) / kFHW);
+    const int64_t T = static_cast<int64_t>(nrt) * nct;
     const int64_t nchunks = (T + kFChunk - 1) / kFChunk;
 
     if (warp == 0) {
@@ -194,15 +236,17 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
             mb_init(&a_full[i], 1);
             mb_init(&a_empty[i], 1);
         }
-        for (int i = 0; i < kFMaxStages; ++i) {
+        for (int i = 0; i < NST; ++i) {
             mb_init(&b_full[i], 1);
             mb_init(&b_empty[i], 1);
         }
-        mb_init(&acc_full, 1);
-        mb_init(&acc_empty, kFEpiWarps);
+        for (int i = 0; i < 2; ++i) {
+            mb_init(&acc_full[i], 1);
+            mb_init(&acc_empty[i], 4 * EPW);
+        }
         for (int i = 0; i < kFQ; ++i) {
             mb_init(&q_full[i], 1);
-            mb_init(&q_empty[i], 1 + kFEpiWarps);
+            mb_init(&q_empty[i], 1 + 4 * EPW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -212,8 +256,9 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
     const uint32_t tbase = tmem_base;
 
     if (warp == 1) {
-        if (lane == 0) {  // ---------------- loads + chunk claims ----------------
-            int64_t cur_ct = -1, u = 0, tiles = 0, bu = 0;
+        if (lane == 0) {  // ---------------- chunk claims + bulk copies ----------------
+            int cur_ct = -1;
+            uint32_t u = 0, tiles = 0;  // A stages issued, tiles walked
             for (int64_t qi = 0;; ++qi) {
                 const int slot = static_cast<int>(qi % kFQ);
                 if (qi >= kFQ) mb_wait(&q_empty[slot], static_cast<uint32_t>((qi / kFQ - 1) & 1));
@@ -221,94 +266,42 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
                 q_chunk[slot] = ch < nchunks ? ch : -1;
                 mb_arrive(&q_full[slot]);  // release: the consumers read q_chunk after the wait
                 if (ch >= nchunks) break;
-                const int64_t t1 = (ch + 1) * kFChunk < T ? (ch + 1) * kFChunk : T;
-                for (int64_t t = ch * kFChunk; t < t1; ++t, ++tiles) {
-                    const int64_t ct = t / nrt, rt = t % nrt;
-                    if (ct != cur_ct) {  // new B tile, stage by stage behind the MMAs of the old one
-                        for (int s = 0; s < nst; ++s) {
-                            if (tiles > 0) mb_wait(&b_empty[s], static_cast<uint32_t>((tiles - 1) & 1));
+                for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+                    if (w.ct != cur_ct) {  // new B tile, stage by stage behind the last MMAs on the old one
+                        for (int s = 0; s < NST; ++s) {
+                            // b_empty[s] completes one phase per tile: wait for the previous tile's
+                            // (the current tile cannot have started: its B is not loaded yet)
+                            if (tiles > 0) mb_wait(&b_empty[s], (tiles - 1) & 1);
                             mb_expect_tx(&b_full[s], kFBStage);
-                            bulk_g2s(sB + s * kFBStage, Bx + (ct * nst + s) * kFBStage, kFBStage, &b_full[s]);
+                            bulk_g2s(sB + s * kFBStage, Bx + (static_cast<int64_t>(w.ct) * NST + s) * kFBStage, kFBStage,
+                                     &b_full[s]);
                         }
-                        cur_ct = ct;
-                        ++bu;
+                        cur_ct = w.ct;
                     }
-                    for (int s = 0; s < nst; ++s, ++u) {
-                        const int sl = static_cast<int>(u % kFRing);
-                        const int64_t f = u / kFRing;
-                        if (f > 0) mb_wait(&a_empty[sl], static_cast<uint32_t>((f - 1) & 1));
+                    for (int s = 0; s < NST; ++s, ++u) {
+                        const uint32_t sl = u % kFRing, f = u / kFRing;
+                        if (f > 0) mb_wait(&a_empty[sl], (f - 1) & 1);
+                        if (dbg & 4) {
+                            mb_arrive(&a_full[sl]);
+                            continue;
+                        }
                         mb_expect_tx(&a_full[sl], kFAStage);
-                        bulk_g2s(sA + sl * kFAStage, Ax + (rt * nst + s) * kFAStage, kFAStage, &a_full[sl]);
+                        bulk_g2s(sA + sl * kFAStage, Ax + (static_cast<int64_t>(w.rt) * NST + s) * kFAStage, kFAStage,
+                                 &a_full[sl]);
                     }
                 }
             }
-            (void)bu;
         }
-    } else if (warp == 0) {
-        if (lane == 0) {  // ---------------- MMA issue ----------------
-            int64_t cur_ct = -1, u = 0, tiles = 0, bu = 0;
-            for (int64_t qi = 0;; ++qi) {
-                const int slot = static_cast<int>(qi % kFQ);
-                mb_wait(&q_full[slot], static_cast<uint32_t>((qi / kFQ) & 1));
-                const int64_t ch = q_chunk[slot];
-                mb_arrive(&q_empty[slot]);
-                if (ch < 0) break;
-                const int64_t t1 = (ch + 1) * kFChunk < T ? (ch + 1) * kFChunk : T;
-                for (int64_t t = ch * kFChunk; t < t1; ++t, ++tiles) {
-                    const int64_t ct = t / nrt;
-                    const bool newb = ct != cur_ct;
-                    if (newb) {
-                        cur_ct = ct;
-                        ++bu;
-                    }
-                    mb_wait(&acc_empty, static_cast<uint32_t>(tiles & 1));
-                    tc_after();
-                    for (int s = 0; s < nst; ++s, ++u) {
-                        if (newb) mb_wait(&b_full[s], static_cast<uint32_t>((bu - 1) & 1));
-                        const int sl = static_cast<int>(u % kFRing);
-                        mb_wait(&a_full[sl], static_cast<uint32_t>((u / kFRing) & 1));
-                        tc_after();
-                        const uint32_t a = su32(sA + sl * kFAStage), b = su32(sB + s * kFBStage);
+    } else if (warp == 0) {  // ---------------- MMA issue (whole warp, one elected lane) ----------------
+        // descriptor bases: a K step of 64 elements is 2 core matrices = 256 B = 16 in the address field
+        uint64_t da0[kFRing], db0[NST];
 #pragma unroll
-                        for (int j = 0; j < kFKS / 64; ++j) {
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-                                "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], "
-                                "p;\n\t}\n" ::"r"(tbase),
-                                "l"(f4_desc(a + j * 256)), "l"(f4_desc(b + j * 256)), "r"(kFIdesc), "r"(tbase + kFSfCol),
-                                "r"(tbase + kFSfCol + 32));
-                        }
-                        mma_commit(&a_empty[sl]);  // A stage free once these MMAs are done
-                        mma_commit(&b_empty[s]);   // (phase per tile) B stage s reusable
-                    }
-                    mma_commit(&acc_full);
-                }
-            }
-        }
-    } else if (warp >= 4) {  // ---------------- epilogue ----------------
-        const int q = warp & 3, h = (warp - 4) >> 2;
-        const uint32_t tl = tbase + (static_cast<uint32_t>(q * 32) << 16);
-        const uint32_t bias = 0x4B000000u;  // 2^23
-        if (h == 0) {  // scale factors: every byte 0x7F = 2^0
-            const uint32_t v = 0x7F7F7F7Fu;
-            for (int c = 0; c < 64; c += 8)
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(tl + kFSfCol + c),
-                             "r"(v));
-        }
-        auto arm = [&]() {  // accumulator columns of this warp := 2^23
+        for (int i = 0; i < kFRing; ++i) da0[i] = f4_desc(su32(sA + i * kFAStage));
 #pragma unroll
-            for (int c = 0; c < 64; c += 16)
-                asm volatile(
-                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
-                        tl + h * 64 + c),
-                    "r"(bias));
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-            tc_before();
-            __syncwarp();
-            if (lane == 0) mb_arrive(&acc_empty);
-        };
-        arm();
-        int64_t tiles = 0;
+        for (int i = 0; i < NST; ++i) db0[i] = f4_desc(su32(sB + i * kFBStage));
+        const uint32_t sfa = tbase + kFSfCol, sfb = tbase + kFSfCol + 32;
+        int cur_ct = -1;
+        uint32_t u = 0, tiles = 0, bu = 0;
         for (int64_t qi = 0;; ++qi) {
             const int slot = static_cast<int>(qi % kFQ);
             mb_wait(&q_full[slot], static_cast<uint32_t>((qi / kFQ) & 1));
@@ -316,14 +309,73 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
             __syncwarp();
             if (lane == 0) mb_arrive(&q_empty[slot]);
             if (ch < 0) break;
-            const int64_t t1 = (ch + 1) * kFChunk < T ? (ch + 1) * kFChunk : T;
-            for (int64_t t = ch * kFChunk; t < t1; ++t, ++tiles) {
-                const int64_t ct = t / nrt, rt = t % nrt;
-                mb_wait(&acc_full, static_cast<uint32_t>(tiles & 1));
+            for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+                const bool newb = w.ct != cur_ct;
+                if (newb) {
+                    cur_ct = w.ct;
+                    ++bu;
+                }
+                const uint32_t acc = tiles & 1;  // double-buffered accumulator
+                mb_wait(&acc_empty[acc], (tiles >> 1) & 1);
                 tc_after();
-                uint32_t half[2];
+                const uint32_t dacc = tbase + acc * kFN;
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {  // 32 columns at a time: fewer live registers
+                for (int s = 0; s < NST; ++s, ++u) {
+                    if (newb) mb_wait(&b_full[s], (bu - 1) & 1);
+                    const uint32_t sl = u % kFRing;
+                    mb_wait(&a_full[sl], (u / kFRing) & 1);
+                    if (!(dbg & 8)) {
+                        uint64_t da = da0[0];
+#pragma unroll
+                        for (int i = 1; i < kFRing; ++i)
+                            if (sl == static_cast<uint32_t>(i)) da = da0[i];
+#pragma unroll
+                        for (int j = 0; j < kFKS / 64; ++j)  // the tile's first MMA overwrites the accumulator
+                            f4_mma(dacc, da + 16 * j, db0[s] + 16 * j, sfa, sfb, (s | j) != 0);
+                    }
+                    f4_commit(&a_empty[sl]);  // A stage free once these MMAs are done
+                    f4_commit(&b_empty[s]);   // B stage s free once the tile's MMAs on it are done
+                }
+                f4_commit(&acc_full[acc]);
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue ----------------
+        // warp: TMEM lane quarter q (rows 32q..32q+31), 32-column groups h, h + EPW, ... of the tile
+        const int q = warp & 3, h = (warp - 4) >> 2;
+        const uint32_t tq = tbase + (static_cast<uint32_t>(q * 32) << 16);
+        if (h == 0) {  // scale factors: every byte 0x7F = 2^0
+            const uint32_t v = 0x7F7F7F7Fu;
+            for (int c = 0; c < 64; c += 8)
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(tq + kFSfCol + c),
+                             "r"(v));
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) {
+            mb_arrive(&acc_empty[0]);
+            mb_arrive(&acc_empty[1]);
+        }
+        uint32_t tiles = 0;
+        for (int64_t qi = 0;; ++qi) {
+            const int slot = static_cast<int>(qi % kFQ);
+            mb_wait(&q_full[slot], static_cast<uint32_t>((qi / kFQ) & 1));
+            const int64_t ch = q_chunk[slot];
+            __syncwarp();
+            if (lane == 0) mb_arrive(&q_empty[slot]);
+            if (ch < 0) break;
+            for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+                const uint32_t acc = tiles & 1;
+                mb_wait(&acc_full[acc], (tiles >> 1) & 1);
+                tc_after();
+                // 32 columns at a time, then release the buffer
+                constexpr int kG = (kFHW + EPW - 1) / EPW;
+                uint32_t par[kG];
+#pragma unroll
+                for (int c = 0; c < kG; ++c) {
+                    par[c] = 0;
+                    const int g = h + c * EPW;
+                    if (g >= kFHW) break;
                     uint32_t v[32];
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -333,18 +385,27 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
                           "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
                           "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
                           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                        : "r"(tl + h * 64 + c * 32));
+                        : "r"(tq + acc * kFN + 32 * g));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    // exact counts <= 1024: adding 2^23 puts the count's parity in bit 0
                     uint32_t x = 0;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) x = __funnelshift_r(x, v[i], 1);
-                    half[c] = x;
+                    for (int i = 0; i < 32; ++i) x = __funnelshift_r(x, __float_as_uint(__uint_as_float(v[i]) + 8388608.0f), 1);
+                    par[c] = x;
                 }
-                arm();
-                const uint32_t lo = half[0], hi = half[1];
-                const int64_t row = r0 + rt * kFM + q * 32 + lane;
-                const int64_t word = cw0 + ct * 4 + h;
-                if (row < m && word < cw1) C.w[row * C.stride + word] ^= static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+                tc_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(&acc_empty[acc]);  // the MMAs of tile + 2 may overwrite it now
+                const int64_t row = static_cast<int64_t>(w.rt) * kFM + q * 32 + lane;
+                if (row < rows && !(dbg & 1)) {
+                    // fire-and-forget XOR at L2 (RED): the epilogue never waits on C
+                    unsigned* cr = reinterpret_cast<unsigned*>(jb.C.w + (jb.c_r0 + d + row) * jb.C.stride + cw0);
+#pragma unroll
+                    for (int c = 0; c < kG; ++c) {
+                        const int64_t x = static_cast<int64_t>(w.ct) * kFHW + h + c * EPW;  // half-word in the range
+                        if (h + c * EPW < kFHW && x < nhw && par[c]) atomicXor(cr + x, par[c]);
+                    }
+                }
             }
         }
     }
@@ -352,30 +413,46 @@ k_schur_f4(Mat C, int64_t cw0, int64_t cw1, const int64_t* __restrict__ rk, int6
     __syncthreads();
     tc_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(512));
+    if (tl && tid == 0) atomicMax(tl + 128, gtimer());
 }
 
 size_t schur_f4_a_bytes(int64_t rows) { return static_cast<size_t>((rows + kFM - 1) / kFM) * kFMaxStages * kFAStage; }
-size_t schur_f4_b_bytes(int64_t words) { return static_cast<size_t>((words + 3) / 4) * kFMaxStages * kFBStage; }
+size_t schur_f4_b_bytes(int64_t words) {
+    return static_cast<size_t>((2 * words + kFHW - 1) / kFHW) * kFMaxStages * kFBStage;
+}
+
+int g_f4_ring = 4, g_f4_dbg = 0, g_f4_epw = 4;
 
 // K is always padded to kFMaxStages stages (zero nibbles): the B ring then spans exactly
 // one tile, which the loader's B-reload waits rely on (one mbarrier phase per tile)
-void launch_schur_f4_expand_a(cudaStream_t s, const Mat& A, int64_t aw0, int64_t kbits, const int64_t* rk, uint8_t* Ax,
-                              int nsm) {
-    const int nst = kFMaxStages;
-    k_f4_expand_a<<<nsm * 8, 256, 0, s>>>(A, aw0, kbits, rk, A.m, Ax, nst);
+void launch_schur_f4_expand_a(cudaStream_t s, const F4Job& jb, uint8_t* Ax, int nsm) {
+    k_f4_expand_a<<<nsm * 8, 256, 0, s>>>(jb, Ax, kFMaxStages);
 }
 
-void launch_schur_f4(cudaStream_t s, const Mat& C, int64_t cw0, int64_t cw1, const int64_t* rk, const int64_t* brow,
-                     int64_t kbits, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm) {
-    if (cw1 <= cw0) return;
-    const int nst = kFMaxStages;
-    k_f4_expand_b<<<nsm * 8, 256, 0, s>>>(C, brow, kbits, cw0, cw1, Bx, nst);
+void launch_schur_f4(cudaStream_t s, const F4Job& jb, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm,
+                     unsigned long long* tl) {
+    if (jb.cw1 <= jb.cw0) return;
+    k_f4_expand_b<<<nsm * 8, 256, 0, s>>>(jb, Bx, kFMaxStages);
     cudaMemsetAsync(claim, 0, sizeof(unsigned), s);
-    k_schur_f4<<<nsm, kFThreads, kFSmem, s>>>(C, cw0, cw1, rk, C.m, Ax, Bx, nst, claim);
+    const int r6 = g_f4_ring == 6, e1 = g_f4_epw == 1;
+    if (r6 && e1)
+        k_schur_f4<6, 1><<<nsm, f4_threads(1), f4_smem(6), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+    else if (r6)
+        k_schur_f4<6, 4><<<nsm, f4_threads(4), f4_smem(6), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+    else if (e1)
+        k_schur_f4<4, 1><<<nsm, f4_threads(1), f4_smem(4), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+    else
+        k_schur_f4<4, 4><<<nsm, f4_threads(4), f4_smem(4), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
 }
 
 void setup_schur_f4_kernels() {
-    cudaFuncSetAttribute(k_schur_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFSmem));
+    cudaFuncSetAttribute(k_schur_f4<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(4)));
+    cudaFuncSetAttribute(k_schur_f4<6, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
+    cudaFuncSetAttribute(k_schur_f4<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(4)));
+    cudaFuncSetAttribute(k_schur_f4<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
+    if (const char* e = std::getenv("F2_F4_EPW")) g_f4_epw = std::atoi(e);
+    if (const char* e = std::getenv("F2_F4_RING")) g_f4_ring = std::atoi(e);
+    if (const char* e = std::getenv("F2_F4_DBG")) g_f4_dbg = std::atoi(e);
 }
 
 }  // namespace f2g

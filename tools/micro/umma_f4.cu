@@ -44,8 +44,8 @@ __device__ __forceinline__ void tmem_setup(uint32_t* tmem_base_smem, int warp) {
 __device__ __forceinline__ void fill_scales(uint32_t tbase, int warp) {
     if (warp < 4) {  // warp w owns TMEM lanes 32w..32w+31
         const uint32_t v = 0x7F7F7F7Fu;
-        for (int c = 0; c < 64; c += 8) {
-            const uint32_t ta = tbase + (uint32_t(warp * 32) << 16) + SF_COL + c;
+        for (int c = 0; c < 128; c += 8) {  // columns 256..319 and 448..511
+            const uint32_t ta = tbase + (uint32_t(warp * 32) << 16) + (c < 64 ? SF_COL + c : 448 + c - 64);
             asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(v), "r"(v),
                          "r"(v), "r"(v), "r"(v), "r"(v), "r"(v), "r"(v));
         }
@@ -151,17 +151,37 @@ __global__ void __launch_bounds__(NT, 1) k_gf2_f4(const uint8_t* A8, const uint8
 
 // MMA issue rate with smem-resident operands: `iters` x (K/64 MMAs of 128x256x64),
 // one commit + wait per group of 16 MMAs; the result is discarded.
+// variant bits: 1 = stage layout (4 K-stages of 256 elements, SBO 1024 B, as the Schur
+// kernel), 2 = one extra commit per 4 MMAs (to a second mbarrier, never waited on),
+// 4 = accumulator alternates between TMEM columns 0 and PN
 template <int PN>
-__global__ void __launch_bounds__(128, 1) k_f4_peak(int iters, int* sink) {
+__global__ void __launch_bounds__(128, 1) k_f4_peak(int iters, int* sink, int mode, int variant = 0) {
     constexpr uint32_t ID = (1u << 7) | (1u << 10) | (1u << 23) | (uint32_t(PN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
     extern __shared__ __align__(1024) uint8_t sm[];
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar, mbar2;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < (BM + BN) * 512 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0x22222222u, 0, 0x2u, 0);
+    // operand data: mode 0 sparse pattern, 1 random bits (E2M1 0/1.0 per nibble), 2 all ones
+    for (int i = tid; i < (BM + BN) * 512 / 16; i += 128) {
+        uint32_t h = (i + 1) * 0x9E3779B9u;
+        uint4 v = make_uint4(0x22222222u, 0, 0x2u, 0);
+        if (mode == 2) v = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);
+        if (mode == 1) {
+            uint32_t w[4];
+            for (int k = 0; k < 4; ++k) {
+                h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+                uint32_t x = 0;
+                for (int b = 0; b < 8; ++b) x |= ((h >> b) & 1u) << (4 * b + 1);
+                w[k] = x;
+            }
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        reinterpret_cast<uint4*>(sm)[i] = v;
+    }
     tmem_setup(&tmem_base, warp);
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar2)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("fence.proxy.async.shared::cta;\n");
@@ -173,14 +193,52 @@ __global__ void __launch_bounds__(128, 1) k_f4_peak(int iters, int* sink) {
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
+    __shared__ volatile int done;
+    if (tid == 0) done = 0;
+    __syncthreads();
+    if (warp > 0 && (variant & 24)) {  // 8: warps 1-3 spin on an mbarrier; 16: they stream TMEM reads
+        uint32_t sink2 = 0;
+        while (!done) {
+            if (variant & 8) {
+                uint32_t ok;
+                asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0;\n\tselp.u32 %0, 1, 0, P1;\n\t}\n"
+                             : "=r"(ok) : "r"(smem_u32(&mbar2)));
+                sink2 += ok;
+            } else {
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                      "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                      "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(tbase + (uint32_t(warp * 32) << 16) + 320));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                for (int i = 0; i < 32; ++i) sink2 += v[i];
+            }
+        }
+        if (sink2 == 12345) *sink = sink2;
+    }
     if (tid == 0) {
         const uint32_t a = smem_u32(sm), b = a + BM * 512;
         for (int it = 0; it < iters; ++it) {
+            // 4: alternate accumulators 0 / PN; 32: scale factors at column 448; 64: accumulator at column 224
+            const uint32_t acc = (variant & 4) ? ((it & 1) ? tbase + PN : tbase) : (variant & 64) ? tbase + 224 : tbase;
+            const uint32_t sf = tbase + ((variant & 32) ? 448 : SF_COL);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const uint64_t da = desc(a + j * 2 * 128, 128, 32 * 128);
-                const uint64_t db = desc(b + j * 2 * 128, 128, 32 * 128);
-                mma_f4<ID>(tbase, da, db, j > 0 ? 1u : 0u, tbase + SF_COL);
+                uint64_t da, db;
+                if (variant & 1) {  // stage s = j / 4 of 16 KB (A) / PN*128 B (B), K-step j % 4 within it
+                    da = desc(a + (j >> 2) * 16384 + (j & 3) * 256, 128, 1024);
+                    db = desc(b + (j >> 2) * (PN * 128) + (j & 3) * 256, 128, 1024);
+                } else {
+                    da = desc(a + j * 2 * 128, 128, 32 * 128);
+                    db = desc(b + j * 2 * 128, 128, 32 * 128);
+                }
+                mma_f4<ID>(acc, da, db, j > 0 ? 1u : 0u, sf);
+                if ((variant & 2) && (j & 3) == 3)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar2)));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar)));
             asm volatile(
@@ -188,6 +246,7 @@ __global__ void __launch_bounds__(128, 1) k_f4_peak(int iters, int* sink) {
                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
                 "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(&mbar)), "r"(it & 1));
         }
+        done = 1;
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
@@ -263,23 +322,22 @@ int main(int argc, char** argv) {
     const size_t psmem = (BM + BN) * 512;
     int nsm;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    auto peak = [&](auto kern, int pn) {
+    auto peak = [&](auto kern, int pn, int mode, int variant = 0) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem)));
-        const int iters = 2000;
-        kern<<<nsm, 128, psmem>>>(10, sink);
+        const int iters = 4000;
+        kern<<<nsm, 128, psmem>>>(10, sink, mode, variant);
         CK(cudaDeviceSynchronize());
         cudaEventRecord(e0);
-        kern<<<nsm, 128, psmem>>>(iters, sink);
+        kern<<<nsm, 128, psmem>>>(iters, sink, mode, variant);
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));
         float t;
         cudaEventElapsedTime(&t, e0, e1);
         const double macs = double(nsm) * iters * 16 * BM * pn * 64.0;
-        printf("MMA-only N=%d: %.3f ms, %.2f P MAC/s = %.2f P bit-op/s\n", pn, t, macs / (t / 1e3) / 1e15, 2 * macs / (t / 1e3) / 1e15);
+        printf("MMA-only N=%d var=%d data=%s: %.3f ms, %.2f P MAC/s = %.2f P bit-op/s\n", pn, variant,
+               mode == 0 ? "sparse" : mode == 1 ? "random" : "ones", t, macs / (t / 1e3) / 1e15, 2 * macs / (t / 1e3) / 1e15);
     };
-    peak(k_f4_peak<256>, 256);
-    peak(k_f4_peak<192>, 192);
-    peak(k_f4_peak<128>, 128);
-    peak(k_f4_peak<64>, 64);
+    for (int v : {0, 32, 96, 36, 37, 39})
+        peak(k_f4_peak<224>, 224, 1, v);
     return bad != 0;
 }
