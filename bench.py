@@ -5,8 +5,9 @@ Gbit-op/s, 64K^2 dense, 1/2/4/8 B200").
 One step = one pls_recursive (pls.hpp:42-47) of the dense 65536x65536 Bernoulli(1/2)
 matrix (config 3, cutoff_bytes pinned to 2 MiB), restored from a pristine HBM copy
 first.  value = effective bit-ops/s (2 n^3 / 3 per PLS) summed over ranks / device
-time (CUDA events on the library stream, max over ranks).  N > 1 runs one replica
-per GPU (weak scaling; the column-sharded NCCL path is not built yet).
+time (CUDA events on the library stream, max over ranks).  N > 1 (torchrun) runs ONE
+65536^2 PLS column-sharded over the ranks with each panel broadcast over NCCL
+(paper_1006_1744_b200/dist.py; strong scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -38,6 +39,14 @@ CONFIG = {"workload": "config3: pls_recursive, dense 65536x65536 GF(2), Bernoull
           "n": N, "cutoff_bytes": CUTOFF, "panel_bits": 1024,
           "l2": "input 512 MiB > 126 MB L2, restored from an HBM copy every step"}
 SAMPLE_N = 16384  # CPU sample size (reference arm / cpu_baseline)
+# tcgen05.mma kind::mxf4 128x224x64 with SMEM-resident operands on all 148 SMs (tools/micro/umma_f4,
+# profiles/r1_umma_f4_peak.txt): the ceiling of the tensor-core Schur kernel, in fp4 TFLOP/s
+F4_MMA_PEAK_TFLOPS = 7500.0
+try:
+    PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+except Exception:
+    PEAKS = {}
+HBM_GBS = PEAKS.get("hbm_gbs", 6650.0)  # fallback: B200_PROFILING.md
 
 
 def dist_env():
@@ -188,7 +197,7 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         res = step()
-    launches = f2.last_launch_count()
+    launches = f2.last_graph_kernels() or f2.last_launch_count()
 
     barrier()
     with Clocks(local) as clk:
@@ -200,7 +209,10 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = ws * args.steps * BITOPS / (ms / 1e3) / 1e9
 
-    # --- dominant kernel roofline: one instrumented (untimed) run
+    # --- dominant kernel roofline: one instrumented (untimed) run.  The stats run times every
+    # Schur update with CUDA events on the library stream (the launches of the tensor-core
+    # GEMM: A/B operand expansion + k_schur_f4), and reconstructs each launch's work
+    # 2 * rows * pivots * trailing columns from the pivot list afterwards.
     f2.stats_reset()
     f2.stats_enable(True)
     step()
@@ -208,31 +220,29 @@ def run_ours(args):
     fam = [f2.stats_get(k) for k in range(4)]
     schur = fam[0]
     total_fam_ms = sum(x["ms"] for x in fam)
-    sm_clock = 1965.0
-    smem_peak_tbitops = 16384 * 148 * sm_clock * 1e6 / 1e12  # 128 B/clk/SM, 8 coefficient bits per 128-B lookup
     achieved = schur["bitops"] / (schur["ms"] / 1e3) / 1e12 if schur["ms"] else 0.0
-    roofline = {"kernel": "k_table_apply (Schur complement C ^= L21*U12, M4RM in SMEM)",
-                "bound": "smem", "achieved": achieved, "peak": smem_peak_tbitops, "unit": "Tbit-op/s",
-                "frac": achieved / smem_peak_tbitops,
-                "peak_source": "derived, not measured: 128 B/clk/SM SMEM crossbar (B300_MICROARCH.md) x 148 SM x "
-                               "1965 MHz; each 128-B table lookup retires 8 coefficient bits x 1024 columns x 2 ops",
-                "hbm_gbs_algorithmic": schur["bytes"] / (schur["ms"] / 1e3) / 1e9 if schur["ms"] else 0.0,
+    mma_peak = F4_MMA_PEAK_TFLOPS
+    roofline = {"kernel": "k_schur_f4 (Schur complement C ^= L21*U12 on tcgen05 kind::mxf4, + operand expansion)",
+                "bound": "tensor", "achieved": achieved, "peak": mma_peak, "unit": "TFLOP/s",
+                "frac": achieved / mma_peak,
+                "peak_source": "measured: tcgen05.mma kind::mxf4 128x224x64 issue rate with SMEM-resident operands, "
+                               "148 SMs at 1965 MHz (tools/micro/umma_f4, profiles/r1_umma_f4_peak.txt); "
+                               "MEASURED_PEAKS.json has no fp4 figure (4 x its bf16 burst = %.0f; nominal fp4 dense "
+                               "9000)" % (4 * PEAKS.get("bf16_tflops", 0.0)),
+                "frac_of_nominal_fp4": achieved / 9000.0,
+                "unit_note": "1 GF(2) bit-op = 1 fp4 flop: each AND-count term is one MMA multiply-add",
                 "share_of_step": schur["ms"] / total_fam_ms if total_fam_ms else None,
                 "launches": schur["launches"], "avg_launch_ms": schur["ms"] / max(schur["launches"], 1),
                 "traffic": None}
-    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    # (first Schur launch of config 3: C 64512 x 64512 ^= A 64512 x 1024 * B 1024 x 64512)
-    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_schur_config3_raw.json")
+    prof = os.path.join(ROOT, "profiles", "r1_ncu_schur_f4_config3_raw.json")
     if os.path.exists(prof):
         raw = json.load(open(prof))
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        tb = sum(float(raw[k][0]) * scale.get(raw[k][1], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        rows_, cw_, kb_ = 64512, 1008, 1024
-        algo = rows_ * (2 * cw_ * 8 + kb_ // 8) + kb_ * cw_ * 8
-        roofline["traffic"] = tb
-        roofline["traffic_note"] = ("dram read+write bytes of one captured launch (the first, largest Schur launch of "
-                                    "config 3, profiles/r1_ncu_schur_config3_raw.json); that launch's algorithmic "
-                                    f"bytes are {algo:.4g}")
+        roofline["traffic"] = sum(float(raw[k][0]) * scale.get(raw[k][1], 1.0)
+                                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        roofline["traffic_note"] = ("dram read+write bytes of the first wide k_schur_f4 launch of config 3 "
+                                    "(ncu --set full, profiles/r1_ncu_schur_f4_config3_raw.json); its algorithmic "
+                                    "bytes (C read+write once) are %.4g" % (64512 * 64512 / 8 * 2))
 
     # --- MMPF table-apply over a 1 GiB trailing matrix: the HBM-bound kernel of the flat MMPF
     table_apply = {}
@@ -254,7 +264,7 @@ def run_ours(args):
             f2.stats_enable(False)
             st = f2.stats_get(0)
             gbs = st["bytes"] / (st["ms"] / 1e3) / 1e9
-            table_apply[f"k{kbits}"] = {"GB_s": gbs, "frac_of_measured_hbm": gbs / 6554.6,
+            table_apply[f"k{kbits}"] = {"GB_s": gbs, "frac_of_measured_hbm": gbs / HBM_GBS,
                                         "ms_per_launch": st["ms"] / st["launches"],
                                         "bytes_per_launch": st["bytes"] / st["launches"],
                                         "shape": f"C {rows}x{cols} ^= A {rows}x{kbits} * B {kbits}x{cols}"}
@@ -303,7 +313,8 @@ def run_ours(args):
                 "rank": res.rank, "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
                 "table_apply_hbm": table_apply, "cpu_baseline": cpu,
                 "gpu_launches": launches * args.steps,
-                "kernel_families_ms": {k: fam[i]["ms"] for i, k in enumerate(["schur_m4rm", "leaf_pivot", "trsm", "other"])}}
+                "gpu_launches_note": "kernel nodes of the replayed CUDA graph per PLS x steps",
+                "kernel_families_ms": {k: fam[i]["ms"] for i, k in enumerate(["schur", "panel", "trsm", "other"])}}
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -178,6 +178,8 @@ int f2_timer_start(void);
 int f2_timer_stop(double* ms);
 /* kernel launches issued by the last compute call (all families) */
 uint64_t f2_last_launch_count(void);
+/* kernel nodes of the CUDA graph the last graph-replayed PLS launched (0: not a graph run) */
+uint64_t f2_last_graph_kernels(void);
 /* phase clocks of the last leaf (only builds compiled with -DF2_LEAF_PROFILE fill them) */
 int f2_debug_clocks(long long* out, int n);
 /* globaltimer stamps of the panel kernel (only builds compiled with -DF2_PANEL_PROFILE fill them) */

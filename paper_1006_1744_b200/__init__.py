@@ -124,6 +124,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_stats_get": ([i, _u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], i),
         "f2_stats_reset": ([], i),
         "f2_last_launch_count": ([], C.c_uint64),
+        "f2_last_graph_kernels": ([], C.c_uint64),
         "f2_set_panel_bits": ([C.c_uint], i),
         "f2_timer_start": ([], i),
         "f2_timer_stop": ([C.POINTER(C.c_double)], i),
@@ -431,6 +432,11 @@ def stats_get(kind: int) -> dict:
 
 def last_launch_count() -> int:
     return int(load_library().f2_last_launch_count())
+
+
+def last_graph_kernels() -> int:
+    """Kernel nodes of the CUDA graph the last graph-replayed PLS launched (0 if none)."""
+    return int(load_library().f2_last_graph_kernels())
 
 
 def timer_start() -> None:

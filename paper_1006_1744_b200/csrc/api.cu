@@ -87,6 +87,7 @@ struct Ctx {
     bool stats = false;
     uint64_t launches = 0;
     uint64_t graph_launches = 0;
+    uint64_t graph_kernels = 0, last_kernels = 0;  // kernel nodes of the cached PLS graph
     struct Family {
         uint64_t n = 0;
         double ms = 0, bytes = 0, bitops = 0;
@@ -280,6 +281,36 @@ void collect_stats() {
     g_timed.clear();
 }
 
+// ---- event timeline (F2_EVTL=1, non-graph runs only): per-panel marks on the GPU clock
+struct EvMark {
+    const char* name;
+    int64_t panel;
+    cudaEvent_t e;
+};
+std::vector<EvMark> g_evm;
+bool g_evtl = false;
+inline void evmark(cudaStream_t s, const char* name, int64_t pi) {
+    if (!g_evtl) return;
+    cudaEvent_t e;
+    cudaError_t er = cudaEventCreate(&e);
+    if (er == cudaSuccess) er = cudaEventRecord(e, s);
+    if (er == cudaSuccess && std::getenv("F2_EVTL_SYNC")) er = cudaStreamSynchronize(s);
+    if (er != cudaSuccess) std::fprintf(stderr, "evmark %s %lld: %s\n", name, static_cast<long long>(pi), cudaGetErrorString(er));
+    g_evm.push_back({name, pi, e});
+}
+void evdump() {
+    if (g_evm.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& m : g_evm) {
+        float ms = 0;
+        const cudaError_t er = cudaEventElapsedTime(&ms, g_evm[0].e, m.e);
+        if (er != cudaSuccess) std::fprintf(stderr, "evtl: %s\n", cudaGetErrorString(er));
+        std::fprintf(stderr, "EVTL %lld %s %.1f\n", static_cast<long long>(m.panel), m.name, 1e3 * ms);
+    }
+    for (auto& m : g_evm) cudaEventDestroy(m.e);
+    g_evm.clear();
+}
+
 // ---- Q of pls_recursive -------------------------------------------------------
 // pls_recursive_impl's Q bookkeeping (proj/src/pls.cpp:63-103) replayed from the
 // pivot columns: leaf rule :71, cut :74-75, merge :96-98.  The recursion's P,
@@ -367,7 +398,9 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         const int64_t pw0_ = c_ / 64, pw1_ = pw0_ + (cw_ + 63) / 64;
         launch_panel_pipe(st_, A, pw0_, static_cast<int>(cw_), pw1_, g.st, g.P, g.Qp, g.pmap, 0, g.bar, ctas, true);
     };
+    evmark(s, "start", -1);
     if (la) panel_kernel(s, 0, g.nsm);
+    evmark(s, "panel0", -1);
 
     for (int64_t pi = 0; pi < npanels && !stop; ++pi) {
         const int64_t c = pi * W;
@@ -400,11 +433,13 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 }
             }
         }
+        evmark(s, "gather0", pi);
         {
             LaunchTimer t(3, 0, 0);
             launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
             ++g.launches;  // save + put
         }
+        evmark(s, "gather1", pi);
         if (pw1 < nw) {
             TableApply ta{};
             ta.C = A;
@@ -427,25 +462,31 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 // side stream while the main stream solves and updates the columns right of it
                 int64_t* snap = g.snap + (pi & 1) * kSnapWords;
                 launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
+                evmark(s, "snapshot", pi);
                 const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
                 launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
+                evmark(s, "trsm_narrow", pi);
                 ta.brow = snap + kSnapBrow;
                 ta.rk = snap;
                 const bool f4 = g.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
                 const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
                 if (f4) {
                     launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
+                    evmark(s, "expand_a", pi);
                     launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
                 } else {
                     TableApply t1 = ta;
                     t1.cw1 = npw1;
                     launch_table_apply(s, t1, g.nsm, erows);
                 }
+                evmark(s, "schur_narrow", pi);
                 CK(cudaEventRecord(g.la_fork, s));
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
                 panel_kernel(g.side, pi + 1, g.side_ctas);
+                evmark(g.side, "panel_next", pi);
                 CK(cudaEventRecord(g.la_join, g.side));
                 launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
+                evmark(s, "trsm_wide", pi);
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
                 if (npw1 < nw) {
                     if (f4) {
@@ -458,6 +499,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                         fw.cw1 = nw;
                         launch_schur_f4(s, fw, g.f4_ax, g.f4_bx + schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + 1,
                                         g.nsm, tl);
+                        evmark(s, "schur_wide", pi);
                     } else {
                         TableApply t2 = ta;
                         t2.cw0 = npw1;
@@ -563,6 +605,7 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     if (g.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw)))) return rc;
     cudaStream_t s = g.stream;
     const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && !std::getenv("F2_NO_GRAPH");
+    g_evtl = !use_graph && std::getenv("F2_EVTL") != nullptr;
     if (use_graph) {
         const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
                          g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen &&
@@ -578,6 +621,18 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             cudaError_t e = cudaStreamEndCapture(s, &graph);
             if (rc) return rc;
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+            {  // kernel launches per call = the graph's kernel nodes
+                size_t nn = 0;
+                cudaGraphGetNodes(graph, nullptr, &nn);
+                std::vector<cudaGraphNode_t> nodes(nn);
+                if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+                uint64_t nk = 0;
+                for (auto nd : nodes) {
+                    cudaGraphNodeType ty;
+                    if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++nk;
+                }
+                g.graph_kernels = nk;
+            }
             e = cudaGraphInstantiate(&g_graph.exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
@@ -593,12 +648,14 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
         } else {
             g.launches += g.graph_launches;
         }
+        g.last_kernels = g.graph_kernels;
         CK(cudaGraphLaunch(g_graph.exec, s));
     } else {
         rc = enqueue_engine(A, W, s, true);
         if (rc) return rc;
     }
     CK(cudaGetLastError());
+    evdump();
     int64_t r = 0;
     CK(cudaMemcpyAsync(&r, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1019,6 +1076,7 @@ int f2_stats_reset(void) {
 }
 
 uint64_t f2_last_launch_count(void) { return g.launches; }
+uint64_t f2_last_graph_kernels(void) { return g.last_kernels; }
 
 // device timer on the library's stream (bench.py: CUDA events, not host clocks)
 static cudaEvent_t g_t0 = nullptr, g_t1 = nullptr;
