@@ -244,7 +244,8 @@ def run_ours(args):
                                     "(ncu --set full, profiles/r1_ncu_schur_f4_config3_raw.json); its algorithmic "
                                     "bytes (C read+write once) are %.4g" % (64512 * 64512 / 8 * 2))
 
-    # --- MMPF table-apply over a 1 GiB trailing matrix: the HBM-bound kernel of the flat MMPF
+    # --- MMPF table-apply (k_mmpf_apply, K <= 64) over a 1 GiB trailing matrix: the HBM-bound
+    # kernel of the flat MMPF; K = 8 is the paper's single 2^8 table, K = 64 the engine's MMPF panel
     table_apply = {}
     if rank == 0:
         rows, cols = 65536, 131072

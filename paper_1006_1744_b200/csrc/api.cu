@@ -135,6 +135,7 @@ int ensure_init() {
     setup_leafupd_kernels();
     setup_trsm_kernels();
     setup_m4rm_kernels();
+    setup_mmpf_apply_kernels();
     setup_schur_f4_kernels();
     if (std::getenv("F2_SCHUR_M4RM")) g.f4 = false;
     setup_misc_kernels();

@@ -80,6 +80,9 @@ void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, i
 // kernel) is placed at once instead of after the first wave of tiles
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0, int idle_ctas = 0);
 void setup_m4rm_kernels();
+// mmpf_apply.cu -- the HBM-streaming table-apply for K <= 64 (one coefficient word per row)
+void launch_mmpf_apply(cudaStream_t s, const TableApply& t, int nsm);
+void setup_mmpf_apply_kernels();
 
 // schur_f4.cu -- C ^= A * B over GF(2) with K <= 1024 on the tensor cores (tcgen05
 // kind::mxf4, parity of exact fp32 counts): the Schur update of pls_recursive and the

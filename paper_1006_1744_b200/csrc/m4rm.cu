@@ -400,6 +400,11 @@ static size_t table_apply_smem() { return kSmem; }
 // the split; correctness never depends on it.
 void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows, int idle_ctas) {
     if (t.cw1 <= t.cw0 || t.kbits <= 0) return;
+    static const bool mmpf_stream = !std::getenv("F2_NO_MMPF_STREAM");
+    if (t.kw == 1 && idle_ctas == 0 && mmpf_stream) {  // K <= 64: HBM-streaming MMPF kernel
+        launch_mmpf_apply(s, t, nsm);
+        return;
+    }
     const int64_t lo = t.row_mode == ROWS_STATIC ? t.c_r0 : 0;
     const int64_t rows = t.c_r1 - lo;
     if (rows <= 0) return;
