@@ -71,6 +71,8 @@ struct Ctx {
     int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
+    cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
+    cudaEvent_t ax_fork = nullptr, ax_join = nullptr;
     int64_t* snap = nullptr;  // [2][kSnapWords]
     // tensor-core Schur of the look-ahead path (F2_SCHUR_M4RM=1: the SMEM table kernel)
     bool f4 = true;
@@ -155,6 +157,9 @@ int ensure_init() {
         CK(cudaStreamCreateWithPriority(&g.side, cudaStreamNonBlocking, hi));
         CK(cudaEventCreateWithFlags(&g.la_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.la_join, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&g.ax_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.ax_join, cudaEventDisableTiming));
         CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
     }
     CK(cudaGetLastError());
@@ -462,18 +467,26 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 // columns narrow and fast, their Schur update, then panel pi+1's kernel on the
                 // side stream while the main stream solves and updates the columns right of it
                 int64_t* snap = g.snap + (pi & 1) * kSnapWords;
+                const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
+                const bool f4 = g.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
+                const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
+                if (f4) {  // the L21 operand only needs the gathered rows: expand it next to snapshot + TRSM
+                    F4Job fa = fj;
+                    fa.rk = &g.st->panel_r;  // stable until panel pi + 1's kernel starts (after the join)
+                    CK(cudaEventRecord(g.ax_fork, s));
+                    CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
+                    launch_schur_f4_expand_a(g.aux, fa, g.f4_ax, g.nsm);
+                    evmark(g.aux, "expand_a", pi);
+                    CK(cudaEventRecord(g.ax_join, g.aux));
+                }
                 launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
                 evmark(s, "snapshot", pi);
-                const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
                 launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
                 evmark(s, "trsm_narrow", pi);
                 ta.brow = snap + kSnapBrow;
                 ta.rk = snap;
-                const bool f4 = g.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
-                const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
                 if (f4) {
-                    launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
-                    evmark(s, "expand_a", pi);
+                    CK(cudaStreamWaitEvent(s, g.ax_join, 0));
                     launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
                 } else {
                     TableApply t1 = ta;
@@ -1458,7 +1471,15 @@ int f2_dist_apply_panel(f2_matrix* a, size_t tw0, unsigned width_bits, int owner
         ta.brow = g.st->brow;
         ta.row_mode = ROWS_AFTER_PANEL;
         ta.st = g.st;
-        launch_table_apply(s, ta, g.nsm);
+        if (g.f4 && width_bits >= 256 && ensure_f4(static_cast<size_t>(A.m), static_cast<size_t>(nw)) == F2_OK) {
+            // the panel's Schur update on the tensor cores (as in the single-GPU engine)
+            F4Job j = pls_f4_job(A, 0, width_bits, static_cast<int64_t>(tw0), nw, &g.st->panel_r, g.st->brow);
+            j.A = Cf;  // coefficients: the broadcast panel words
+            launch_schur_f4_expand_a(s, j, g.f4_ax, g.nsm);
+            launch_schur_f4(s, j, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+        } else {
+            launch_table_apply(s, ta, g.nsm);
+        }
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));

@@ -175,10 +175,14 @@ void launch_set_r(cudaStream_t s, PlsState* st, int64_t r) { k_set_r<<<1, 1, 0, 
 __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
                                                   uint64_t* scratch) {
     const int n = st->nmoved;
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);  // word pair (16 B)
     if (k >= nwords) return;
-    for (int i = blockIdx.y; i < n; i += gridDim.y)
-        scratch[static_cast<int64_t>(i) * A.stride + k] = A.w[pmap[st->moved[i]] * A.stride + k];
+    for (int i = blockIdx.y; i < n; i += gridDim.y) {
+        const uint64_t* src = A.w + pmap[st->moved[i]] * A.stride + k;
+        uint64_t* dst = scratch + static_cast<int64_t>(i) * A.stride + k;
+        if (k + 1 < nwords) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        else dst[0] = src[0];
+    }
 }
 
 // Panel end, step 2: physical row x <- saved content, pmap back to identity.
@@ -186,10 +190,13 @@ __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const 
 __global__ void __launch_bounds__(256) k_perm_put(Mat A, int64_t nwords, const PlsState* st, int64_t* pmap,
                                                  const uint64_t* scratch) {
     const int n = st->nmoved;
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
     for (int i = blockIdx.y; i < n; i += gridDim.y) {
         const int64_t x = st->moved[i];
-        if (k < nwords) A.w[x * A.stride + k] = scratch[static_cast<int64_t>(i) * A.stride + k];
+        const uint64_t* src = scratch + static_cast<int64_t>(i) * A.stride + k;
+        uint64_t* dst = A.w + x * A.stride + k;
+        if (k + 1 < nwords) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        else if (k < nwords) dst[0] = src[0];
         if (k == 0) pmap[x] = x;
     }
 }
@@ -206,7 +213,9 @@ void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int fir
 }
 
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch) {
-    dim3 grid(static_cast<unsigned>((nwords + 255) / 256), 64);
+    // rows are 128-byte aligned (stride % 16 words == 0): 16-byte accesses, ~1024 CTAs
+    const unsigned gx = static_cast<unsigned>((nwords + 511) / 512);
+    dim3 grid(gx, gx >= 1024 ? 1u : 1024u / gx);
     k_perm_save<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
     k_perm_put<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
 }

@@ -18,7 +18,7 @@ if os.environ.get("F2_EVTL") is None:
     per = collections.defaultdict(dict)
     for _, p, name, t in lines:
         per[int(p)][name] = float(t)
-    order = ["gather0", "gather1", "snapshot", "trsm_narrow", "expand_a", "schur_narrow", "trsm_wide", "schur_wide"]
+    order = ["gather0", "gather1", "snapshot", "trsm_narrow", "schur_narrow", "trsm_wide", "schur_wide"]
     tot = collections.Counter()
     prev_end = per[-1].get("panel0", 0.0)
     rows = []
