@@ -42,7 +42,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libf2gpu.so")
+# F2_LIB: an alternative build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("F2_LIB") or os.path.join(_HERE, "libf2gpu.so")
 
 F2_OK, F2_INVALID_ARGUMENT, F2_OUT_OF_RANGE, F2_CUDA_ERROR, F2_NO_DEVICE, F2_OUT_OF_MEMORY, F2_FORMAT_ERROR = range(7)
 ALG_GAUSS, ALG_M4RI, ALG_MMPF, ALG_PLS, ALG_HYBRID = range(5)

@@ -14,7 +14,7 @@
 //   k_f4_expand_b: the pivot rows U12 gathered by the raw-column map (brow), 32x32
 //     bit blocks transposed by warp shuffles (the MMA wants B K-major too) and
 //     expanded; one 32 KB block per (256-column tile, K stage).
-//   k_schur_f4: persistent, one CTA per SM.  A CTA claims chunks of 16 consecutive
+//   k_schur_f4: persistent, one CTA per SM.  A CTA claims chunks of <= 32 consecutive
 //     tiles (column-tile major, so the CTA's B tile -- 128 KB, the whole K -- stays in
 //     SMEM across a chunk and is reloaded stage by stage while the last tile of the
 //     old column still computes).  Warp 1 streams A stages through a 4-deep ring
@@ -41,7 +41,6 @@ constexpr int kFAStage = kFM * kFKS / 2;          // 16 KB of nibbles
 constexpr int kFBStage = kFN * kFKS / 2;          // 28 KB
 constexpr int kFMaxStages = 4;                    // K <= 1024
 constexpr int kFRingMax = 6;                      // A stages in flight (template RING <= this)
-constexpr int kFChunk = 16;                       // tiles per claimed chunk
 constexpr int kFQ = 8;                            // chunk-id broadcast ring
 // threads: warp 0 MMA, warp 1 loads, warps 2-3 idle, 4 * EPW epilogue warps from warp 4
 constexpr int f4_threads(int epw) { return 128 + 128 * epw; }
@@ -188,11 +187,11 @@ __device__ __forceinline__ void f4_commit(uint64_t* b) {
 // column-major tile order (row tile fastest), so consecutive tiles share the B tile.
 struct F4Walk {
     int rt, ct, n;  // current tile, tiles left in the chunk
-    __device__ __forceinline__ F4Walk(int64_t ch, int nrt, int64_t T) {
-        const int64_t t = ch * kFChunk;
+    __device__ __forceinline__ F4Walk(int64_t ch, int nrt, int64_t T, int chunk) {
+        const int64_t t = ch * chunk;
         ct = static_cast<int>(t / nrt);
         rt = static_cast<int>(t - static_cast<int64_t>(ct) * nrt);
-        n = static_cast<int>(T - t < kFChunk ? T - t : kFChunk);
+        n = static_cast<int>(T - t < chunk ? T - t : chunk);
     }
     __device__ __forceinline__ void next(int nrt) {
         if (++rt == nrt) {
@@ -202,7 +201,8 @@ struct F4Walk {
     }
 };
 
-// dbg (experiments only): bit 0 skips the C update, bit 2 the A stage copies, bit 3 the MMAs
+// dbg (experiments only): bit 0 skips the C update, bit 2 the A stage copies, bit 3 the MMAs;
+// bits 16+: tiles per claimed chunk (0: from the launch size)
 template <int kFRing, int EPW>
 __global__ void __launch_bounds__(f4_threads(EPW), 1)
 k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
@@ -225,7 +225,13 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
     const int64_t nhw = 2 * (cw1 - cw0);
     const int nrt = static_cast<int>((rows + kFM - 1) / kFM), nct = static_cast<int>((nhw + kFHW - 1) / kFHW);
     const int64_t T = static_cast<int64_t>(nrt) * nct;
-    const int64_t nchunks = (T + kFChunk - 1) / kFChunk;
+    // chunk: k = ceil(tiles per CTA / 32) chunks per CTA of equal size <= 32 (long runs on one
+    // B tile, at most one tile of imbalance when the grid divides the work evenly)
+    const int64_t per_cta = (T + gridDim.x - 1) / gridDim.x;
+    const int64_t kch = (per_cta + 31) / 32;
+    int chunk = static_cast<int>((T + gridDim.x * kch - 1) / (gridDim.x * kch));
+    if (dbg >> 16) chunk = dbg >> 16;
+    const int64_t nchunks = (T + chunk - 1) / chunk;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(&tmem_base)), "r"(512));
@@ -266,7 +272,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                 q_chunk[slot] = ch < nchunks ? ch : -1;
                 mb_arrive(&q_full[slot]);  // release: the consumers read q_chunk after the wait
                 if (ch >= nchunks) break;
-                for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+                for (F4Walk w(ch, nrt, T, chunk); w.n > 0; --w.n, w.next(nrt), ++tiles) {
                     if (w.ct != cur_ct) {  // new B tile, stage by stage behind the last MMAs on the old one
                         for (int s = 0; s < NST; ++s) {
                             // b_empty[s] completes one phase per tile: wait for the previous tile's
@@ -309,7 +315,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
             __syncwarp();
             if (lane == 0) mb_arrive(&q_empty[slot]);
             if (ch < 0) break;
-            for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+            for (F4Walk w(ch, nrt, T, chunk); w.n > 0; --w.n, w.next(nrt), ++tiles) {
                 const bool newb = w.ct != cur_ct;
                 if (newb) {
                     cur_ct = w.ct;
@@ -364,7 +370,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
             __syncwarp();
             if (lane == 0) mb_arrive(&q_empty[slot]);
             if (ch < 0) break;
-            for (F4Walk w(ch, nrt, T); w.n > 0; --w.n, w.next(nrt), ++tiles) {
+            for (F4Walk w(ch, nrt, T, chunk); w.n > 0; --w.n, w.next(nrt), ++tiles) {
                 const uint32_t acc = tiles & 1;
                 mb_wait(&acc_full[acc], (tiles >> 1) & 1);
                 tc_after();
@@ -451,6 +457,7 @@ void setup_schur_f4_kernels() {
     cudaFuncSetAttribute(k_schur_f4<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(4)));
     cudaFuncSetAttribute(k_schur_f4<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
     if (const char* e = std::getenv("F2_F4_EPW")) g_f4_epw = std::atoi(e);
+    if (const char* e = std::getenv("F2_F4_CHUNK")) g_f4_dbg |= std::atoi(e) << 16;
     if (const char* e = std::getenv("F2_F4_RING")) g_f4_ring = std::atoi(e);
     if (const char* e = std::getenv("F2_F4_DBG")) g_f4_dbg = std::atoi(e);
 }
