@@ -48,6 +48,23 @@ def test_mul_m4rm_vs_reference(f2, oracle):
         assert (got == oracle.mul(a, s, b, n)).all(), (m, s, n)
 
 
+@pytest.mark.parametrize("k", [1, 8, 9, 33, 64])
+def test_addmul_mmpf_streaming_kernel(f2, oracle, k):
+    """K <= 64 takes the HBM-streaming MMPF table-apply: every table count (1-8 8-bit tables,
+    4096- to 512-bit tiles), a C window starting at an odd word, rows across 2048-row blocks."""
+    rng = np.random.default_rng(k)
+    p, q, c0 = 4500, 5000, 64 * 3
+    a, b = rand_words(rng, p, k), rand_words(rng, k, q)
+    big = rand_words(rng, p, q + c0 + 64)
+    dc = f2.DeviceMatrix.from_host(big, q + c0 + 64)
+    f2.addmul(dc, f2.DeviceMatrix.from_host(a, k), f2.DeviceMatrix.from_host(b, q), wc=dc.window(0, c0, p, c0 + q))
+    got = dc.download()
+    exp = big.copy()
+    prod = oracle.mul(a, k, b, q)
+    exp[:, c0 // 64:c0 // 64 + words(q)] ^= prod
+    assert (got == exp).all()
+
+
 @pytest.mark.parametrize("c0", [64, 69])
 def test_addmul_windows(f2, oracle, c0):
     """C, A, B as windows of larger matrices: only the C window changes."""
