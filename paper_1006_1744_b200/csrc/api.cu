@@ -69,6 +69,7 @@ struct Ctx {
     // CTAs while the Schur update of panel p covers the columns right of panel p+1
     bool lookahead = true;    // F2_NO_LOOKAHEAD=1 disables
     int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
+    int side_ctas_late = 48;  // F2_SIDE_CTAS_LATE: the second half of the factorisation (0: same)
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
     cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
@@ -147,6 +148,7 @@ int ensure_init() {
     g.fused = !(std::getenv("F2_UNFUSED") && std::getenv("F2_UNFUSED")[0] == '1');
     g.pipe = !(std::getenv("F2_NO_PIPE") && std::getenv("F2_NO_PIPE")[0] == '1');
     g.lookahead = !(std::getenv("F2_NO_LOOKAHEAD") && std::getenv("F2_NO_LOOKAHEAD")[0] == '1');
+    if (const char* e = std::getenv("F2_SIDE_CTAS_LATE")) g.side_ctas_late = std::atoi(e);
     if (const char* e = std::getenv("F2_SIDE_CTAS")) {
         const int v = std::atoi(e);
         if (v >= 2 && v <= g.nsm) g.side_ctas = v;
@@ -496,7 +498,10 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 evmark(s, "schur_narrow", pi);
                 CK(cudaEventRecord(g.la_fork, s));
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
-                panel_kernel(g.side, pi + 1, g.side_ctas);
+                // once the trailing update no longer dwarfs the panel kernel (~45 % of the panels
+                // done), give the side kernel more SMs: it is then on the critical path
+                const int side = g.side_ctas_late > 0 && 20 * (pi + 1) >= 9 * npanels ? g.side_ctas_late : g.side_ctas;
+                panel_kernel(g.side, pi + 1, side);
                 evmark(g.side, "panel_next", pi);
                 CK(cudaEventRecord(g.la_join, g.side));
                 launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);

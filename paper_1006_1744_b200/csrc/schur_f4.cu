@@ -427,7 +427,7 @@ size_t schur_f4_b_bytes(int64_t words) {
     return static_cast<size_t>((2 * words + kFHW - 1) / kFHW) * kFMaxStages * kFBStage;
 }
 
-int g_f4_ring = 4, g_f4_dbg = 0, g_f4_epw = 4;
+int g_f4_ring = 6, g_f4_dbg = 0, g_f4_epw = 4;
 
 // K is always padded to kFMaxStages stages (zero nibbles): the B ring then spans exactly
 // one tile, which the loader's B-reload waits rely on (one mbarrier phase per tile)
