@@ -34,6 +34,11 @@ namespace f2g {
 namespace {
 
 constexpr int kPT = 1024;                  // threads per CTA
+#ifdef F2_ONE_WARP_PIVOTS
+constexpr bool kSrcFromSearch = false;
+#else
+constexpr bool kSrcFromSearch = true;      // the two-warp search's tracker warp leaves the slot sources
+#endif
 constexpr int kRows = (kPT / 32) * 4 * 4;  // rows per update tile (512): 4 lane groups x 4 rows per warp
 constexpr int kW = 16;                     // words of the panel remainder a tile covers (W <= 1024)
 constexpr int kTab = 256 * kW;             // one 8-bit group table (CTA 0's fallback solve), words
@@ -662,6 +667,17 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->q[l] = q;
         pk->q[l] = q;
         F.posc[l] = -1;
+    } else if (tid >= 320 && kSrcFromSearch) {
+        // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order): they need
+        // only the slot sources, so they are built here, beside L11^-1, by the idle threads
+        for (int i = tid - 320; i < 16 * 16 * nrest; i += kPT - 320) {
+            const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
+            uint64_t v = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
+            S.t16[ge * 15 + k] = v;
+        }
     }
     if (first)
         for (int i = tid; i < nleaves * 64; i += kPT) st->brow[i] = -1;
@@ -680,14 +696,15 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     if (tid < kb) F.posc[F.step_c[tid]] = tid;
     if (tid >= 960) pk->linv[tid - 960] = F.linv[tid - 960];  // the lmap is a worker's job
     if (tid == 0) pk->leaf = leaf;
-    // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order)
-    for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
-        const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
-        uint64_t v = 0;
+    if (!kSrcFromSearch) {  // (one-warp search: the slot sources were derived above)
+        for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
+            const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
+            uint64_t v = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
-        S.t16[ge * 15 + k] = v;
+            for (int b = 0; b < 4; ++b)
+                if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
+            S.t16[ge * 15 + k] = v;
+        }
     }
     __syncthreads();
     if (clk) st->dbg[26] = clock64() - c0;
