@@ -74,6 +74,8 @@ struct Ctx {
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
     cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
     cudaEvent_t ax_fork = nullptr, ax_join = nullptr;
+    cudaEvent_t tw_fork = nullptr, tw_join = nullptr;  // wide TRSM beside the narrow one (early panels)
+    bool early_wide_trsm = true;                       // F2_NO_EARLY_WIDE_TRSM=1 disables
     int64_t* snap = nullptr;  // [2][kSnapWords]
     // tensor-core Schur of the look-ahead path (F2_SCHUR_M4RM=1: the SMEM table kernel)
     bool f4 = true;
@@ -162,6 +164,9 @@ int ensure_init() {
         CK(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g.ax_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.ax_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.tw_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.tw_join, cudaEventDisableTiming));
+        g.early_wide_trsm = !std::getenv("F2_NO_EARLY_WIDE_TRSM");
         CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
     }
     CK(cudaGetLastError());
@@ -483,6 +488,17 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 }
                 launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
                 evmark(s, "snapshot", pi);
+                // while the trailing update dominates (the first ~45 % of the panels), the wide
+                // TRSM (disjoint columns) runs beside the narrow one instead of after the fork
+                const bool late = 20 * (pi + 1) >= 9 * npanels;
+                const bool wide_early = !late && g.early_wide_trsm && npw1 < nw;
+                if (wide_early) {
+                    CK(cudaEventRecord(g.tw_fork, s));
+                    CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
+                    launch_panel_trsm_snap(g.aux, A, snap, nleaves, npw1, nw, 8);
+                    evmark(g.aux, "trsm_wide", pi);
+                    CK(cudaEventRecord(g.tw_join, g.aux));
+                }
                 launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
                 evmark(s, "trsm_narrow", pi);
                 ta.brow = snap + kSnapBrow;
@@ -500,12 +516,16 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
                 // once the trailing update no longer dwarfs the panel kernel (~45 % of the panels
                 // done), give the side kernel more SMs: it is then on the critical path
-                const int side = g.side_ctas_late > 0 && 20 * (pi + 1) >= 9 * npanels ? g.side_ctas_late : g.side_ctas;
+                const int side = g.side_ctas_late > 0 && late ? g.side_ctas_late : g.side_ctas;
                 panel_kernel(g.side, pi + 1, side);
                 evmark(g.side, "panel_next", pi);
                 CK(cudaEventRecord(g.la_join, g.side));
-                launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
-                evmark(s, "trsm_wide", pi);
+                if (wide_early) {
+                    CK(cudaStreamWaitEvent(s, g.tw_join, 0));
+                } else {
+                    launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
+                    evmark(s, "trsm_wide", pi);
+                }
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
                 if (npw1 < nw) {
                     if (f4) {
