@@ -111,6 +111,14 @@ unsigned f2_auto_table_bits(size_t dim);
 int f2_rref_from_pls(f2_matrix* a, f2_window w, uint64_t rank, const uint64_t* q, size_t qlen);
 /* echelonize: RREF via pls_recursive + rref_from_pls (equals gauss_rref / m4ri_rref, gauss.hpp:28) */
 int f2_rref(f2_matrix* a, f2_window w, const f2_elim_config* cfg, uint64_t* rank);
+/* size_t m4ri_rref(BitMatrix&, unsigned k = 0, bool full = true) — m4ri.hpp:41, m4ri.cpp:68-87.
+ * full: the RREF; !full: M4RI's echelon form (each gauss_submatrix block reduced inside
+ * itself, rows above untouched), bit-identical to the reference's.  k > 8 -> F2_INVALID_ARGUMENT */
+int f2_m4ri_rref(f2_matrix* a, unsigned k, int full, uint64_t* rank);
+/* size_t hybrid_rref(BitMatrix&, const EliminationConfig&) — pls.hpp:61, pls.cpp:163-198 (the RREF) */
+int f2_hybrid_rref(f2_matrix* a, const f2_elim_config* cfg, uint64_t* rank);
+/* size_t rank(const BitMatrix&, const EliminationConfig&) — pls.hpp:64, pls.cpp:200-216 (A untouched) */
+int f2_rank(const f2_matrix* a, const f2_elim_config* cfg, uint64_t* rank);
 
 /* ---- multiply / triangular solve --------------------------------------- */
 /* void addmul(MatrixWindow c, MatrixWindow a, MatrixWindow b, unsigned k=0) — mul.hpp:20, mul.cpp:102-107 */

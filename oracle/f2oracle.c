@@ -293,3 +293,73 @@ int f2o_rref_from_pls(uint64_t* w, size_t m, size_t n, size_t rank, const uint64
         if (q[j] != j) col_swap_rows(w, s, 0, rank, j, (size_t)q[j]);
     return 0;
 }
+
+/* row i ^= row src over columns [from, n) — BitMatrix::row_add, include/f2lin/bitmat.hpp */
+static void row_add_from(uint64_t* w, size_t s, size_t n, size_t i, size_t src, size_t from) {
+    if (from >= n) return;
+    size_t k0 = from / 64;
+    uint64_t first = ~0ull << (from % 64);
+    w[i * s + k0] ^= w[src * s + k0] & first;
+    for (size_t k = k0 + 1; k < WORDS(n); ++k) w[i * s + k] ^= w[src * s + k];
+}
+
+static void row_swap_full(uint64_t* w, size_t s, size_t a, size_t b) {
+    if (a == b) return;
+    for (size_t k = 0; k < s; ++k) {
+        uint64_t t = w[a * s + k];
+        w[a * s + k] = w[b * s + k];
+        w[b * s + k] = t;
+    }
+}
+
+/* gauss_submatrix — src/m4ri.cpp:45-67: RREF of the k-column block at (r, c), pivots
+ * searched in rows [r, r_end) with lazy clearing of the block's earlier columns. */
+static unsigned gauss_submatrix(uint64_t* w, size_t s, size_t n, size_t r, size_t c, unsigned k, size_t r_end) {
+    size_t r_s = r;
+    for (size_t j = c; j < c + k; ++j) {
+        int found = 0;
+        for (size_t i = r_s; i < r_end; ++i) {
+            for (size_t l = 0; l < j - c; ++l)
+                if (GET(w, s, i, c + l)) row_add_from(w, s, n, i, r + l, c + l);
+            if (GET(w, s, i, j)) {
+                row_swap_full(w, s, i, r_s);
+                for (size_t l = r; l < r_s; ++l)
+                    if (GET(w, s, l, j)) row_add_from(w, s, n, l, r_s, j);
+                ++r_s;
+                found = 1;
+                break;
+            }
+        }
+        if (!found) break;
+    }
+    return (unsigned)(r_s - r);
+}
+
+/* m4ri_rref — src/m4ri.cpp:68-87.  The table step (make_table :11-26 +
+ * add_rows_from_table :28-38) adds, to every row outside the block, the combination
+ * of the block's pivot rows that clears its kbar block bits; the block rows are the
+ * identity on the block's (consecutive) pivot columns, so that combination is the
+ * sum of the pivot rows whose column bit is set.  Returns the rank, or -1 for k > 8. */
+long f2o_m4ri_rref(uint64_t* w, size_t m, size_t n, unsigned k, int full) {
+    if (m == 0 || n == 0) return 0;
+    if (k > 8) return -1;
+    size_t s = WORDS(n);
+    unsigned k0 = k ? k : f2o_auto_table_bits(m < n ? m : n);
+    size_t r = 0, c = 0;
+    while (r < m && c < n) {
+        unsigned kc = (unsigned)(n - c < k0 ? n - c : k0);
+        unsigned kbar = gauss_submatrix(w, s, n, r, c, kc, m);
+        if (kbar > 0) {
+            for (size_t i = 0; i < m; ++i) {
+                if (i >= r && i < r + kbar) continue;
+                if (i < r && !full) continue;
+                for (unsigned b = 0; b < kbar; ++b)
+                    if (GET(w, s, i, c + b)) row_add_from(w, s, n, i, r + b, c);
+            }
+            r += kbar;
+            c += kbar;
+        }
+        if (kbar != kc) ++c;
+    }
+    return (long)r;
+}

@@ -28,4 +28,5 @@ int f2o_pls_check(const uint64_t* orig, const uint64_t* packed, size_t m, size_t
                   const uint64_t* p, const uint64_t* q);
 size_t f2o_gauss_rref(uint64_t* w, size_t m, size_t n);
 int f2o_rref_from_pls(uint64_t* w, size_t m, size_t n, size_t rank, const uint64_t* q, size_t qlen);
+long f2o_m4ri_rref(uint64_t* w, size_t m, size_t n, unsigned k, int full);
 #endif

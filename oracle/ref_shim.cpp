@@ -8,6 +8,8 @@
 //   gauss_pls           (proj/src/gauss.cpp:26-55)
 //   rref_from_pls       (proj/src/pls.cpp:128-161)
 //   gauss_rref          (proj/src/gauss.cpp:7-23)
+//   m4ri_rref           (proj/include/f2lin/m4ri.hpp:41, proj/src/m4ri.cpp:68-87)
+//   hybrid_rref, rank   (proj/include/f2lin/pls.hpp:61-64, proj/src/pls.cpp:163-216)
 //   io::read/write_matrix, read/write_permutation (proj/src/io.cpp)
 //   mul_m4rm / addmul   (proj/src/mul.cpp:90-107)
 //   trsm_*_left_unit    (proj/src/mul.cpp:109-157)
@@ -23,6 +25,7 @@
 #include <f2lin/gauss.hpp>
 #include <f2lin/io.hpp>
 #include <filesystem>
+#include <f2lin/m4ri.hpp>
 #include <f2lin/mmpf.hpp>
 #include <f2lin/mul.hpp>
 #include <f2lin/perm.hpp>
@@ -117,6 +120,40 @@ int ref_rref_from_pls(uint64_t* w, size_t m, size_t n, uint64_t rank, const uint
         std::vector<size_t> qv(q, q + qlen);
         rref_from_pls(a.view(), rank, std::span<const size_t>(qv));
         store(a, w);
+    });
+}
+
+int ref_m4ri_rref(uint64_t* w, size_t m, size_t n, unsigned k, int full, uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        *rank = m4ri_rref(a, k, full != 0);
+        store(a, w);
+    });
+}
+
+int ref_hybrid_rref(uint64_t* w, size_t m, size_t n, unsigned k, uint64_t cutoff, double threshold,
+                    uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        EliminationConfig cfg;
+        cfg.k = k;
+        cfg.cutoff_bytes = cutoff;
+        cfg.hybrid_threshold = threshold;
+        *rank = hybrid_rref(a, cfg);
+        store(a, w);
+    });
+}
+
+int ref_rank(const uint64_t* w, size_t m, size_t n, int algorithm, unsigned k, uint64_t cutoff, double threshold,
+             uint64_t* rank) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        EliminationConfig cfg;
+        cfg.k = k;
+        cfg.cutoff_bytes = cutoff;
+        cfg.hybrid_threshold = threshold;
+        cfg.algorithm = static_cast<Algorithm>(algorithm);
+        *rank = f2lin::rank(a, cfg);
     });
 }
 

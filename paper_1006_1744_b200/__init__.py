@@ -124,6 +124,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_stats_enable": ([i], i),
         "f2_stats_get": ([i, _u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], i),
         "f2_stats_reset": ([], i),
+        "f2_m4ri_rref": ([vp, C.c_uint, i, C.POINTER(C.c_uint64)], i),
+        "f2_hybrid_rref": ([vp, C.POINTER(_Cfg), C.POINTER(C.c_uint64)], i),
+        "f2_rank": ([vp, C.POINTER(_Cfg), C.POINTER(C.c_uint64)], i),
         "f2_last_launch_count": ([], C.c_uint64),
         "f2_last_graph_kernels": ([], C.c_uint64),
         "f2_set_panel_bits": ([C.c_uint], i),
@@ -349,6 +352,30 @@ def rref(a: DeviceMatrix, cfg: Optional[EliminationConfig] = None, window: Optio
     cc = (cfg or EliminationConfig()).c()
     r = C.c_uint64()
     _check(_lib.f2_rref(a.handle, _win(a, window).c(), C.byref(cc), C.byref(r)))
+    return int(r.value)
+
+
+def m4ri_rref(a: DeviceMatrix, k: int = 0, full: bool = True) -> int:
+    """In-place M4RI elimination (m4ri.hpp:41): the RREF, or with full=False M4RI's echelon
+    form; returns the rank."""
+    r = C.c_uint64()
+    _check(_lib.f2_m4ri_rref(a.handle, k, int(full), C.byref(r)))
+    return int(r.value)
+
+
+def hybrid_rref(a: DeviceMatrix, cfg: Optional[EliminationConfig] = None) -> int:
+    """hybrid_rref (pls.hpp:61): in-place RREF; returns the rank."""
+    r = C.c_uint64()
+    cc = (cfg or EliminationConfig(algorithm=ALG_HYBRID)).c()
+    _check(_lib.f2_hybrid_rref(a.handle, C.byref(cc), C.byref(r)))
+    return int(r.value)
+
+
+def rank(a: DeviceMatrix, cfg: Optional[EliminationConfig] = None) -> int:
+    """rank(const BitMatrix&, cfg) (pls.hpp:64); A is not modified."""
+    r = C.c_uint64()
+    cc = (cfg or EliminationConfig()).c()
+    _check(_lib.f2_rank(a.handle, C.byref(cc), C.byref(r)))
     return int(r.value)
 
 

@@ -1649,4 +1649,113 @@ int f2_rref(f2_matrix* a, f2_window w, const f2_elim_config* cfg, uint64_t* rank
     return f2_rref_from_pls(a, w, *rank, q.data(), static_cast<size_t>(*rank));
 }
 
+// m4ri_rref(BitMatrix&, k, full) — m4ri.hpp:41, m4ri.cpp:68-87.  full: the RREF (unique,
+// so PLS + rref_from_pls gives it bit for bit).  !full: M4RI's echelon form, U (the PLS
+// pivot rows in original columns) with every block of consecutive pivots that one
+// gauss_submatrix call forms (m4ri.cpp:45-67, blocks of <= k0 = k or auto_table_bits
+// columns, cut at a pivot-less column) reduced inside the block.
+int f2_m4ri_rref(f2_matrix* a, unsigned k, int full, uint64_t* rank) {
+    if (!a || !rank) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const size_t m = a->m, n = a->n;
+    *rank = 0;
+    if (m == 0 || n == 0) return F2_OK;
+    if (k > 8) return fail(F2_INVALID_ARGUMENT, "m4ri_rref: k must be in 0..8");
+    const f2_window w{0, 0, m, n};
+    std::vector<uint64_t> p(m), q(n);
+    int rc = f2_pls_recursive(a, w, p.data(), m, q.data(), n, nullptr, rank);
+    if (rc) return rc;
+    if (full) return f2_rref_from_pls(a, w, *rank, q.data(), static_cast<size_t>(*rank));
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int64_t r = static_cast<int64_t>(*rank);
+    if ((rc = ensure_workspace(m, std::max<size_t>(m, *rank) + 1, 1, static_cast<size_t>(kMaxMoved) * a->stride)))
+        return rc;
+    std::vector<int64_t> qq(q.begin(), q.begin() + r);
+    // the blocks of m4ri_rref's column walk (:73-85) from the pivot columns
+    const unsigned k0 = k ? k : f2_auto_table_bits(std::min(m, n));
+    std::vector<int64_t> bstart;
+    {
+        size_t rr = 0, c = 0;
+        while (rr < m && c < n) {
+            const size_t kc = std::min<size_t>(k0, n - c);
+            size_t kbar = 0;
+            while (kbar < kc && rr + kbar < static_cast<size_t>(r) && static_cast<size_t>(qq[rr + kbar]) == c + kbar) ++kbar;
+            if (kbar) {
+                bstart.push_back(static_cast<int64_t>(rr));
+                rr += kbar;
+                c += kbar;
+            }
+            if (kbar != kc) ++c;
+        }
+        bstart.push_back(r);
+    }
+    if (r) CK(cudaMemcpyAsync(g.Qp, qq.data(), sizeof(int64_t) * r, cudaMemcpyHostToDevice, g.stream));
+    launch_rref_prepare(g.stream, mat_of(a), r, g.Qp);  // U in original columns, rows >= rank zero
+    const int64_t nb = static_cast<int64_t>(bstart.size()) - 1;
+    if (nb > 0) {
+        int64_t* dstart = nullptr;
+        CK(cudaMalloc(&dstart, sizeof(int64_t) * bstart.size()));
+        CK(cudaMemcpyAsync(dstart, bstart.data(), sizeof(int64_t) * bstart.size(), cudaMemcpyHostToDevice, g.stream));
+        launch_block_backsub(g.stream, mat_of(a), dstart, g.Qp, nb, g.nsm);
+        const cudaError_t e = cudaStreamSynchronize(g.stream);
+        cudaFree(dstart);
+        if (e != cudaSuccess) return cuda_fail(e, "m4ri echelon");
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g.stream));
+    return F2_OK;
+}
+
+namespace {
+int validate_cfg(const f2_elim_config& c) {  // pls.cpp:57-61
+    if ((c.cutoff_bytes ? c.cutoff_bytes : default_cutoff()) == 0)
+        return fail(F2_INVALID_ARGUMENT, "cutoff_bytes must be positive");
+    if (!(c.hybrid_threshold >= 0.0 && c.hybrid_threshold <= 1.0))
+        return fail(F2_INVALID_ARGUMENT, "hybrid_threshold must be in [0, 1]");
+    return F2_OK;
+}
+}  // namespace
+
+// hybrid_rref(BitMatrix&, cfg) — pls.hpp:61, pls.cpp:163-198: its result is the RREF of A
+// whatever the density switch decides, so PLS + rref_from_pls gives it bit for bit.
+// k > 8 is rejected (the reference's pls_recursive leaf rejects it once the switch fires).
+int f2_hybrid_rref(f2_matrix* a, const f2_elim_config* cfg, uint64_t* rank) {
+    if (!a || !rank) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const f2_elim_config c0{0, 0, 0.15, F2_ALG_HYBRID};
+    const f2_elim_config& c = cfg ? *cfg : c0;
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    *rank = 0;
+    if (a->m == 0 || a->n == 0) return F2_OK;
+    if (c.k > 8) return fail(F2_INVALID_ARGUMENT, "hybrid_rref: k must be in 0..8");
+    return f2_rref(a, f2_window{0, 0, a->m, a->n}, &c, rank);
+}
+
+// rank(const BitMatrix&, cfg) — pls.hpp:64, pls.cpp:200-216: rank on a working copy, with
+// the validation of the configured algorithm (the rank itself does not depend on it).
+int f2_rank(const f2_matrix* a, const f2_elim_config* cfg, uint64_t* rank) {
+    if (!a || !rank) return fail(F2_INVALID_ARGUMENT, "null argument");
+    const f2_elim_config c0{0, 0, 0.15, F2_ALG_PLS};
+    const f2_elim_config& c = cfg ? *cfg : c0;
+    if (c.algorithm < F2_ALG_GAUSS || c.algorithm > F2_ALG_HYBRID)
+        return fail(F2_INVALID_ARGUMENT, "rank: unknown algorithm");
+    if (c.algorithm == F2_ALG_PLS || c.algorithm == F2_ALG_HYBRID) {
+        int rc = validate_cfg(c);
+        if (rc) return rc;
+    }
+    *rank = 0;
+    if (a->m == 0 || a->n == 0) return F2_OK;
+    if (c.algorithm != F2_ALG_GAUSS && c.k > 8) return fail(F2_INVALID_ARGUMENT, "rank: k must be in 0..8");
+    f2_matrix* work = nullptr;
+    int rc = f2_matrix_create(a->m, a->n, &work);
+    if (rc) return rc;
+    if (!(rc = f2_matrix_copy(work, a))) {
+        std::vector<uint64_t> p(a->m), q(a->n);
+        // the rank is independent of k and of the cutoff: run the engine with the defaults
+        const f2_elim_config cp{0, 0, 0.15, F2_ALG_PLS};
+        rc = f2_pls_recursive(work, f2_window{0, 0, a->m, a->n}, p.data(), a->m, q.data(), a->n, &cp, rank);
+    }
+    f2_matrix_destroy(work);
+    return rc;
+}
+
 }  // extern "C"

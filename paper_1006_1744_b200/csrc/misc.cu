@@ -302,6 +302,47 @@ void launch_rref_coeffs(cudaStream_t s, const Mat& S, int64_t rank, const int64_
     k_rref_coeffs<<<static_cast<int>(g), 256, sizeof(uint64_t) * S.stride, s>>>(S, rank, Qp, Lrev);
 }
 
+// M4RI's non-full echelon form (m4ri_rref(a, k, false), m4ri.cpp:68-87) from U: within
+// each block of consecutive pivots that one gauss_submatrix call forms (m4ri.cpp:45-67),
+// the block's rows are reduced against each other on the block's pivot columns (RREF
+// inside the block only).  One CTA per block, rows bottom-up; a row's coefficients come
+// from its unreduced bits (the reduced later rows are zero on each other's pivots).
+__global__ void __launch_bounds__(256) k_block_backsub(Mat U, const int64_t* __restrict__ bstart,
+                                                       const int64_t* __restrict__ Qp, int64_t nblocks) {
+    __shared__ uint32_t s_mask;
+    const int64_t nw = (U.n + 63) >> 6;
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+        const int64_t t0 = bstart[b], t1 = bstart[b + 1];
+        const int64_t w0 = Qp[t0] >> 6;  // every row of the block is zero left of its first pivot
+        for (int64_t t = t1 - 2; t >= t0; --t) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t mk = 0;
+                for (int64_t u = t + 1; u < t1; ++u) {
+                    const int64_t q = Qp[u];
+                    if ((U.w[t * U.stride + (q >> 6)] >> (q & 63)) & 1ull) mk |= 1u << (u - t - 1);
+                }
+                s_mask = mk;
+            }
+            __syncthreads();
+            const uint32_t mk = s_mask;
+            if (!mk) continue;
+            for (int64_t k = w0 + threadIdx.x; k < nw; k += blockDim.x) {
+                uint64_t v = U.w[t * U.stride + k];
+                for (uint32_t x = mk; x; x &= x - 1) v ^= U.w[(t + 1 + __ffs(x) - 1) * U.stride + k];
+                U.w[t * U.stride + k] = v;
+            }
+        }
+    }
+}
+
+void launch_block_backsub(cudaStream_t s, const Mat& U, const int64_t* bstart, const int64_t* Qp, int64_t nblocks,
+                          int nsm) {
+    if (nblocks <= 0) return;
+    const int64_t g = nblocks < 8 * nsm ? nblocks : 8 * nsm;
+    k_block_backsub<<<static_cast<int>(g), 256, 0, s>>>(U, bstart, Qp, nblocks);
+}
+
 void setup_rref_kernels() {
     cudaFuncSetAttribute(k_rref_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }

@@ -69,6 +69,8 @@ class Oracle:
         L.f2o_gauss_rref.restype = sz
         L.f2o_rref_from_pls.argtypes = [u64p, sz, sz, sz, u64p, sz]
         L.f2o_rref_from_pls.restype = C.c_int
+        L.f2o_m4ri_rref.argtypes = [u64p, sz, sz, C.c_uint, C.c_int]
+        L.f2o_m4ri_rref.restype = C.c_long
 
     def randomize(self, m, n, density, seed):
         w = np.zeros((m, words(n)), dtype=np.uint64)
@@ -115,6 +117,13 @@ class Oracle:
         r = self.lib.f2o_gauss_rref(ptr(w), w.shape[0], n)
         return w, int(r)
 
+    def m4ri_rref(self, w, n, k=0, full=True):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        r = self.lib.f2o_m4ri_rref(ptr(w), w.shape[0], n, k, int(full))
+        if r < 0:
+            raise ValueError("m4ri_rref: k must be in 0..8")
+        return w, int(r)
+
     def rref_from_pls(self, w, n, rank, q):
         w = np.array(w, dtype=np.uint64, copy=True, order="C")
         q = np.ascontiguousarray(q, dtype=np.uint64)
@@ -136,6 +145,9 @@ class RefLib:
         L.ref_gauss_pls.argtypes = [u64p, sz, sz, u64p, u64p, u64p]
         L.ref_rref_from_pls.argtypes = [u64p, sz, sz, C.c_uint64, u64p, sz]
         L.ref_gauss_rref.argtypes = [u64p, sz, sz, u64p]
+        L.ref_m4ri_rref.argtypes = [u64p, sz, sz, C.c_uint, C.c_int, u64p]
+        L.ref_hybrid_rref.argtypes = [u64p, sz, sz, C.c_uint, C.c_uint64, C.c_double, u64p]
+        L.ref_rank.argtypes = [u64p, sz, sz, C.c_int, C.c_uint, C.c_uint64, C.c_double, u64p]
         L.ref_mul_m4rm.argtypes = [u64p, sz, sz, u64p, sz, C.c_uint, u64p]
         L.ref_mul_naive.argtypes = [u64p, sz, sz, u64p, sz, u64p]
         L.ref_trsm_lower_left_unit.argtypes = [u64p, sz, u64p, sz]
@@ -182,6 +194,30 @@ class RefLib:
         if rc:
             raise ValueError(f"reference raised (code {rc})")
         return w
+
+    def m4ri_rref(self, w, n, k=0, full=True):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        r = np.zeros(1, dtype=np.uint64)
+        rc = self.lib.ref_m4ri_rref(ptr(w), w.shape[0], n, k, int(full), ptr(r))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return w, int(r[0])
+
+    def hybrid_rref(self, w, n, k=0, cutoff=0, threshold=0.15):
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        r = np.zeros(1, dtype=np.uint64)
+        rc = self.lib.ref_hybrid_rref(ptr(w), w.shape[0], n, k, cutoff, threshold, ptr(r))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return w, int(r[0])
+
+    def rank(self, w, n, algorithm=3, k=0, cutoff=0, threshold=0.15):
+        w = np.ascontiguousarray(w, dtype=np.uint64)
+        r = np.zeros(1, dtype=np.uint64)
+        rc = self.lib.ref_rank(ptr(w), w.shape[0], n, algorithm, k, cutoff, threshold, ptr(r))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return int(r[0])
 
     def mul_m4rm(self, a, s, b, n, k=0):
         m = a.shape[0]

@@ -111,3 +111,49 @@ def test_window(f2, oracle):
                 assert b == (int(want[i - r0, (j - c0) // 64]) >> ((j - c0) % 64)) & 1
             else:
                 assert b == (int(big[i, j // 64]) >> (j % 64)) & 1
+
+
+@pytest.mark.parametrize("m,n,dens,k", [(50, 70, 0.5, 0), (300, 200, 0.5, 3), (200, 900, 0.1, 8), (1500, 1300, 0.5, 0),
+                                        (700, 700, 0.02, 1), (2100, 3000, 0.5, 5)])
+def test_m4ri_rref_both_modes(f2, oracle, m, n, dens, k):
+    """m4ri_rref (m4ri.cpp:68-87): full = the RREF; full=False = M4RI's block-reduced echelon
+    form, bit for bit against the oracle's restatement (pinned to the reference in
+    test_oracle.py)."""
+    a = oracle.randomize(m, n, dens, m * 7 + n + k)
+    if m > 10:
+        a[m // 2] = a[3]  # rank deficient
+    for full in (True, False):
+        want, wr = oracle.m4ri_rref(a, n, k, full)
+        d = f2.DeviceMatrix.from_host(a, n)
+        assert f2.m4ri_rref(d, k, full) == wr
+        assert (d.download() == want).all(), (m, n, k, full)
+
+
+def test_m4ri_rref_vs_reference_and_errors(f2, oracle, reflib):
+    a = reflib.randomize(600, 800, 0.3, 5)
+    for full in (True, False):
+        want, wr = reflib.m4ri_rref(a, 800, 0, full)
+        d = f2.DeviceMatrix.from_host(a, 800)
+        assert f2.m4ri_rref(d, 0, full) == wr and (d.download() == want).all()
+    with pytest.raises(ValueError):
+        f2.m4ri_rref(f2.DeviceMatrix(4, 4), 9)
+    assert f2.m4ri_rref(f2.DeviceMatrix(0, 5), 9) == 0  # empty: returns before the k check
+
+
+def test_hybrid_rref_and_rank(f2, oracle, reflib):
+    rng = np.random.default_rng(3)
+    for t, (m, n) in enumerate([(64, 64), (500, 700), (1200, 1000)]):
+        a = reflib.randomize(m, n, [0.5, 0.05, 0.5][t], 10 + t)
+        want, wr = reflib.hybrid_rref(a, n, 0, 4096, 0.15)
+        d = f2.DeviceMatrix.from_host(a, n)
+        assert f2.hybrid_rref(d, f2.EliminationConfig(cutoff_bytes=4096, algorithm=f2.ALG_HYBRID)) == wr
+        assert (d.download() == want).all()
+        d = f2.DeviceMatrix.from_host(a, n)
+        for alg in range(5):
+            assert f2.rank(d, f2.EliminationConfig(algorithm=alg)) == wr
+        assert (d.download() == a).all()  # rank leaves A alone
+    with pytest.raises(ValueError):
+        f2.hybrid_rref(f2.DeviceMatrix(3, 3), f2.EliminationConfig(hybrid_threshold=1.5))
+    with pytest.raises(ValueError):
+        f2.rank(f2.DeviceMatrix(3, 3), f2.EliminationConfig(k=9, algorithm=f2.ALG_MMPF))
+    assert f2.rank(f2.DeviceMatrix(3, 3), f2.EliminationConfig(k=9, algorithm=f2.ALG_GAUSS)) == 0
