@@ -129,6 +129,8 @@ int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix*
 int f2_mul_m4rm(const f2_matrix* a, const f2_matrix* b, unsigned k, f2_matrix** out);
 /* void trsm_lower_left_unit(MatrixWindow l, MatrixWindow b) — mul.hpp:24, mul.cpp:109-131 */
 int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window wb);
+/* void trsm_upper_left_unit(MatrixWindow u, MatrixWindow b) — mul.hpp:28, mul.cpp:133-155 */
+int f2_trsm_upper_left_unit(f2_matrix* u, f2_window wu, f2_matrix* b, f2_window wb);
 /* void compress_columns(BitMatrix&, rank, const Permutation& q) — perm.hpp:61, perm.cpp:55-60 */
 int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t qlen);
 /* Permutation::apply_rows / apply_rows_inverse — perm.hpp:42-45, perm.cpp:29-38 */

@@ -119,6 +119,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_addmul": ([vp, _Window, vp, _Window, vp, _Window, C.c_uint], i),
         "f2_mul_m4rm": ([vp, vp, C.c_uint, C.POINTER(vp)], i),
         "f2_trsm_lower_left_unit": ([vp, _Window, vp, _Window], i),
+        "f2_trsm_upper_left_unit": ([vp, _Window, vp, _Window], i),
         "f2_compress_columns": ([vp, C.c_uint64, _u64p, sz], i),
         "f2_apply_rows": ([vp, _Window, _u64p, sz, i], i),
         "f2_stats_enable": ([i], i),
@@ -421,6 +422,12 @@ def trsm_lower_left_unit(l: DeviceMatrix, b: DeviceMatrix, wl: Optional[Window] 
                          wb: Optional[Window] = None) -> None:
     """B <- L^{-1} B, L unit lower (upper part ignored); mul.hpp:24."""
     _check(_lib.f2_trsm_lower_left_unit(l.handle, _win(l, wl).c(), b.handle, _win(b, wb).c()))
+
+
+def trsm_upper_left_unit(u: DeviceMatrix, b: DeviceMatrix, wu: Optional[Window] = None,
+                         wb: Optional[Window] = None) -> None:
+    """B <- U^{-1} B, U unit upper (lower part ignored); mul.hpp:28."""
+    _check(_lib.f2_trsm_upper_left_unit(u.handle, _win(u, wu).c(), b.handle, _win(b, wb).c()))
 
 
 def compress_columns(a: DeviceMatrix, rank: int, q: np.ndarray) -> None:

@@ -1340,6 +1340,42 @@ int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window 
     return F2_OK;
 }
 
+// void trsm_upper_left_unit(MatrixWindow u, MatrixWindow b) — mul.hpp:28, mul.cpp:133-155:
+// B <- U^{-1} B, U unit upper triangular (its lower part ignored).  With R the row/column
+// reversal, U^{-1} B = R (R U R)^{-1} R B: the lower solver on reversed copies.
+int f2_trsm_upper_left_unit(f2_matrix* u, f2_window wu, f2_matrix* b, f2_window wb) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!u || !b) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (!window_ok(u, wu) || !window_ok(b, wb)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
+    const size_t r = wu.r1 - wu.r0;
+    if (r != wu.c1 - wu.c0) return fail(F2_INVALID_ARGUMENT, "trsm: U must be square");
+    if (r != wb.r1 - wb.r0) return fail(F2_INVALID_ARGUMENT, "trsm: dimension mismatch");
+    if (r <= 1 || wb.c1 == wb.c0) return F2_OK;
+    int rc = ensure_init();
+    if (rc) return rc;
+    g.launches = 0;
+    TmpMat ut, bt, lrev, brev;
+    if ((rc = extract_tmp(u, wu, ut)) || (rc = extract_tmp(b, wb, bt))) return rc;
+    if ((rc = alloc_matrix(r, r, &lrev.m)) || (rc = alloc_matrix(r, wb.c1 - wb.c0, &brev.m))) return rc;
+    const int64_t rr = static_cast<int64_t>(r);
+    launch_reverse_square(g.stream, mat_of(lrev.m), mat_of(ut.m), rr);
+    std::vector<int64_t> rev(r);
+    for (int64_t i = 0; i < rr; ++i) rev[i] = rr - 1 - i;
+    int64_t* dmap = nullptr;
+    CK(cudaMalloc(&dmap, sizeof(int64_t) * r));
+    CK(cudaMemcpyAsync(dmap, rev.data(), sizeof(int64_t) * r, cudaMemcpyHostToDevice, g.stream));
+    const int64_t nwb = static_cast<int64_t>(bt.m->stride);
+    launch_gather_rows(g.stream, mat_of(brev.m), mat_of(bt.m), dmap, rr, nwb);
+    trsm_rec(mat_of(lrev.m), mat_of(brev.m), 0, rr);
+    launch_gather_rows(g.stream, mat_of(bt.m), mat_of(brev.m), dmap, rr, nwb);
+    launch_insert(g.stream, mat_of(b), static_cast<int64_t>(wb.r0), static_cast<int64_t>(wb.c0), mat_of(bt.m));
+    const cudaError_t e = cudaStreamSynchronize(g.stream);
+    cudaFree(dmap);
+    if (e != cudaSuccess) return cuda_fail(e, "trsm_upper_left_unit");
+    if (g.stats) collect_stats();
+    return F2_OK;
+}
+
 int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t qlen) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!a || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");

@@ -127,6 +127,7 @@ void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, i
 void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
                        int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm, bool cooperative = true);
 void setup_panel_kernels();
+void launch_reverse_square(cudaStream_t s, const Mat& dst, const Mat& src, int64_t r);
 void launch_block_backsub(cudaStream_t s, const Mat& U, const int64_t* bstart, const int64_t* Qp, int64_t nblocks,
                           int nsm);
 void launch_rref_prepare(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* Qp);

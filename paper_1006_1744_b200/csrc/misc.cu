@@ -209,6 +209,31 @@ void launch_insert(cudaStream_t s, const Mat& dst, int64_t r0, int64_t c0, const
     k_insert<<<grid_for(total, 256), 256, 0, s>>>(dst, r0, c0, src);
 }
 
+// dst[i][j] = src[r-1-i][r-1-j] for an r x r bit matrix: a unit upper triangular U becomes
+// the unit lower triangular R U R, so U^{-1} B = R (R U R)^{-1} R B runs on the lower solver
+__global__ void k_reverse_square(Mat dst, Mat src, int64_t r) {
+    const int64_t nw = (r + 63) >> 6, total = r * nw;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / nw, w = idx - i * nw;
+        const uint64_t* srow = src.w + (r - 1 - i) * src.stride;
+        uint64_t v = 0;
+        for (int b = 0; b < 64; ++b) {
+            const int64_t j = 64 * w + b;
+            if (j >= r) break;
+            const int64_t sj = r - 1 - j;
+            v |= ((srow[sj >> 6] >> (sj & 63)) & 1ull) << b;
+        }
+        dst.w[i * dst.stride + w] = v;
+    }
+}
+
+void launch_reverse_square(cudaStream_t s, const Mat& dst, const Mat& src, int64_t r) {
+    const int64_t total = r * ((r + 63) >> 6);
+    if (total == 0) return;
+    k_reverse_square<<<grid_for(total, 256), 256, 0, s>>>(dst, src, r);
+}
+
 void launch_gather_rows(cudaStream_t s, const Mat& dst, const Mat& src, const int64_t* rowmap, int64_t nrows,
                         int64_t nwords) {
     const int64_t total = nrows * nwords;

@@ -109,6 +109,52 @@ def test_trsm_lower_left_unit(f2, oracle, r, nb):
     assert (dl.download() == lw).all()
 
 
+@pytest.mark.parametrize("r,nb", [(2, 5), (64, 100), (700, 900), (2500, 1100)])
+def test_trsm_upper_left_unit(f2, oracle, r, nb):
+    """B <- U^{-1} B (mul.cpp:133-155): U * B' == B with U's unit upper part (lower ignored),
+    and a window case at bit offsets."""
+    rng = np.random.default_rng(r + 1)
+    uw, b = rand_words(rng, r, r), rand_words(rng, r, nb)
+    du, db = f2.DeviceMatrix.from_host(uw, r), f2.DeviceMatrix.from_host(b, nb)
+    f2.trsm_upper_left_unit(du, db)
+    x = db.download()
+    unit = uw.copy()
+    for i in range(r):  # keep the strictly upper part, put 1 on the diagonal
+        w, bit = divmod(i, 64)
+        unit[i, :w] = 0
+        unit[i, w] &= ~np.uint64((1 << (bit + 1)) - 1) if bit < 63 else np.uint64(0)
+        unit[i, w] |= np.uint64(1 << bit)
+    assert (oracle.mul(unit, r, x, nb) == b).all()
+    assert (du.download() == uw).all()
+
+
+def test_trsm_upper_window(f2, oracle):
+    rng = np.random.default_rng(9)
+    r, nb = 300, 200
+    bigu = rand_words(rng, r + 10, r + 77)
+    bigb = rand_words(rng, r + 5, nb + 70)
+    du, db = f2.DeviceMatrix.from_host(bigu, r + 77), f2.DeviceMatrix.from_host(bigb, nb + 70)
+    f2.trsm_upper_left_unit(du, db, wu=du.window(3, 70, 3 + r, 70 + r), wb=db.window(2, 5, 2 + r, 5 + nb))
+    got = db.download()
+    u = get_bits(bigu, 3, 3 + r, 70, 70 + r)
+    for i in range(r):
+        w, bit = divmod(i, 64)
+        u[i, :w] = 0
+        u[i, w] &= ~np.uint64((1 << (bit + 1)) - 1) if bit < 63 else np.uint64(0)
+        u[i, w] |= np.uint64(1 << bit)
+    x = get_bits(got, 2, 2 + r, 5, 5 + nb)
+    assert (oracle.mul(u, r, x, nb) == get_bits(bigb, 2, 2 + r, 5, 5 + nb)).all()
+    outside = got.copy()
+    ref = bigb.copy()
+    for i in range(2, 2 + r):  # bits outside the window untouched
+        for j in range(5, 5 + nb):
+            wd, bt = divmod(j, 64)
+            m = np.uint64(1) << np.uint64(bt)
+            outside[i, wd] &= ~m
+            ref[i, wd] &= ~m
+    assert (outside == ref).all()
+
+
 def test_mul_errors(f2):
     """invalid_argument (mul.cpp:103-111) surfaces as ValueError."""
     a, b = f2.DeviceMatrix(10, 20), f2.DeviceMatrix(21, 5)
