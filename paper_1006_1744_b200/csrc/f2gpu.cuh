@@ -101,6 +101,11 @@ static __device__ int g_prof_on = 0;
     } while (0)
 #endif
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while its
+// stream predecessor drains; it waits here before touching anything the predecessor
+// wrote (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -174,6 +174,7 @@ void launch_set_r(cudaStream_t s, PlsState* st, int64_t r) { k_set_r<<<1, 1, 0, 
 // (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
 __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
                                                   uint64_t* scratch) {
+    pdl_wait();
     const int n = st->nmoved;
     const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);  // word pair (16 B)
     if (k >= nwords) return;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const 
 // This applies the panel's transpositions (perm.cpp:8-16) to every column.
 __global__ void __launch_bounds__(256) k_perm_put(Mat A, int64_t nwords, const PlsState* st, int64_t* pmap,
                                                  const uint64_t* scratch) {
+    pdl_wait();
     const int n = st->nmoved;
     const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
     for (int i = blockIdx.y; i < n; i += gridDim.y) {
@@ -216,8 +218,8 @@ void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* s
     // rows are 128-byte aligned (stride % 16 words == 0): 16-byte accesses, ~1024 CTAs
     const unsigned gx = static_cast<unsigned>((nwords + 511) / 512);
     dim3 grid(gx, gx >= 1024 ? 1u : 1024u / gx);
-    k_perm_save<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
-    k_perm_put<<<grid, 256, 0, s>>>(A, nwords, st, pmap, scratch);
+    launch_pdl(k_perm_save, grid, dim3(256), 0, s, A, nwords, st, static_cast<const int64_t*>(pmap), scratch);
+    launch_pdl(k_perm_put, grid, dim3(256), 0, s, A, nwords, st, pmap, static_cast<const uint64_t*>(scratch));
 }
 
 void launch_leaf_tables(cudaStream_t s, PlsState* st, int leaf_in_panel) {

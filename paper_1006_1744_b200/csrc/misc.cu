@@ -375,6 +375,7 @@ void setup_rref_kernels() {
 
 __global__ void __launch_bounds__(256) k_panel_snapshot(const PlsState* st, int64_t* snap, Mat Cf, int64_t coef_w0,
                                                         int nleaves) {
+    pdl_wait();
     __shared__ int s_b[2];
     const int j = blockIdx.x, tid = threadIdx.x;
     const int t = blockIdx.y * 256 + tid;
@@ -414,7 +415,8 @@ __global__ void __launch_bounds__(256) k_panel_snapshot(const PlsState* st, int6
 
 void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int nleaves, const Mat& Cf,
                            int64_t coef_w0) {
-    k_panel_snapshot<<<dim3(nleaves, (nleaves * 64 + 255) / 256), 256, 0, s>>>(st, snap, Cf, coef_w0, nleaves);
+    launch_pdl(k_panel_snapshot, dim3(nleaves, (nleaves * 64 + 255) / 256), dim3(256), 0, s, st, snap, Cf, coef_w0,
+               nleaves);
 }
 
 }  // namespace f2g

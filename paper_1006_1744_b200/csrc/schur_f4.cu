@@ -119,6 +119,7 @@ __device__ __forceinline__ int64_t f4_row_shift(const F4Job& jb) { return jb.rk 
 
 // A = coefficient bits [aw0*64, aw0*64 + kbits) of rows a_r0 + d + i
 __global__ void __launch_bounds__(256) k_f4_expand_a(F4Job jb, uint8_t* __restrict__ Ax, int nst) {
+    pdl_wait();
     const int64_t d = f4_row_shift(jb);
     const int64_t rows = jb.rows_end - d;
     if (rows <= 0) return;
@@ -143,7 +144,10 @@ __global__ void __launch_bounds__(256) k_f4_expand_a(F4Job jb, uint8_t* __restri
 
 // B^T: element (n, j) = bit n of B row (brow ? brow[j] : b_r0 + j), columns from 32-bit
 // half-word 2*bw0 on; a tile is kFHW half-words of C starting at 2*cw0 + ct*kFHW
-__global__ void __launch_bounds__(256) k_f4_expand_b(F4Job jb, uint8_t* __restrict__ Bx, int nst) {
+// (also zeroes the Schur launch's work counter: no memset node between the two kernels)
+__global__ void __launch_bounds__(256) k_f4_expand_b(F4Job jb, uint8_t* __restrict__ Bx, int nst, unsigned* claim) {
+    pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *claim = 0u;
     const int lane = threadIdx.x & 31;
     const int64_t nhw = 2 * (jb.cw1 - jb.cw0);
     const int64_t nct = (nhw + kFHW - 1) / kFHW;
@@ -201,12 +205,14 @@ struct F4Walk {
     }
 };
 
-// dbg (experiments only): bit 0 skips the C update, bit 2 the A stage copies, bit 3 the MMAs;
+// dbg (experiments only): bit 0 skips the C update, bit 1 the TMEM reads, bit 2 the A stage
+// copies, bit 3 the MMAs;
 // bits 16+: tiles per claimed chunk (0: from the launch size)
 template <int kFRing, int EPW>
 __global__ void __launch_bounds__(f4_threads(EPW), 1)
 k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
            unsigned long long* tl, int dbg) {
+    pdl_wait();
     constexpr int NST = kFMaxStages;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sB = smem;                        // [NST][28 KB], the whole K of one column tile
@@ -383,6 +389,10 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                     const int g = h + c * EPW;
                     if (g >= kFHW) break;
                     uint32_t v[32];
+                    if (dbg & 2) {  // experiment: no TMEM reads
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = static_cast<uint32_t>(i);
+                    } else {
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -393,6 +403,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(tq + acc * kFN + 32 * g));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    }
                     // exact counts <= 1024: adding 2^23 puts the count's parity in bit 0
                     uint32_t x = 0;
 #pragma unroll
@@ -428,27 +439,31 @@ size_t schur_f4_b_bytes(int64_t words) {
 }
 
 int g_f4_ring = 6, g_f4_dbg = 0, g_f4_epw = 4;
+bool g_pdl = !std::getenv("F2_NO_PDL");  // kernels.cuh: launch_pdl
 
 // K is always padded to kFMaxStages stages (zero nibbles): the B ring then spans exactly
 // one tile, which the loader's B-reload waits rely on (one mbarrier phase per tile)
 void launch_schur_f4_expand_a(cudaStream_t s, const F4Job& jb, uint8_t* Ax, int nsm) {
-    k_f4_expand_a<<<nsm * 8, 256, 0, s>>>(jb, Ax, kFMaxStages);
+    launch_pdl(k_f4_expand_a, dim3(nsm * 8), dim3(256), 0, s, jb, Ax, kFMaxStages);
 }
 
 void launch_schur_f4(cudaStream_t s, const F4Job& jb, const uint8_t* Ax, uint8_t* Bx, unsigned* claim, int nsm,
                      unsigned long long* tl) {
     if (jb.cw1 <= jb.cw0) return;
-    k_f4_expand_b<<<nsm * 8, 256, 0, s>>>(jb, Bx, kFMaxStages);
-    cudaMemsetAsync(claim, 0, sizeof(unsigned), s);
+    launch_pdl(k_f4_expand_b, dim3(nsm * 8), dim3(256), 0, s, jb, Bx, kFMaxStages, claim);
     const int r6 = g_f4_ring == 6, e1 = g_f4_epw == 1;
     if (r6 && e1)
-        k_schur_f4<6, 1><<<nsm, f4_threads(1), f4_smem(6), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+        launch_pdl(k_schur_f4<6, 1>, dim3(nsm), dim3(f4_threads(1)), f4_smem(6), s, jb, Ax,
+                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
     else if (r6)
-        k_schur_f4<6, 4><<<nsm, f4_threads(4), f4_smem(6), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+        launch_pdl(k_schur_f4<6, 4>, dim3(nsm), dim3(f4_threads(4)), f4_smem(6), s, jb, Ax,
+                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
     else if (e1)
-        k_schur_f4<4, 1><<<nsm, f4_threads(1), f4_smem(4), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+        launch_pdl(k_schur_f4<4, 1>, dim3(nsm), dim3(f4_threads(1)), f4_smem(4), s, jb, Ax,
+                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
     else
-        k_schur_f4<4, 4><<<nsm, f4_threads(4), f4_smem(4), s>>>(jb, Ax, Bx, claim, tl, g_f4_dbg);
+        launch_pdl(k_schur_f4<4, 4>, dim3(nsm), dim3(f4_threads(4)), f4_smem(4), s, jb, Ax,
+                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
 }
 
 void setup_schur_f4_kernels() {

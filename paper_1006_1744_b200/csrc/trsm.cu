@@ -519,6 +519,7 @@ void launch_panel_trsm(cudaStream_t s, const Mat& A, const Mat& Cf, int64_t coef
 template <int SW>
 __global__ void __launch_bounds__(512, 1)
 k_panel_trsm_snap(Mat A, const int64_t* __restrict__ snap, int nleaves, int64_t tw0, int64_t tw1) {
+    pdl_wait();
     extern __shared__ __align__(16) uint64_t smem[];
     const int rows_cap = nleaves * 64;
     uint64_t* X = smem;                                               // [rows_cap][SW]
@@ -666,11 +667,11 @@ void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, i
                             int strip) {
     if (tw1 <= tw0) return;
     if (strip == 1) {
-        k_panel_trsm_snap<1><<<static_cast<unsigned>(tw1 - tw0), 512, panel_trsm_snap_smem<1>(nleaves), s>>>(
-            A, snap, nleaves, tw0, tw1);
+        launch_pdl(k_panel_trsm_snap<1>, dim3(static_cast<unsigned>(tw1 - tw0)), dim3(512),
+                   panel_trsm_snap_smem<1>(nleaves), s, A, snap, nleaves, tw0, tw1);
     } else {
-        k_panel_trsm_snap<8><<<static_cast<unsigned>((tw1 - tw0 + 7) / 8), 512, panel_trsm_snap_smem<8>(nleaves), s>>>(
-            A, snap, nleaves, tw0, tw1);
+        launch_pdl(k_panel_trsm_snap<8>, dim3(static_cast<unsigned>((tw1 - tw0 + 7) / 8)), dim3(512),
+                   panel_trsm_snap_smem<8>(nleaves), s, A, snap, nleaves, tw0, tw1);
     }
 }
 
