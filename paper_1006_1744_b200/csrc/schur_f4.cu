@@ -205,9 +205,7 @@ struct F4Walk {
     }
 };
 
-// dbg (experiments only): bit 0 skips the C update, bit 1 the TMEM reads, bit 2 the A stage
-// copies, bit 3 the MMAs;
-// bits 16+: tiles per claimed chunk (0: from the launch size)
+// dbg: bits 16+ = tiles per claimed chunk (0: from the launch size; F2_F4_CHUNK)
 template <int kFRing, int EPW>
 __global__ void __launch_bounds__(f4_threads(EPW), 1)
 k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
@@ -293,10 +291,6 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                     for (int s = 0; s < NST; ++s, ++u) {
                         const uint32_t sl = u % kFRing, f = u / kFRing;
                         if (f > 0) mb_wait(&a_empty[sl], (f - 1) & 1);
-                        if (dbg & 4) {
-                            mb_arrive(&a_full[sl]);
-                            continue;
-                        }
                         mb_expect_tx(&a_full[sl], kFAStage);
                         bulk_g2s(sA + sl * kFAStage, Ax + (static_cast<int64_t>(w.rt) * NST + s) * kFAStage, kFAStage,
                                  &a_full[sl]);
@@ -336,7 +330,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                     if (newb) mb_wait(&b_full[s], (bu - 1) & 1);
                     const uint32_t sl = u % kFRing;
                     mb_wait(&a_full[sl], (u / kFRing) & 1);
-                    if (!(dbg & 8)) {
+                    {
                         uint64_t da = da0[0];
 #pragma unroll
                         for (int i = 1; i < kFRing; ++i)
@@ -389,10 +383,6 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                     const int g = h + c * EPW;
                     if (g >= kFHW) break;
                     uint32_t v[32];
-                    if (dbg & 2) {  // experiment: no TMEM reads
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = static_cast<uint32_t>(i);
-                    } else {
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -403,7 +393,6 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(tq + acc * kFN + 32 * g));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    }
                     // exact counts <= 1024: adding 2^23 puts the count's parity in bit 0
                     uint32_t x = 0;
 #pragma unroll
@@ -414,7 +403,7 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
                 __syncwarp();
                 if (lane == 0) mb_arrive(&acc_empty[acc]);  // the MMAs of tile + 2 may overwrite it now
                 const int64_t row = static_cast<int64_t>(w.rt) * kFM + q * 32 + lane;
-                if (row < rows && !(dbg & 1)) {
+                if (row < rows) {
                     // fire-and-forget XOR at L2 (RED): the epilogue never waits on C
                     unsigned* cr = reinterpret_cast<unsigned*>(jb.C.w + (jb.c_r0 + d + row) * jb.C.stride + cw0);
 #pragma unroll
@@ -474,7 +463,6 @@ void setup_schur_f4_kernels() {
     if (const char* e = std::getenv("F2_F4_EPW")) g_f4_epw = std::atoi(e);
     if (const char* e = std::getenv("F2_F4_CHUNK")) g_f4_dbg |= std::atoi(e) << 16;
     if (const char* e = std::getenv("F2_F4_RING")) g_f4_ring = std::atoi(e);
-    if (const char* e = std::getenv("F2_F4_DBG")) g_f4_dbg = std::atoi(e);
 }
 
 }  // namespace f2g
