@@ -84,6 +84,13 @@ __device__ __forceinline__ uint64_t ldw(const uint64_t* p) {
 }
 __device__ __forceinline__ int64_t ldi(const int64_t* p) { return __ldcg(reinterpret_cast<const long long*>(p)); }
 
+// phase clocks of the panel kernel (tools/dbgclk.py; builds with -DF2_LEAF_CLOCKS only)
+#ifdef F2_LEAF_CLOCKS
+#define F2_CLK(...) __VA_ARGS__
+#else
+#define F2_CLK(...)
+#endif
+
 #ifdef F2_PANEL_PROFILE
 static __device__ int g_prof_on = 0;
 #define F2_STAMP(stp, k)                                                               \

@@ -603,15 +603,14 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     }
     __syncthreads();
     F2_STAMP(st, 16);
-    const bool clk = pw0 == 0 && leaf == 2 && tid == 0;
-    long long c0 = clock64();
+    F2_CLK(const bool clk = pw0 == 0 && leaf == 2 && tid == 0; long long c0 = clock64();)
 #ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
 #else
     if (warp < 3) two_warp_pivots(F, lw, base + kPW < m, false);
 #endif
     __syncthreads();
-    if (clk) st->dbg[20] = clock64() - c0;
+    F2_CLK(if (clk) st->dbg[20] = clock64() - c0;)
     F2_STAMP(st, 18);
     const int kb = F.final_kb;
     if (kb < 0) return -1;
@@ -619,7 +618,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     // warp 0: L11^-1 while the others derive everything that does not need it
 #ifndef F2_ONE_WARP_PIVOTS
     if (warp < 2) pair_linv(F, kb);
-    if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;
+    F2_CLK(if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;)
     if (false) {  // slot sources come from the search's tracker warp
 #else
     if (tid >= 32 && tid < 32 + kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
@@ -637,7 +636,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
             }
         }
         F.src[sl] = x;
-        if (pw0 == 0 && leaf == 2 && tid == 32) st->dbg[29] = clock64() - c0;
+        F2_CLK(if (pw0 == 0 && leaf == 2 && tid == 32) st->dbg[29] = clock64() - c0;)
     } else if (tid >= 32 + kPW && tid < 32 + kPW + 64) {  // finalize basis
         const int e = tid - 32 - kPW, g = e >> 3, b = e & 7;
         int lo = 0, hi = kb;
@@ -657,7 +656,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         }
         pk->fb[e] = corr;
         F.fbas[e] = corr;
-        if (pw0 == 0 && leaf == 2 && e == 63) st->dbg[30] = clock64() - c0;
+        F2_CLK(if (pw0 == 0 && leaf == 2 && e == 63) st->dbg[30] = clock64() - c0;)
     } else if (tid >= 256 && tid < 320) {
         const int l = tid - 256;
         const bool in = l < kb;
@@ -682,7 +681,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     if (first)
         for (int i = tid; i < nleaves * 64; i += kPT) st->brow[i] = -1;
     __syncthreads();
-    if (clk) st->dbg[25] = clock64() - c0;
+    F2_CLK(if (clk) st->dbg[25] = clock64() - c0;)
     F2_STAMP(st, 19);
     // carry finalize tables from the basis; posc; L11^-1 rows in raw columns (for lmap)
     for (int i = tid; i < 8 * 256; i += kPT) {
@@ -707,7 +706,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         }
     }
     __syncthreads();
-    if (clk) st->dbg[26] = clock64() - c0;
+    F2_CLK(if (clk) st->dbg[26] = clock64() - c0;)
     F2_STAMP(st, 21);
     // solved rest words U_l = sum over t of Linv[l][t] A12_t
     for (int i = tid; i < 64 * 16; i += kPT) {
@@ -738,7 +737,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->brow[leaf * 64 + F.step_c[l]] = base + l;
     }
     __syncthreads();
-    if (clk) st->dbg[27] = clock64() - c0;
+    F2_CLK(if (clk) st->dbg[27] = clock64() - c0;)
     F2_STAMP(st, 22);
     // pivot rows' slices: earlier leaf words as carried, the final leaf word, U
     for (int i = tid; i < kb * 16; i += kPT) {
@@ -797,7 +796,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         }
     }
     __syncthreads();
-    if (clk) st->dbg[21] = clock64() - c0;
+    F2_CLK(if (clk) st->dbg[21] = clock64() - c0;)
     return kb;
 }
 
@@ -843,10 +842,10 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
             const int j = static_cast<int>(leaf);
             const int pb = j & 1;
             if (state == S_FRESH || state == S_CARRY || state == S_FINAL) {
-                const long long cb = clock64();
+                F2_CLK(const long long cb = clock64();)
                 pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
                                   j == 0 ? 0 : st->pmap_hi);
-                if (pw0 == 0 && j == 2 && threadIdx.x == 0) st->dbg[22] = clock64() - cb;
+                F2_CLK(if (pw0 == 0 && j == 2 && threadIdx.x == 0) st->dbg[22] = clock64() - cb;)
                 F2_STAMP(st, 1);
                 if (state == S_FINAL) {
                     pipe_write_back(A, pw0, nwp, S, Z, pb);
@@ -911,10 +910,10 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
 #ifdef F2_PANEL_PROFILE
         if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = 0;
 #endif
-        const long long cbar = clock64();
+        F2_CLK(const long long cbar = clock64();)
         grid_barrier(bar, target);
-        if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 0) st->dbg[23] = clock64() - cbar;
-        if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 1) st->dbg[24] = clock64() - cbar;
+        F2_CLK(if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 0) st->dbg[23] = clock64() - cbar;)
+        F2_CLK(if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 1) st->dbg[24] = clock64() - cbar;)
     }
 #ifdef F2_TIMELINE
     if (threadIdx.x == 0) atomicMax(&st->tl[1][(pw0 / 16) & 127], gtimer());

@@ -1,3 +1,5 @@
+"""Phase clocks of the panel kernel (leaf 2 of the first panel).  Needs tools/libf2gpu_prof.so built with
+-DF2_PANEL_PROFILE -DF2_LEAF_CLOCKS (nvcc <flags of __graft_entry__> ... -o tools/libf2gpu_prof.so csrc/*.cu)."""
 import ctypes as C, sys
 sys.path.insert(0, ".")
 import paper_1006_1744_b200 as f2

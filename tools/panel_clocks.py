@@ -1,6 +1,6 @@
 """globaltimer stamps of k_panel_leaves (first panel, leaf 1) and the K1 internals.
-Needs tools/libf2gpu_prof.so built with -DF2_PANEL_PROFILE:
-  nvcc <NVCC_FLAGS of __graft_entry__> -DF2_PANEL_PROFILE -o tools/libf2gpu_prof.so paper_1006_1744_b200/csrc/*.cu"""
+Needs tools/libf2gpu_prof.so built with -DF2_PANEL_PROFILE -DF2_LEAF_CLOCKS:
+  nvcc <NVCC_FLAGS of __graft_entry__> -DF2_PANEL_PROFILE -DF2_LEAF_CLOCKS -o tools/libf2gpu_prof.so paper_1006_1744_b200/csrc/*.cu"""
 import ctypes as C
 import sys
 
