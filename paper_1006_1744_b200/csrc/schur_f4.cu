@@ -13,18 +13,19 @@
 //     one 16 KB block per (128-row tile, 256-K stage): a tile stage is one bulk copy.
 //   k_f4_expand_b: the pivot rows U12 gathered by the raw-column map (brow), 32x32
 //     bit blocks transposed by warp shuffles (the MMA wants B K-major too) and
-//     expanded; one 32 KB block per (256-column tile, K stage).
-//   k_schur_f4: persistent, one CTA per SM.  A CTA claims chunks of <= 32 consecutive
-//     tiles (column-tile major, so the CTA's B tile -- 128 KB, the whole K -- stays in
-//     SMEM across a chunk and is reloaded stage by stage while the last tile of the
-//     old column still computes).  Warp 1 streams A stages through a 4-deep ring
-//     (cp.async.bulk + mbarrier transaction counts), one thread of warp 0 issues 4
-//     MMAs of 128x256x64 per stage into a 256-column TMEM accumulator, and 16
-//     epilogue warps (4 per TMEM lane quarter, 64 columns each) read the counts,
-//     release the accumulator (the next tile's first MMA overwrites it), pack 64
-//     parities into a word by funnel shifts and XOR it into C.  Tiles and the chunk
-//     queue are data dependent (the row count comes from the panel snapshot), so no
-//     host sync is needed.
+//     expanded; one 28 KB block per (224-column tile, K stage).
+//   k_schur_f4: persistent, one CTA per SM.  A CTA claims chunks of consecutive tiles
+//     (column-tile major, so the CTA's B tile -- 112 KB, the whole K -- stays in SMEM
+//     across a chunk and is reloaded stage by stage behind the last MMAs on the old
+//     one; chunk size from the launch: k equal chunks of <= 64 tiles per CTA).  Warp 1
+//     streams A stages through a 6-deep ring (cp.async.bulk + mbarrier transaction
+//     counts); one elected lane of the converged warp 0 issues 4 MMAs of 128x224x64 per
+//     stage into one of two TMEM accumulators (2 x 224 columns + 64 scale-factor
+//     columns = all 512); 4 epilogue warps (one per TMEM lane quarter) read 32-column
+//     groups, release the buffer, pack parities by funnel shifts and XOR them into C
+//     with fire-and-forget RED.  Tiles and the chunk queue are data dependent (the row
+//     count comes from the panel snapshot), so no host sync is needed.  No runtime
+//     switch may sit in the issue, load or epilogue loops: a single one cost 5-9 %.
 #include <cstdint>
 #include <cstdlib>
 
@@ -205,7 +206,8 @@ struct F4Walk {
     }
 };
 
-// dbg: bits 16+ = tiles per claimed chunk (0: from the launch size; F2_F4_CHUNK)
+// dbg: bits 16+ = tiles per claimed chunk (0: from the launch size; F2_F4_CHUNK), bits 8-15 =
+// the largest chunk of the launch-size rule (0: 64; F2_F4_CHUNK_CAP)
 template <int kFRing, int EPW>
 __global__ void __launch_bounds__(f4_threads(EPW), 1)
 k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
@@ -229,10 +231,11 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
     const int64_t nhw = 2 * (cw1 - cw0);
     const int nrt = static_cast<int>((rows + kFM - 1) / kFM), nct = static_cast<int>((nhw + kFHW - 1) / kFHW);
     const int64_t T = static_cast<int64_t>(nrt) * nct;
-    // chunk: k = ceil(tiles per CTA / 32) chunks per CTA of equal size <= 32 (long runs on one
+    // chunk: k = ceil(tiles per CTA / cap) chunks per CTA of equal size <= cap (long runs on one
     // B tile, at most one tile of imbalance when the grid divides the work evenly)
     const int64_t per_cta = (T + gridDim.x - 1) / gridDim.x;
-    const int64_t kch = (per_cta + 31) / 32;
+    const int cap = (dbg >> 8) & 255 ? (dbg >> 8) & 255 : 64;
+    const int64_t kch = (per_cta + cap - 1) / cap;
     int chunk = static_cast<int>((T + gridDim.x * kch - 1) / (gridDim.x * kch));
     if (dbg >> 16) chunk = dbg >> 16;
     const int64_t nchunks = (T + chunk - 1) / chunk;
@@ -427,7 +430,7 @@ size_t schur_f4_b_bytes(int64_t words) {
     return static_cast<size_t>((2 * words + kFHW - 1) / kFHW) * kFMaxStages * kFBStage;
 }
 
-int g_f4_ring = 6, g_f4_dbg = 0, g_f4_epw = 4;
+int g_f4_ring = 6, g_f4_dbg = 0, g_f4_epw = 1;
 bool g_pdl = !std::getenv("F2_NO_PDL");  // kernels.cuh: launch_pdl
 
 // K is always padded to kFMaxStages stages (zero nibbles): the B ring then spans exactly
@@ -462,6 +465,7 @@ void setup_schur_f4_kernels() {
     cudaFuncSetAttribute(k_schur_f4<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
     if (const char* e = std::getenv("F2_F4_EPW")) g_f4_epw = std::atoi(e);
     if (const char* e = std::getenv("F2_F4_CHUNK")) g_f4_dbg |= std::atoi(e) << 16;
+    if (const char* e = std::getenv("F2_F4_CHUNK_CAP")) g_f4_dbg |= (std::atoi(e) & 255) << 8;
     if (const char* e = std::getenv("F2_F4_RING")) g_f4_ring = std::atoi(e);
 }
 
