@@ -70,6 +70,7 @@ struct Ctx {
     bool lookahead = true;    // F2_NO_LOOKAHEAD=1 disables
     int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
     int side_ctas_late = 48;  // F2_SIDE_CTAS_LATE: the second half of the factorisation (0: same)
+    int late_pct = 38;        // F2_LATE_PCT: where the "late" schedule starts (% of the panels)
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
     cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
@@ -151,6 +152,7 @@ int ensure_init() {
     g.pipe = !(std::getenv("F2_NO_PIPE") && std::getenv("F2_NO_PIPE")[0] == '1');
     g.lookahead = !(std::getenv("F2_NO_LOOKAHEAD") && std::getenv("F2_NO_LOOKAHEAD")[0] == '1');
     if (const char* e = std::getenv("F2_SIDE_CTAS_LATE")) g.side_ctas_late = std::atoi(e);
+    if (const char* e = std::getenv("F2_LATE_PCT")) g.late_pct = std::atoi(e);
     if (const char* e = std::getenv("F2_SIDE_CTAS")) {
         const int v = std::atoi(e);
         if (v >= 2 && v <= g.nsm) g.side_ctas = v;
@@ -490,7 +492,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 evmark(s, "snapshot", pi);
                 // while the trailing update dominates (the first ~45 % of the panels), the wide
                 // TRSM (disjoint columns) runs beside the narrow one instead of after the fork
-                const bool late = 20 * (pi + 1) >= 9 * npanels;
+                const bool late = 100 * (pi + 1) >= g.late_pct * npanels;
                 const bool wide_early = !late && g.early_wide_trsm && npw1 < nw;
                 if (wide_early) {
                     CK(cudaEventRecord(g.tw_fork, s));
