@@ -3,7 +3,7 @@
 import ctypes as C, sys
 sys.path.insert(0, ".")
 import paper_1006_1744_b200 as f2
-L = f2.load_library("tools/libf2gpu_prof.so")
+L = f2.load_library(sys.argv[1] if len(sys.argv) > 1 else "tools/libf2gpu_prof.so")
 L.f2_debug_clocks.argtypes = [C.POINTER(C.c_longlong), C.c_int]
 for m, n in [(65536, 2048), (16384, 2048)]:
     a = f2.DeviceMatrix(m, n); a.randomize(0.5, 7)
