@@ -158,7 +158,8 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     dist = None
-    if ws > 1:
+    sharded = ws > 1 or args.sharded
+    if sharded:
         import torch
         import torch.distributed as dist_mod
 
@@ -169,7 +170,7 @@ def run_ours(args):
     import paper_1006_1744_b200 as f2
 
     f2.set_device(local)
-    if ws > 1:
+    if sharded:
         return run_sharded(args, f2, dist, ws, rank, local)
     cfg = f2.EliminationConfig(cutoff_bytes=CUTOFF)
     a0 = f2.DeviceMatrix(N, N)
@@ -383,6 +384,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sharded", action="store_true",
+                    help="the column-sharded NCCL schedule even at one rank (exercises the N > 1 path)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -178,3 +178,39 @@ def test_sharded_gpu_emulated(f2, oracle, world, m, n, W):
     f2._check(f2.load_library().f2_pls_compress(g.handle, res.rank, pc.ctypes.data_as(
         __import__("ctypes").POINTER(__import__("ctypes").c_uint64))))
     assert (g.download() == w).all()
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_world1(f2, oracle):
+    """The N > 1 code path of bench.py (pls_sharded with TorchComm over NCCL and GpuOps)
+    at world size 1, one process on the box's GPU: the real NCCL broadcast of the header
+    and panel words, checked against the Gaussian oracle."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_1006_1744_b200 import dist as D
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        m, n, W = 1500, 2300, 512
+        a = oracle.randomize(m, n, 0.5, 77)
+        d = f2.DeviceMatrix.from_host(D.split_columns(a, n, 0, 1, W), D.local_ncols(0, 1, n, W))
+        res = D.pls_sharded(D.GpuOps(f2), D.TorchComm(), d, m, n, W, 0, 1)
+        w, p, q, r = oracle.gauss_pls(a, n)
+        assert res.rank == r and (res.P == p).all() and (res.pivcols == q[:r]).all()
+        got = D.gather([d.download()], m, n, W)
+        g = f2.DeviceMatrix.from_host(got, n)
+        import ctypes as C
+        L = f2.load_library()
+        L.f2_pls_compress.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        pc = np.ascontiguousarray(res.pivcols)
+        f2._check(L.f2_pls_compress(g.handle, res.rank, pc.ctypes.data_as(C.POINTER(C.c_uint64))))
+        assert (g.download() == w).all()
+    finally:
+        dist.destroy_process_group()
