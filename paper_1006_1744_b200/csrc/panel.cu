@@ -362,12 +362,15 @@ __device__ void update_tile(const Mat& A, int64_t wl, int64_t pw1, const int64_t
         for (int j = 0; j < 4; ++j) w0[j] = c[j];
     }
     F2_STAMP(st, 51);
+    // lanes whose words lie right of the panel read their row's first entry instead: the
+    // same address as lane wp = 0, so the lookup costs no extra shared-memory wavefront
+    const int wpa = h0 ? wp : 0;
 #pragma unroll
     for (int g4 = 0; g4 < 16; ++g4) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const unsigned e = static_cast<unsigned>(c[j] >> (4 * g4)) & 15u;
-            const uint4 v = lds128(T4 + (g4 * 16 + e) * kW + 2 * wp);
+            const uint4 v = lds128(T4 + (g4 * 16 + e) * kW + 2 * wpa);
             w0[j] ^= static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
             w1[j] ^= static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w) << 32);
         }
