@@ -222,15 +222,17 @@ def run_ours(args):
     schur = fam[0]
     total_fam_ms = sum(x["ms"] for x in fam)
     achieved = schur["bitops"] / (schur["ms"] / 1e3) / 1e12 if schur["ms"] else 0.0
-    mma_peak = F4_MMA_PEAK_TFLOPS
+    nominal = 9000.0  # fp4 dense, B200_PROFILING.md (MEASURED_PEAKS.json has no fp4 figure)
     roofline = {"kernel": "k_schur_f4 (Schur complement C ^= L21*U12 on tcgen05 kind::mxf4, + operand expansion)",
-                "bound": "tensor", "achieved": achieved, "peak": mma_peak, "unit": "TFLOP/s",
-                "frac": achieved / mma_peak,
-                "peak_source": "measured: tcgen05.mma kind::mxf4 128x224x64 issue rate with SMEM-resident operands, "
-                               "148 SMs at 1965 MHz (tools/micro/umma_f4, profiles/r1_umma_f4_peak.txt); "
-                               "MEASURED_PEAKS.json has no fp4 figure (4 x its bf16 burst = %.0f; nominal fp4 dense "
-                               "9000)" % (4 * PEAKS.get("bf16_tflops", 0.0)),
-                "frac_of_nominal_fp4": achieved / 9000.0,
+                "bound": "tensor", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                "frac": achieved / nominal,
+                "peak_source": "nominal fp4 dense 9 PFLOP/s (B200_PROFILING.md table; MEASURED_PEAKS.json has no fp4 "
+                               "figure; 4 x its bf16 burst = %.0f)" % (4 * PEAKS.get("bf16_tflops", 0.0)),
+                "measured_mma_ceiling": F4_MMA_PEAK_TFLOPS,
+                "frac_of_measured_mma_ceiling": achieved / F4_MMA_PEAK_TFLOPS,
+                "measured_mma_ceiling_source": "tcgen05.mma kind::mxf4 128x224x64 issue rate with SMEM-resident "
+                                               "operands on 148 SMs at 1965 MHz (tools/micro/umma_f4, "
+                                               "profiles/r1_umma_f4_peak.txt)",
                 "unit_note": "1 GF(2) bit-op = 1 fp4 flop: each AND-count term is one MMA multiply-add",
                 "share_of_step": schur["ms"] / total_fam_ms if total_fam_ms else None,
                 "launches": schur["launches"], "avg_launch_ms": schur["ms"] / max(schur["launches"], 1),
@@ -243,7 +245,7 @@ def run_ours(args):
                                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         roofline["traffic_note"] = ("dram read+write bytes of the first wide k_schur_f4 launch of config 3 "
                                     "(ncu --set full, profiles/r1_ncu_schur_f4_config3_raw.json); its algorithmic "
-                                    "bytes (C read+write once) are %.4g" % (64512 * 64512 / 8 * 2))
+                                    "bytes (C read+write once) are %.4g" % (64512 * 63488 / 8 * 2))
 
     # --- MMPF table-apply (k_mmpf_apply, K <= 64) over a 1 GiB trailing matrix: the HBM-bound
     # kernel of the flat MMPF; K = 8 is the paper's single 2^8 table, K = 64 the engine's MMPF panel
