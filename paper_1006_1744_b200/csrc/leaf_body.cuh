@@ -365,31 +365,43 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     for (int phase = 0; phase < 2; ++phase) {
         const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32;
         if (w == phase) {
-            // select the pivots of columns c0 .. c1-1
+            // select the pivots of columns c0 .. c1-1.  Branch-free: a column without a
+            // pivot (or any column after one the window cannot decide) is a masked no-op
+            // step, so the chain from one shuffle to the next has no convergence points
+            bool bad = false;
             for (int c = c0; c < c1; ++c) {
                 const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
                 const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
                 const uint64_t clo = mlo & (~0ull << t);
-                if ((clo | mhi) == 0) {
-                    if (more) {
-                        ok = false;
-                        break;
-                    }
-                    continue;
-                }
+                const bool zero = (clo | mhi) == 0;
+                bad = bad || (zero && more);  // rows past the window could hold the pivot
+                const bool act = !zero && !bad;
                 const int p = clo ? __ffsll(static_cast<long long>(clo)) - 1 : 63 + __ffsll(static_cast<long long>(mhi));
-                const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
-                const uint64_t elo = (mlo & ~plo) & (t == 63 ? 0ull : (~0ull << (t + 1)));
-                const uint64_t ehi = mhi & ~phi;
-                apply(t, p, elo, ehi, col > c);
+                const uint64_t keep = act ? ~0ull : 0ull;
+                const uint64_t plo = (p < 64 ? (1ull << (p & 63)) : 0ull) & keep;
+                const uint64_t phi = (p < 64 ? 0ull : (1ull << ((p - 64) & 63))) & keep;
+                const uint64_t elo = (mlo & ~plo) & (t == 63 ? 0ull : (~0ull << (t + 1))) & keep;
+                const uint64_t ehi = mhi & ~phi & keep;
+                {  // apply(t, p, elo, ehi, col > c) with every mask gated by act
+                    const uint64_t tb = (1ull << t) & keep;
+                    const uint64_t d = (((C.lo & tb) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
+                    C.lo ^= d & (tb | plo);
+                    C.hi ^= d & phi;
+                    const bool a = col > c && (C.lo & tb);
+                    C.lo ^= a ? elo : 0ull;
+                    C.hi ^= a ? ehi : 0ull;
+                }
+                // (a no-op step writes slot t, which the next real step overwrites; readers
+                // only read below the published count)
                 F.step_p[t] = p;
                 F.step_c[t] = c;
                 F.step_e[t][0] = elo;
                 F.step_e[t][1] = ehi;
-                ++t;
+                t += act ? 1 : 0;
                 // every lane stored the same step and releases the same count: no branch
                 asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
             }
+            ok = ok && !bad;
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
