@@ -131,13 +131,16 @@ struct FastSmem {
     int wcount[4];
     int final_kb;                // -1: fell back
     // two-warp search: published steps (the selecting warp writes, the other replays)
-    uint64_t step_e[64][2];
+    ulonglong2 step_m[64];       // step t's candidate mask: the pivot column's bits at slots >= t
     uint32_t ufl[64], ufh[64];   // pivot rows' leaf words, columns 0-31 / 32-63
     uint64_t fbas[64];           // finalize basis
     uint64_t cfin[64];           // post-search column masks, slots 0..63 (bit l = row l's bit in column c)
     uint32_t ainv[32], brows[32];
     volatile int q_n;            // steps published
     volatile int q_done[2];      // warp w finished selecting: its final step count, -1 when undecidable
+#ifdef F2_LEAF_CLOCKS
+    long long clk[2][2];         // selecting loop start / end per phase
+#endif
 };
 
 // Warp 0: the column-form pivot rule on F.colw (leaf columns as 128-slot masks).
@@ -321,9 +324,12 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
         F.q_done[1] = -2;
     }
     asm volatile("bar.sync 1, 96;\n" ::: "memory");
-    auto apply = [&](int t, int p, uint64_t elo, uint64_t ehi, bool xr) {
+    // step t from its candidate mask m: the pivot is m's lowest bit, the rows to
+    // eliminate are m's other bits (all below slot t after the swap)
+    auto apply = [&](int t, ulonglong2 m, bool xr) {
         const uint64_t tb = 1ull << t;
-        const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
+        const uint64_t plo = m.x & (0ull - m.x), phi = m.x ? 0ull : (m.y & (0ull - m.y));
+        const uint64_t elo = m.x ^ plo, ehi = m.y ^ phi;
         const uint64_t d = (((C.lo & tb) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
         C.lo ^= d & (tb | plo);
         C.hi ^= d & phi;
@@ -341,11 +347,11 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(n) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
                 const int dn = F.q_done[phase];
                 __threadfence_block();
-                for (; t < n; ++t) apply(t, F.step_p[t], 0ull, 0ull, false);
+                for (; t < n; ++t) apply(t, F.step_m[t], false);
                 if (dn != -2) {
                     if (dn < 0) ok = false;
                     else
-                        for (; t < dn; ++t) apply(t, F.step_p[t], 0ull, 0ull, false);
+                        for (; t < dn; ++t) apply(t, F.step_m[t], false);
                     break;
                 }
 #ifdef F2_POLL_SLEEP
@@ -369,39 +375,40 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
             // pivot (or any column after one the window cannot decide) is a masked no-op
             // step, so the chain from one shuffle to the next has no convergence points
             bool bad = false;
+            F2_CLK(if (lane == 0) F.clk[phase][0] = clock64();)
+            uint64_t tb = 1ull << t, tm = ~0ull << t;  // slot t, slots >= t
             for (int c = c0; c < c1; ++c) {
                 const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
                 const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
-                const uint64_t clo = mlo & (~0ull << t);
-                const bool zero = (clo | mhi) == 0;
+                // candidates: slots >= t; the pivot is the lowest (as a bit: x & -x), the
+                // rows to eliminate the others.  Every quantity is masked, none branched on,
+                // and the pivot's index is left to the readers of the candidate mask.
+                const uint64_t clo = mlo & tm;
+                const bool nzlo = clo != 0, zero = !nzlo && mhi == 0;
                 bad = bad || (zero && more);  // rows past the window could hold the pivot
-                const bool act = !zero && !bad;
-                const int p = clo ? __ffsll(static_cast<long long>(clo)) - 1 : 63 + __ffsll(static_cast<long long>(mhi));
-                const uint64_t keep = act ? ~0ull : 0ull;
-                const uint64_t plo = (p < 64 ? (1ull << (p & 63)) : 0ull) & keep;
-                const uint64_t phi = (p < 64 ? 0ull : (1ull << ((p - 64) & 63))) & keep;
-                const uint64_t elo = (mlo & ~plo) & (t == 63 ? 0ull : (~0ull << (t + 1))) & keep;
-                const uint64_t ehi = mhi & ~phi & keep;
-                {  // apply(t, p, elo, ehi, col > c) with every mask gated by act
-                    const uint64_t tb = (1ull << t) & keep;
-                    const uint64_t d = (((C.lo & tb) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
-                    C.lo ^= d & (tb | plo);
+                const uint64_t plo = clo & (0ull - clo), phi = nzlo ? 0ull : (mhi & (0ull - mhi));
+                const uint64_t elo = clo ^ plo, ehi = mhi ^ phi;
+                const uint64_t tz = zero ? 0ull : tb;
+                {  // apply step t to this lane's column (a no-op when zero)
+                    const uint64_t d = (((C.lo & tz) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
+                    C.lo ^= d & (tz | plo);
                     C.hi ^= d & phi;
-                    const bool a = col > c && (C.lo & tb);
+                    const bool a = col > c && (C.lo & tz);
                     C.lo ^= a ? elo : 0ull;
                     C.hi ^= a ? ehi : 0ull;
                 }
                 // (a no-op step writes slot t, which the next real step overwrites; readers
                 // only read below the published count)
-                F.step_p[t] = p;
+                F.step_m[t] = make_ulonglong2(clo, mhi);
                 F.step_c[t] = c;
-                F.step_e[t][0] = elo;
-                F.step_e[t][1] = ehi;
-                t += act ? 1 : 0;
+                t += zero ? 0 : 1;
+                tb = zero ? tb : tb << 1;
+                tm = zero ? tm : tm << 1;
                 // every lane stored the same step and releases the same count: no branch
                 asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
             }
             ok = ok && !bad;
+            F2_CLK(if (lane == 0) F.clk[phase][1] = clock64();)
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -415,11 +422,11 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 const int dn = F.q_done[phase];
                 __threadfence_block();
                 for (; t < n; ++t)
-                    apply(t, F.step_p[t], F.step_e[t][0], F.step_e[t][1], w > phase);
+                    apply(t, F.step_m[t], w > phase);
                 if (dn != -2) {
                     if (dn < 0) ok = false;
                     else
-                        for (; t < dn; ++t) apply(t, F.step_p[t], F.step_e[t][0], F.step_e[t][1], w > phase);
+                        for (; t < dn; ++t) apply(t, F.step_m[t], w > phase);
                     break;
                 }
 #ifdef F2_POLL_SLEEP
@@ -431,6 +438,10 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     }
     if (lane == 0 && w == 0) F.final_kb = ok ? t : -1;
     if (w < 2) F.cfin[col] = C.lo;
+    if (ok && w < 2 && col < t) {  // pivot slot of every step, from its candidate mask
+        const ulonglong2 m = F.step_m[col];
+        F.step_p[col] = m.x ? __ffsll(static_cast<long long>(m.x)) - 1 : 63 + __ffsll(static_cast<long long>(m.y));
+    }
     if (ok && w < 2) {
         // pivot rows' final leaf words (slots 0..63), this warp's 32 columns
         const uint32_t r0 = warp_transpose32(static_cast<uint32_t>(C.lo), lane);

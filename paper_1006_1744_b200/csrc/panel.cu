@@ -613,7 +613,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     if (warp < 3) two_warp_pivots(F, lw, base + kPW < m, false);
 #endif
     __syncthreads();
-    F2_CLK(if (clk) st->dbg[20] = clock64() - c0;)
+    F2_CLK(if (clk) { st->dbg[20] = clock64() - c0; st->dbg[29] = F.clk[0][1] - F.clk[0][0]; st->dbg[31] = F.clk[1][1] - F.clk[1][0]; })
     F2_STAMP(st, 18);
     const int kb = F.final_kb;
     if (kb < 0) return -1;
