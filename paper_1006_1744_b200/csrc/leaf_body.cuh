@@ -105,6 +105,11 @@ struct U128 {
     uint64_t lo, hi;
 };
 
+// (nlo, nhi) = -(lo, hi) as one 128-bit two's complement (one carry chain)
+__device__ __forceinline__ void neg128(uint64_t lo, uint64_t hi, uint64_t& nlo, uint64_t& nhi) {
+    asm("sub.cc.u64 %0, 0, %2;\n\tsubc.u64 %1, 0, %3;\n" : "=l"(nlo), "=l"(nhi) : "l"(lo), "l"(hi));
+}
+
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
     // lane i holds bits (i, 0..31) -> lane j holds bits (0..31, j)
     uint32_t m = 0x0000FFFFu;
@@ -372,21 +377,25 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
         const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32;
         if (w == phase) {
             // select the pivots of columns c0 .. c1-1.  Branch-free: a column without a
-            // pivot (or any column after one the window cannot decide) is a masked no-op
-            // step, so the chain from one shuffle to the next has no convergence points
-            bool bad = false;
+            // pivot is a masked no-op step, so the chain from one shuffle to the next has
+            // no convergence points (after a column the window cannot decide the later
+            // steps still run, and the leaf is discarded)
+            const int t0 = t;
             F2_CLK(if (lane == 0) F.clk[phase][0] = clock64();)
             uint64_t tb = 1ull << t, tm = ~0ull << t;  // slot t, slots >= t
             for (int c = c0; c < c1; ++c) {
                 const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
                 const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
-                // candidates: slots >= t; the pivot is the lowest (as a bit: x & -x), the
-                // rows to eliminate the others.  Every quantity is masked, none branched on,
-                // and the pivot's index is left to the readers of the candidate mask.
+                // candidates: slots >= t; the pivot is the lowest (as a bit: x & -x over
+                // the 128-bit mask), the rows to eliminate the others.  Every quantity is
+                // masked, none branched on, and the pivot's index is left to the readers of
+                // the candidate mask.
                 const uint64_t clo = mlo & tm;
-                const bool nzlo = clo != 0, zero = !nzlo && mhi == 0;
-                bad = bad || (zero && more);  // rows past the window could hold the pivot
-                const uint64_t plo = clo & (0ull - clo), phi = nzlo ? 0ull : (mhi & (0ull - mhi));
+                uint64_t plo, phi;
+                neg128(clo, mhi, plo, phi);
+                plo &= clo;
+                phi &= mhi;
+                const bool zero = (plo | phi) == 0;
                 const uint64_t elo = clo ^ plo, ehi = mhi ^ phi;
                 const uint64_t tz = zero ? 0ull : tb;
                 {  // apply step t to this lane's column (a no-op when zero)
@@ -407,7 +416,8 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 // every lane stored the same step and releases the same count: no branch
                 asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
             }
-            ok = ok && !bad;
+            // a column without candidates is undecidable when rows past the window could hold them
+            ok = ok && !(more && t - t0 < c1 - c0);  // (c1 < c0 for narrow leaves)
             F2_CLK(if (lane == 0) F.clk[phase][1] = clock64();)
             __syncwarp();
             if (lane == 0) {
