@@ -383,6 +383,7 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
             const int t0 = t;
             F2_CLK(if (lane == 0) F.clk[phase][0] = clock64();)
             uint64_t tb = 1ull << t, tm = ~0ull << t;  // slot t, slots >= t
+#pragma unroll 2
             for (int c = c0; c < c1; ++c) {
                 const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
                 const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
