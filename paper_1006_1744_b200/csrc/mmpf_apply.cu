@@ -15,6 +15,7 @@
 // when its run crosses a column tile.  Rows and the row start come from the device
 // (TableApply row modes), so the launch needs no host sync.
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "f2gpu.cuh"
@@ -32,21 +33,27 @@ __device__ __forceinline__ uint4 xor4m(uint4 a, uint4 b) { return make_uint4(a.x
 
 }  // namespace
 
-// TW: words per column tile, 64 / ntab (ntab = tables rounded up to a power of two), so
-// the tables always take 128 KB: K <= 8 streams 512-byte row segments (4 lines, one DRAM
-// page), K <= 64 64-byte ones.  Tiles are aligned to absolute multiples of TW words, so
-// every full 16-byte access is aligned; words of a tile outside [cw0, cw1) are neither
-// read nor written.
-template <int TW>
+// TW: words per column tile; NB: coefficient bits per table (2^NB entries).  The tables take
+// 128 KB: with 8-bit tables TW = 64 / ntab (ntab rounded up to a power of two), so K <= 8
+// streams 512-byte row segments (4 lines, one DRAM page) and K <= 32 128-byte ones.  For
+// 32 < K <= 44 up to 11 4-bit tables at TW = 64 (512-byte segments again) beat 8-bit
+// tables at 64-byte segments (K = 33: 2.77 vs 2.32 TB/s over a 1 GiB C); from K = 48 on
+// the 4-bit lookups (up to 16 per row) cost more than the short segments (K = 64: 1.85 vs
+// 2.05 TB/s), so K > 44 keeps 8-bit tables at TW = 8.  Tiles are aligned to
+// absolute multiples of TW words, so every full 16-byte access is aligned; words of a tile
+// outside [cw0, cw1) are neither read nor written.
+template <int TW, int NB>
 __global__ void __launch_bounds__(kMThreads) k_mmpf_apply(TableApply p, int ntab) {
     constexpr int LPR = TW / 2;               // lanes per row (16 bytes each)
     constexpr int RPI = 32 / LPR;             // rows per warp instruction
     constexpr int U = kMGroups;               // row groups in flight
-    using coef_t = typename std::conditional<TW >= 16, uint32_t, uint64_t>::type;  // K <= 32: 32-bit coefficients
-    constexpr int KB = 8 * (64 / TW);         // B rows the tables cover
+    constexpr int E = 1 << NB;                // entries per table
+    constexpr int NT = 16384 / (E * TW);      // tables that fit 128 KB
+    constexpr int KB = NB * NT;               // B rows the tables cover
+    using coef_t = typename std::conditional<KB <= 32, uint32_t, uint64_t>::type;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* Bs = reinterpret_cast<uint64_t*>(smem);             // [KB][TW] B rows of the tile
-    uint4* T = reinterpret_cast<uint4*>(smem + KB * TW * 8);      // [ntab][256][LPR] uint4
+    uint4* T = reinterpret_cast<uint4*>(smem + KB * TW * 8);      // [ntab][E][LPR] uint4
 
     int64_t c_r0 = p.c_r0, a_r0 = p.a_r0;
     if (p.row_mode == ROWS_AFTER_LEAF) {
@@ -85,15 +92,15 @@ __global__ void __launch_bounds__(kMThreads) k_mmpf_apply(TableApply p, int ntab
                 }
                 Bs[e] = v;
             }
-            // subset sums by doubling: entries [2^b, 2^(b+1)) of table t = entries [0, 2^b) ^ B row 8t + b
-            for (int e = tid; e < ntab * LPR; e += kMThreads) T[(e / LPR) * 256 * LPR + e % LPR] = make_uint4(0, 0, 0, 0);
-            for (int b = 0; b < 8; ++b) {
+            // subset sums by doubling: entries [2^b, 2^(b+1)) of table t = entries [0, 2^b) ^ B row NB*t + b
+            for (int e = tid; e < ntab * LPR; e += kMThreads) T[(e / LPR) * E * LPR + e % LPR] = make_uint4(0, 0, 0, 0);
+            for (int b = 0; b < NB; ++b) {
                 __syncthreads();
                 const int half = 1 << b, n = ntab * half * LPR;
                 for (int e = tid; e < n; e += kMThreads) {
                     const int q = e % LPR, v = (e / LPR) % half, t = e / (half * LPR);
-                    const uint4 brow4 = reinterpret_cast<const uint4*>(Bs)[(8 * t + b) * LPR + q];
-                    T[(t * 256 + half + v) * LPR + q] = xor4m(T[(t * 256 + v) * LPR + q], brow4);
+                    const uint4 brow4 = reinterpret_cast<const uint4*>(Bs)[(NB * t + b) * LPR + q];
+                    T[(t * E + half + v) * LPR + q] = xor4m(T[(t * E + v) * LPR + q], brow4);
                 }
             }
             cur_ct = ct;
@@ -131,8 +138,8 @@ __global__ void __launch_bounds__(kMThreads) k_mmpf_apply(TableApply p, int ntab
             for (int u = 0; u < U; ++u) {
                 if (row0 + u * RPI >= rhi) continue;
                 coef_t x = a[u];
-                for (int t = 0; t < ntab && x; ++t, x >>= 8)
-                    if (x & 255) c[u] = xor4m(c[u], T[(t * 256 + static_cast<int>(x & 255)) * LPR + sub]);
+                for (int t = 0; t < ntab && x; ++t, x >>= NB)
+                    if (x & (E - 1)) c[u] = xor4m(c[u], T[(t * E + static_cast<int>(x & (E - 1))) * LPR + sub]);
                 uint64_t* cp = cp0 + u * cstep;
                 if (vlo && vhi) {
                     *reinterpret_cast<uint4*>(cp) = c[u];
@@ -147,27 +154,39 @@ __global__ void __launch_bounds__(kMThreads) k_mmpf_apply(TableApply p, int ntab
 }
 
 namespace {
-template <int TW>
-constexpr size_t mmpf_smem() { return static_cast<size_t>(8 * (64 / TW)) * TW * 8 + static_cast<size_t>(64 / TW) * 256 * TW * 8; }
-template <int TW>
-void launch_tw(cudaStream_t s, const TableApply& t, int nsm, int ntab) {
-    k_mmpf_apply<TW><<<nsm, kMThreads, mmpf_smem<TW>(), s>>>(t, ntab);
+template <int TW, int NB>
+constexpr size_t mmpf_smem() {
+    constexpr int E = 1 << NB, NT = 16384 / (E * TW);
+    return static_cast<size_t>(NB * NT) * TW * 8 + static_cast<size_t>(NT) * E * TW * 8;
 }
+template <int TW, int NB>
+void launch_tw(cudaStream_t s, const TableApply& t, int nsm, int ntab) {
+    k_mmpf_apply<TW, NB><<<nsm, kMThreads, mmpf_smem<TW, NB>(), s>>>(t, ntab);
+}
+template <int TW, int NB>
+void setup_tw() {
+    cudaFuncSetAttribute(k_mmpf_apply<TW, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(mmpf_smem<TW, NB>()));
+}
+bool g_mmpf_nb8 = false;  // F2_MMPF_NB8=1: 32 < K <= 44 with 8-bit tables too (comparison)
 }  // namespace
 
 void launch_mmpf_apply(cudaStream_t s, const TableApply& t, int nsm) {
     const int ntab = static_cast<int>((t.kbits + 7) / 8);
-    if (ntab <= 1) launch_tw<64>(s, t, nsm, ntab);
-    else if (ntab <= 2) launch_tw<32>(s, t, nsm, ntab);
-    else if (ntab <= 4) launch_tw<16>(s, t, nsm, ntab);
-    else launch_tw<8>(s, t, nsm, ntab);
+    if (ntab <= 1) launch_tw<64, 8>(s, t, nsm, ntab);
+    else if (ntab <= 2) launch_tw<32, 8>(s, t, nsm, ntab);
+    else if (ntab <= 4) launch_tw<16, 8>(s, t, nsm, ntab);
+    else if (t.kbits <= 44 && !g_mmpf_nb8) launch_tw<64, 4>(s, t, nsm, static_cast<int>((t.kbits + 3) / 4));
+    else launch_tw<8, 8>(s, t, nsm, ntab);
 }
 
 void setup_mmpf_apply_kernels() {
-    cudaFuncSetAttribute(k_mmpf_apply<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mmpf_smem<64>()));
-    cudaFuncSetAttribute(k_mmpf_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mmpf_smem<32>()));
-    cudaFuncSetAttribute(k_mmpf_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mmpf_smem<16>()));
-    cudaFuncSetAttribute(k_mmpf_apply<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mmpf_smem<8>()));
+    setup_tw<64, 8>();
+    setup_tw<32, 8>();
+    setup_tw<16, 8>();
+    setup_tw<8, 8>();
+    setup_tw<64, 4>();
+    if (const char* e = std::getenv("F2_MMPF_NB8")) g_mmpf_nb8 = std::atoi(e) != 0;
 }
 
 }  // namespace f2g

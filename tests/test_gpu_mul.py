@@ -48,10 +48,11 @@ def test_mul_m4rm_vs_reference(f2, oracle):
         assert (got == oracle.mul(a, s, b, n)).all(), (m, s, n)
 
 
-@pytest.mark.parametrize("k", [1, 8, 9, 33, 64])
+@pytest.mark.parametrize("k", [1, 8, 9, 33, 44, 45, 64])
 def test_addmul_mmpf_streaming_kernel(f2, oracle, k):
     """K <= 64 takes the HBM-streaming MMPF table-apply: every table count (1-8 8-bit tables,
-    4096- to 512-bit tiles), a C window starting at an odd word, rows across 2048-row blocks."""
+    4096- to 512-bit tiles; 9-11 4-bit tables at 4096-bit tiles for 32 < K <= 44), a C window
+    starting at an odd word, rows across 2048-row blocks."""
     rng = np.random.default_rng(k)
     p, q, c0 = 4500, 5000, 64 * 3
     a, b = rand_words(rng, p, k), rand_words(rng, k, q)
