@@ -141,8 +141,7 @@ struct FastSmem {
     uint64_t fbas[64];           // finalize basis
     uint64_t cfin[64];           // post-search column masks, slots 0..63 (bit l = row l's bit in column c)
     uint32_t ainv[32], brows[32];
-    volatile int q_n;            // steps published
-    volatile int q_done[2];      // warp w finished selecting: its final step count, -1 when undecidable
+    volatile int q_n;            // published progress: (columns processed << 8) | steps
 #ifdef F2_LEAF_CLOCKS
     long long clk[2][2];         // selecting loop start / end per phase
 #endif
@@ -325,8 +324,6 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     }
     if (threadIdx.x == 0) {
         F.q_n = 0;
-        F.q_done[0] = -2;
-        F.q_done[1] = -2;
     }
     asm volatile("bar.sync 1, 96;\n" ::: "memory");
     // step t from its candidate mask m: the pivot is m's lowest bit, the rows to
@@ -342,26 +339,27 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
         C.lo ^= a ? elo : 0ull;
         C.hi ^= a ? ehi : 0ull;
     };
+    // The selecting warp releases (columns processed << 8) | steps after every column; a
+    // replaying warp applies the steps it sees and knows the phase is over when the column
+    // count reaches the phase's end (and whether it was decidable from the step count).
+    auto progress = [&]() {
+        unsigned v;
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
+        return v;
+    };
     int t = 0;
     bool ok = true;
     if (w == 2) {
         for (int phase = 0; phase < 2 && ok; ++phase) {
             if (32 * phase >= lw) break;
+            const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32, t0 = t;
             while (true) {
-                int n;
-                asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(n) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
-                const int dn = F.q_done[phase];
-                __threadfence_block();
-                for (; t < n; ++t) apply(t, F.step_m[t], false);
-                if (dn != -2) {
-                    if (dn < 0) ok = false;
-                    else
-                        for (; t < dn; ++t) apply(t, F.step_m[t], false);
+                const unsigned v = progress();
+                for (; t < static_cast<int>(v & 255u); ++t) apply(t, F.step_m[t], false);
+                if (static_cast<int>(v >> 8) >= c1) {
+                    ok = ok && !(more && t - t0 < c1 - c0);
                     break;
                 }
-#ifdef F2_POLL_SLEEP
-                __nanosleep(F2_POLL_SLEEP);
-#endif
             }
         }
         if (ok) {
@@ -414,35 +412,22 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 t += zero ? 0 : 1;
                 tb = zero ? tb : tb << 1;
                 tm = zero ? tm : tm << 1;
-                // every lane stored the same step and releases the same count: no branch
-                asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(t) : "memory");
+                // every lane stored the same step and releases the same word: no branch
+                asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(static_cast<unsigned>(((c + 1) << 8) | t)) : "memory");
             }
             // a column without candidates is undecidable when rows past the window could hold them
             ok = ok && !(more && t - t0 < c1 - c0);  // (c1 < c0 for narrow leaves)
             F2_CLK(if (lane == 0) F.clk[phase][1] = clock64();)
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                F.q_done[phase] = ok ? t : -1;
-            }
         } else if (c0 < lw) {
             // replay the other warp's steps as they are published
+            const int t0 = t;
             while (true) {
-                int n;
-                asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(n) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
-                const int dn = F.q_done[phase];
-                __threadfence_block();
-                for (; t < n; ++t)
-                    apply(t, F.step_m[t], w > phase);
-                if (dn != -2) {
-                    if (dn < 0) ok = false;
-                    else
-                        for (; t < dn; ++t) apply(t, F.step_m[t], w > phase);
+                const unsigned v = progress();
+                for (; t < static_cast<int>(v & 255u); ++t) apply(t, F.step_m[t], w > phase);
+                if (static_cast<int>(v >> 8) >= c1) {
+                    ok = ok && !(more && t - t0 < c1 - c0);
                     break;
                 }
-#ifdef F2_POLL_SLEEP
-                __nanosleep(F2_POLL_SLEEP);
-#endif
             }
         }
         if (!ok) break;
