@@ -48,13 +48,14 @@ def test_mul_m4rm_vs_reference(f2, oracle):
         assert (got == oracle.mul(a, s, b, n)).all(), (m, s, n)
 
 
-@pytest.mark.parametrize("k", [1, 8, 9, 33, 44, 45, 64])
+@pytest.mark.parametrize("k", [1, 8, 9, 33, 36, 44, 45, 50, 60, 64])
 def test_addmul_mmpf_streaming_kernel(f2, oracle, k):
-    """K <= 64 takes the HBM-streaming MMPF table-apply: every table count (1-8 8-bit tables,
-    4096- to 512-bit tiles; 9-11 4-bit tables at 4096-bit tiles for 32 < K <= 44), a C window
-    starting at an odd word, rows across 2048-row blocks."""
+    """K <= 64 takes the HBM-streaming MMPF table-apply: every table layout (1-4 8-bit tables
+    at 4096- to 1024-bit tiles for K <= 32; 5-10 7-bit tables at 1024-bit tiles for K > 32),
+    a C window starting at an odd word (tile-edge lanes with one valid word), rows across
+    2048-row blocks (K <= 32) and 8192-row blocks (K = 64)."""
     rng = np.random.default_rng(k)
-    p, q, c0 = 4500, 5000, 64 * 3
+    p, q, c0 = 9000 if k == 64 else 4500, 5000, 64 * 3
     a, b = rand_words(rng, p, k), rand_words(rng, k, q)
     big = rand_words(rng, p, q + c0 + 64)
     dc = f2.DeviceMatrix.from_host(big, q + c0 + 64)
