@@ -79,6 +79,9 @@ int f2_matrix_clear(f2_matrix* a);                                       /* clea
 /* BitMatrix::randomize — bitmat.hpp:196, bitmat.cpp:136-154: same SplitMix64
  * stream, bit for bit, generated on the device (counter-based). */
 int f2_matrix_randomize(f2_matrix* a, double density, uint64_t seed);
+/* config 5's fixed-weight sparse rows (the reference has no generator):
+ * one SplitMix64 stream (prng.hpp:11-22), per row draws next() % ncols, repeats rejected */
+int f2_matrix_fixed_weight(f2_matrix* a, size_t weight, uint64_t seed);
 /* order-sensitive fingerprint over the reference packing (tests/oracle_lib.digest) */
 int f2_matrix_digest(const f2_matrix* a, uint64_t* out);
 
@@ -137,25 +140,42 @@ int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t q
 int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int inverse);
 
 /* ---- column-sharded PLS (one rank per GPU; paper_1006_1744_b200/dist.py) ----
- * Rank k holds panels k, k+N, ... of W bits side by side in a local matrix.  Per
- * panel the owner calls f2_dist_factor_panel (fills a header of
- * f2_dist_header_words(W) words and the panel's words for rows >= r), the caller
- * broadcasts both (NCCL), then every rank calls f2_dist_apply_panel on its trailing
- * columns (owner = 1 on the owner, which already applied the row gather). */
-size_t f2_dist_header_words(unsigned panel_bits);
-int f2_dist_begin(f2_matrix* a);
-int f2_dist_factor_panel(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t r, uint64_t panel_col,
-                         uint64_t* hdr_dev, uint64_t* words_dev, size_t words_stride, uint64_t* kb_out);
-int f2_dist_apply_panel(f2_matrix* a, size_t tw0, unsigned width_bits, int owner, const uint64_t* hdr_dev,
-                        const uint64_t* words_dev, size_t words_stride);
+ * The reference has no distributed entry point: this is the multi-GPU form of
+ * pls_recursive (pls.hpp:42-47, the recursion pls.cpp:63-103 split by columns,
+ * SURVEY.md §8e).  Rank k holds panels k, k+N, ... of W bits side by side in a
+ * local matrix with all m rows.  Every call ENQUEUES on the caller's CUDA streams
+ * (cudaStream_t passed as void*) and returns without waiting on the GPU.
+ * Exchange buffer of one panel: f2_dist_buffer_words(m, W) words = the panel's
+ * words of every row (W/64 per row) then its header; a broadcast may start at
+ * row r_lo <= the panel's first pivot row (its tail is all a receiver reads).
+ *   f2_dist_begin    reset the elimination state (r = 0, identity row order)
+ *   f2_dist_factor   owner of a panel: pivot search + panel update, export into buf
+ *   f2_dist_step     every rank, panel p: import (owner = 0), row gather, TRSM and
+ *                    Schur update of the local trailing columns (from word tw0); with
+ *                    lookahead = 1 (this rank owns panel p+1, whose local words start
+ *                    at tw0) the next panel's columns are updated first and
+ *                    f2_dist_factor(p+1) runs on side_stream beside the rest
+ *   f2_dist_note     record (kb, panel_r) of buf's header on `stream`;
+ *   f2_dist_header_rk  wait for that record and return it
+ *   f2_dist_finish   rank, P (m entries) and the pivot columns (Q prefix) */
+size_t f2_dist_buffer_words(size_t nrows, unsigned panel_bits);
+int f2_dist_begin(f2_matrix* a, unsigned panel_bits, size_t npanels, void* stream);
+int f2_dist_factor(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t panel_col, uint64_t* buf, int ctas,
+                   void* stream);
+int f2_dist_step(f2_matrix* a, int64_t p, int owner, size_t pw0, unsigned width_bits, const uint64_t* buf,
+                 size_t tw0, int lookahead, unsigned next_width, uint64_t next_col, uint64_t* next_buf, int side_ctas,
+                 void* main_stream, void* side_stream);
+int f2_dist_note(const uint64_t* buf, int64_t p, void* stream);
+int f2_dist_header_rk(int64_t p, uint64_t* kb, uint64_t* r0);
+int f2_dist_finish(f2_matrix* a, void* stream, uint64_t* rank, uint64_t* p, size_t plen, uint64_t* pivcols,
+                   size_t qcap);
+/* a non-owning f2_matrix over caller device memory (stride a multiple of 16 words);
+ * f2_matrix_destroy releases only the handle */
+int f2_matrix_view(uint64_t* dev, size_t nrows, size_t ncols, size_t stride_words, f2_matrix** out);
 /* compress_columns of a packed PLS result from its pivot columns (perm.cpp:18-21) */
 int f2_pls_compress(f2_matrix* a, uint64_t rank, const uint64_t* pivcols);
 /* pls_recursive's full Q (tail included) from (m, n, cutoff, pivot columns) — pls.cpp:63-103 */
 int f2_recursive_q(size_t m, size_t n, uint64_t cutoff, uint64_t rank, const uint64_t* pivcols, uint64_t* q);
-/* raw device buffers (exchange buffers of the sharded path) */
-void* f2_device_alloc(size_t bytes);
-void f2_device_free(void* p);
-int f2_device_copy(void* dst, const void* src, size_t bytes, int kind);
 
 /* ---- on-disk formats (io.hpp:3-11, io.cpp) ------------------------------ */
 enum f2_format { F2_FMT_ASCII = 0, F2_FMT_BINARY = 1 }; /* io::Format (io.hpp:22) */

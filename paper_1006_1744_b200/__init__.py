@@ -93,12 +93,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "f2_matrix_ncols": ([vp], sz),
         "f2_matrix_stride": ([vp], sz),
         "f2_matrix_device_ptr": ([vp], _u64p),
+        "f2_matrix_view": ([_u64p, sz, sz, sz, C.POINTER(vp)], i),
         "f2_matrix_upload": ([vp, _u64p, sz], i),
         "f2_matrix_download": ([vp, _u64p, sz], i),
         "f2_matrix_copy": ([vp, vp], i),
         "f2_matrix_clear": ([vp], i),
         "f2_matrix_randomize": ([vp, C.c_double, C.c_uint64], i),
         "f2_matrix_digest": ([vp, _u64p], i),
+        "f2_matrix_fixed_weight": ([vp, sz, C.c_uint64], i),
         "f2_host_alloc": ([sz], vp),
         "f2_host_free": ([vp], None),
         "f2_mmpf_pls": ([vp, _Window, _u64p, sz, _u64p, sz, C.c_uint, _u64p], i),
@@ -252,6 +254,26 @@ class DeviceMatrix:
         a.upload(words)
         return a
 
+    @staticmethod
+    def stride_for(ncols: int) -> int:
+        """Row stride in words: ceil(ncols / 64) padded to 16 words (128 B)."""
+        return (host_words(ncols) + 15) // 16 * 16
+
+    @classmethod
+    def from_torch(cls, t, ncols: int) -> "DeviceMatrix":
+        """A matrix over the memory of a CUDA tensor of shape (m, stride_for(ncols)), int64
+        (f2_matrix_view; the tensor is kept alive by the matrix).  Padding words must be 0."""
+        assert t.is_cuda and t.dim() == 2 and t.is_contiguous() and t.element_size() == 8
+        assert t.shape[1] % 16 == 0 and t.shape[1] >= host_words(ncols)
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.f2_matrix_view(C.cast(C.c_void_p(t.data_ptr()), _u64p), t.shape[0], ncols, t.shape[1], C.byref(h)))
+        a = cls.__new__(cls)
+        a._h = h
+        a.nrows, a.ncols = int(t.shape[0]), ncols
+        a.tensor = t
+        return a
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and _lib is not None:
@@ -279,6 +301,10 @@ class DeviceMatrix:
 
     def randomize(self, density: float, seed: int) -> None:
         _check(_lib.f2_matrix_randomize(self._h, float(density), int(seed) & (2 ** 64 - 1)))
+
+    def fixed_weight(self, weight: int, seed: int) -> None:
+        """Every row gets exactly ``weight`` ones at distinct uniform columns (config 5)."""
+        _check(_lib.f2_matrix_fixed_weight(self._h, int(weight), int(seed) & (2 ** 64 - 1)))
 
     def clear(self) -> None:
         _check(_lib.f2_matrix_clear(self._h))

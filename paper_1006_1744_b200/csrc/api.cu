@@ -2,16 +2,16 @@
 //
 // The engine is a blocked right-looking PLS.  The matrix is walked in panels of
 // W columns (64 for the MMPF entry point, 1024 by default for the recursive
-// entry point); each panel is walked in 64-column leaves.  Per leaf:
-//   k_leaf_pivot     exact pivot search (gauss.cpp:33-44 rule), 1 CTA; the row
+// entry point).  Per panel:
+//   k_panel_pipe     all 64-column leaves of the panel in one persistent kernel:
+//                    exact Gaussian pivot search (gauss.cpp:33-49 rule) on CTA 0,
+//                    leaf updates of the panel's rows on the other CTAs; the row
 //                    transpositions only re-map the panel's virtual row order
-//   k_leaf_update    leaf word -> L coefficients (gauss.cpp:47-49), leaf pivot rows
-//                    solved over the rest of the panel (mul.cpp:109-131), Gray-table
-//                    update of the rest of the panel (m4ri.cpp:28-38)
-// Per panel:
 //   k_perm_save/put  the panel's transpositions applied to whole rows (perm.cpp:8-16)
-//   k_pivot_trsm     panel pivot rows solved over the trailing columns
-//   k_table_apply    Schur complement C ^= L21 * U12 (M4RM, mul.cpp:21-68)
+//   k_panel_snapshot the finished panel's pivots + per-row solve words
+//   k_panel_trsm_snap panel pivot rows solved over the trailing columns (mul.cpp:109-131)
+//   k_schur_f4       Schur complement C ^= L21 * U12 on the tensor cores (mul.cpp:21-68),
+//                    k_mmpf_apply / k_table_apply for the narrow (MMPF) panels
 // and finally k_compress (compress_columns, perm.cpp:18-21) when Q != identity.
 // Every row offset and pivot count lives in device memory (PlsState), so the
 // launch sequence is fixed by (m, n, W) alone and the host never waits on the
@@ -37,12 +37,55 @@ struct f2_matrix {
     size_t m = 0, n = 0, stride = 0;
     uint64_t* d = nullptr;
     int device = 0;
+    bool owns = true;  // false: a view over caller memory (f2_matrix_view)
 };
 
 namespace {
 
 thread_local std::string g_err;
-std::mutex g_mu;  // one compute call at a time per process (shared stream + workspace)
+// one compute call at a time per process (shared stream + workspace); recursive so the
+// host-buffer entry points hold it across upload, decomposition and download
+std::recursive_mutex g_mu;
+
+// Schedule tuning.  The defaults are the measured best on B200; the
+// environment overrides exist for A/B runs, are read once at initialisation, and every
+// alternative path they select is exercised by tests/test_gpu_tuning.py.
+struct Tuning {
+    bool lookahead = true;        // F2_NO_LOOKAHEAD=1: panel kernels in stream order, no side stream
+    bool f4 = true;               // F2_SCHUR_M4RM=1: Schur update on the SMEM table kernel, not tcgen05
+    bool graph = true;            // F2_NO_GRAPH=1: enqueue the launch sequence instead of a cached graph
+    bool pdl = true;              // F2_NO_PDL=1: ordinary launches instead of programmatic dependent ones
+    bool early_wide_trsm = true;  // F2_NO_EARLY_WIDE_TRSM=1: wide TRSM after the fork in early panels too
+    int side_ctas = 24;           // F2_SIDE_CTAS: CTAs of the look-ahead panel kernel, early panels
+    int side_ctas_late = 48;      // F2_SIDE_CTAS_LATE: late panels (0: as early)
+    int late_pct = 38;            // F2_LATE_PCT: first late panel, % of the panels
+    bool evtl = false;            // F2_EVTL=1 (no graph): per-panel event timeline on stderr
+    bool evtl_sync = false;       // F2_EVTL_SYNC=1: synchronise at every timeline mark
+
+    void load(int nsm) {
+        auto flag = [](const char* k) {
+            const char* e = std::getenv(k);
+            return e && e[0] == '1';
+        };
+        auto num = [](const char* k, int d) {
+            const char* e = std::getenv(k);
+            return e ? std::atoi(e) : d;
+        };
+        lookahead = !flag("F2_NO_LOOKAHEAD");
+        f4 = !flag("F2_SCHUR_M4RM");
+        graph = !flag("F2_NO_GRAPH");
+        pdl = !flag("F2_NO_PDL");
+        early_wide_trsm = !flag("F2_NO_EARLY_WIDE_TRSM");
+        const int sc = num("F2_SIDE_CTAS", side_ctas);
+        if (sc >= 2 && sc <= nsm) side_ctas = sc;
+        const int sl = num("F2_SIDE_CTAS_LATE", side_ctas_late);
+        if (sl == 0 || (sl >= 2 && sl <= nsm)) side_ctas_late = sl;
+        late_pct = num("F2_LATE_PCT", late_pct);
+        evtl = flag("F2_EVTL");
+        evtl_sync = flag("F2_EVTL_SYNC");
+    }
+};
+Tuning tune;
 
 struct Ctx {
     bool init = false;
@@ -62,24 +105,16 @@ struct Ctx {
     int64_t* P = nullptr;
     int64_t* Qp = nullptr;
     int64_t* pmap = nullptr;
-    unsigned* bar = nullptr;  // grid barrier counter of k_panel_leaves
-    bool fused = true;        // panel leaves in one persistent kernel (F2_UNFUSED=1: three launches per leaf)
-    bool pipe = true;         // pipelined panel kernel (F2_NO_PIPE=1: one leaf per barrier pair)
-    // look-ahead: panel p+1's kernel runs on a high-priority side stream with side_ctas
-    // CTAs while the Schur update of panel p covers the columns right of panel p+1
-    bool lookahead = true;    // F2_NO_LOOKAHEAD=1 disables
-    int side_ctas = 24;       // F2_SIDE_CTAS (16-24 measured best at 64K^2)
-    int side_ctas_late = 48;  // F2_SIDE_CTAS_LATE: the second half of the factorisation (0: same)
-    int late_pct = 38;        // F2_LATE_PCT: where the "late" schedule starts (% of the panels)
+    unsigned* bar = nullptr;  // grid barrier counter of k_panel_pipe
+    // look-ahead: panel p+1's kernel runs on a high-priority side stream with
+    // tune.side_ctas CTAs while the Schur update of panel p covers the columns right of it
     cudaStream_t side = nullptr;
     cudaEvent_t la_fork = nullptr, la_join = nullptr;
     cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
     cudaEvent_t ax_fork = nullptr, ax_join = nullptr;
     cudaEvent_t tw_fork = nullptr, tw_join = nullptr;  // wide TRSM beside the narrow one (early panels)
-    bool early_wide_trsm = true;                       // F2_NO_EARLY_WIDE_TRSM=1 disables
     int64_t* snap = nullptr;  // [2][kSnapWords]
-    // tensor-core Schur of the look-ahead path (F2_SCHUR_M4RM=1: the SMEM table kernel)
-    bool f4 = true;
+    // tensor-core Schur operands (expanded L21 for every row, expanded U12 column tiles)
     uint8_t* f4_ax = nullptr;
     uint8_t* f4_bx = nullptr;
     unsigned* f4_claim = nullptr;
@@ -137,26 +172,17 @@ int ensure_init() {
     CK(cudaEventCreateWithFlags(&g.dl_join, cudaEventDisableTiming));
     CK(cudaMalloc(&g.st, sizeof(PlsState)));
     CK(cudaMalloc(&g.d_digest, sizeof(unsigned long long)));
+    tune.load(g.nsm);
+    g_pdl = tune.pdl;
     setup_leaf_kernels();
-    setup_leafupd_kernels();
     setup_trsm_kernels();
     setup_m4rm_kernels();
     setup_mmpf_apply_kernels();
     setup_schur_f4_kernels();
-    if (std::getenv("F2_SCHUR_M4RM")) g.f4 = false;
     setup_misc_kernels();
     setup_rref_kernels();
     setup_panel_kernels();
     CK(cudaMalloc(&g.bar, sizeof(unsigned)));
-    g.fused = !(std::getenv("F2_UNFUSED") && std::getenv("F2_UNFUSED")[0] == '1');
-    g.pipe = !(std::getenv("F2_NO_PIPE") && std::getenv("F2_NO_PIPE")[0] == '1');
-    g.lookahead = !(std::getenv("F2_NO_LOOKAHEAD") && std::getenv("F2_NO_LOOKAHEAD")[0] == '1');
-    if (const char* e = std::getenv("F2_SIDE_CTAS_LATE")) g.side_ctas_late = std::atoi(e);
-    if (const char* e = std::getenv("F2_LATE_PCT")) g.late_pct = std::atoi(e);
-    if (const char* e = std::getenv("F2_SIDE_CTAS")) {
-        const int v = std::atoi(e);
-        if (v >= 2 && v <= g.nsm) g.side_ctas = v;
-    }
     {
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -168,7 +194,6 @@ int ensure_init() {
         CK(cudaEventCreateWithFlags(&g.ax_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.tw_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.tw_join, cudaEventDisableTiming));
-        g.early_wide_trsm = !std::getenv("F2_NO_EARLY_WIDE_TRSM");
         CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
     }
     CK(cudaGetLastError());
@@ -179,25 +204,34 @@ int ensure_init() {
 extern uint64_t g_ws_gen;
 int ensure_workspace(size_t m, size_t nq, size_t npanels, size_t scratch_words) {
     if (m > g.cap_m || nq > g.cap_q || scratch_words > g.cap_scratch) ++g_ws_gen;
+    // a failed allocation leaves the buffer null with capacity 0 (never a stale pointer)
     if (m > g.cap_m) {
-        if (g.P) cudaFree(g.P);
-        if (g.pmap) cudaFree(g.pmap);
+        cudaFree(g.P);
+        cudaFree(g.pmap);
+        g.P = g.pmap = nullptr;
+        g.cap_m = 0;
         CK(cudaMalloc(&g.P, sizeof(int64_t) * std::max<size_t>(m, 1)));
         CK(cudaMalloc(&g.pmap, sizeof(int64_t) * std::max<size_t>(m, 1)));
         g.cap_m = m;
     }
     if (scratch_words > g.cap_scratch) {
-        if (g.scratch) cudaFree(g.scratch);
+        cudaFree(g.scratch);
+        g.scratch = nullptr;
+        g.cap_scratch = 0;
         CK(cudaMalloc(&g.scratch, sizeof(uint64_t) * scratch_words));
         g.cap_scratch = scratch_words;
     }
     if (nq > g.cap_q) {
-        if (g.Qp) cudaFree(g.Qp);
+        cudaFree(g.Qp);
+        g.Qp = nullptr;
+        g.cap_q = 0;
         CK(cudaMalloc(&g.Qp, sizeof(int64_t) * std::max<size_t>(nq, 1)));
         g.cap_q = nq;
     }
     if (npanels > g.h_r_cap) {
-        if (g.h_r) cudaFreeHost(g.h_r);
+        cudaFreeHost(g.h_r);
+        g.h_r = nullptr;
+        g.h_r_cap = 0;
         CK(cudaMallocHost(&g.h_r, sizeof(int64_t) * npanels));
         g.h_r_cap = npanels;
     }
@@ -211,12 +245,16 @@ int ensure_f4(size_t m, size_t nw) {
     const size_t b = schur_f4_b_bytes(static_cast<int64_t>(nw)) + schur_f4_b_bytes(kMaxPanelBits / 64);
     if (a > g.cap_f4a || b > g.cap_f4b) ++g_ws_gen;
     if (a > g.cap_f4a) {
-        if (g.f4_ax) cudaFree(g.f4_ax);
+        cudaFree(g.f4_ax);
+        g.f4_ax = nullptr;
+        g.cap_f4a = 0;
         CK(cudaMalloc(&g.f4_ax, a));
         g.cap_f4a = a;
     }
     if (b > g.cap_f4b) {
-        if (g.f4_bx) cudaFree(g.f4_bx);
+        cudaFree(g.f4_bx);
+        g.f4_bx = nullptr;
+        g.cap_f4b = 0;
         CK(cudaMalloc(&g.f4_bx, b));
         g.cap_f4b = b;
     }
@@ -309,7 +347,7 @@ inline void evmark(cudaStream_t s, const char* name, int64_t pi) {
     cudaEvent_t e;
     cudaError_t er = cudaEventCreate(&e);
     if (er == cudaSuccess) er = cudaEventRecord(e, s);
-    if (er == cudaSuccess && std::getenv("F2_EVTL_SYNC")) er = cudaStreamSynchronize(s);
+    if (er == cudaSuccess && tune.evtl_sync) er = cudaStreamSynchronize(s);
     if (er != cudaSuccess) std::fprintf(stderr, "evmark %s %lld: %s\n", name, static_cast<long long>(pi), cudaGetErrorString(er));
     g_evm.push_back({name, pi, e});
 }
@@ -405,7 +443,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
     int64_t checked = 0;
     bool stop = false;
 
-    const bool la = g.lookahead && g.fused && g.pipe && !g.stats && npanels > 1;
+    const bool la = tune.lookahead && !g.stats && npanels > 1;
     // the side kernel is launched cooperatively too: the scheduler then places all its
     // CTAs next to the running Schur update at once (plain launches waited for it to drain)
     auto panel_kernel = [&](cudaStream_t st_, int64_t pi_, int ctas) {
@@ -424,29 +462,9 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
         const int64_t pw0 = c / 64, pw1 = pw0 + nleaves;
         if (la) {
             // panel pi's kernel ran ahead (panel 0: above; others: on the side stream)
-        } else if (g.fused) {
-            LaunchTimer t(1, 0, 0);
-            if (g.pipe)
-                launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
-            else
-                launch_panel_leaves(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         } else {
-            for (int j = 0; j < nleaves; ++j) {
-                const int64_t wl = pw0 + j;
-                const int lw = static_cast<int>(std::min<int64_t>(64, n - 64 * wl));
-                {
-                    LaunchTimer t(1, 0, 0);
-                    launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, 0);
-                }
-                {
-                    LaunchTimer t(3, 0, 0);
-                    launch_leaf_tables(s, g.st, j);
-                }
-                {
-                    LaunchTimer t(3, 0, 0);
-                    launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
-                }
-            }
+            LaunchTimer t(1, 0, 0);
+            launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         }
         evmark(s, "gather0", pi);
         {
@@ -471,13 +489,13 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             ta.row_mode = ROWS_AFTER_PANEL;
             ta.st = g.st;
             const int64_t erows = m - std::min<int64_t>(m, c + cw);  // rows below the pivots at full rank
-            if (la && nleaves * 64 <= 1024) {
+            if (la) {
                 // snapshot the finished panel (rows, pivots, solve words), solve panel pi+1's
                 // columns narrow and fast, their Schur update, then panel pi+1's kernel on the
                 // side stream while the main stream solves and updates the columns right of it
                 int64_t* snap = g.snap + (pi & 1) * kSnapWords;
                 const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
-                const bool f4 = g.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
+                const bool f4 = tune.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
                 const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
                 if (f4) {  // the L21 operand only needs the gathered rows: expand it next to snapshot + TRSM
                     F4Job fa = fj;
@@ -492,8 +510,8 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 evmark(s, "snapshot", pi);
                 // while the trailing update dominates (the first ~45 % of the panels), the wide
                 // TRSM (disjoint columns) runs beside the narrow one instead of after the fork
-                const bool late = 100 * (pi + 1) >= g.late_pct * npanels;
-                const bool wide_early = !late && g.early_wide_trsm && npw1 < nw;
+                const bool late = 100 * (pi + 1) >= tune.late_pct * npanels;
+                const bool wide_early = !late && tune.early_wide_trsm && npw1 < nw;
                 if (wide_early) {
                     CK(cudaEventRecord(g.tw_fork, s));
                     CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
@@ -518,7 +536,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
                 // once the trailing update no longer dwarfs the panel kernel (~45 % of the panels
                 // done), give the side kernel more SMs: it is then on the critical path
-                const int side = g.side_ctas_late > 0 && late ? g.side_ctas_late : g.side_ctas;
+                const int side = tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas;
                 panel_kernel(g.side, pi + 1, side);
                 evmark(g.side, "panel_next", pi);
                 CK(cudaEventRecord(g.la_join, g.side));
@@ -545,44 +563,20 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                         TableApply t2 = ta;
                         t2.cw0 = npw1;
                         t2.bw0 = npw1;
-                        launch_table_apply(s, t2, g.nsm - g.side_ctas, erows);
+                        launch_table_apply(s, t2, g.nsm - tune.side_ctas, erows);
                     }
                 }
                 CK(cudaStreamWaitEvent(s, g.la_join, 0));
             } else {
                 {
                     LaunchTimer t(2, 0, 0);
-                    if (!g.fused) {  // the panel kernel leaves the maps behind
-                        launch_panel_lmaps(s, A, pw0, nleaves, g.st);
-                        ++g.launches;
-                    }
                     launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
                 }
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
-                if (la) {  // look-ahead without the snapshot TRSM (panels wider than 1024)
-                    int64_t* snap = g.snap + (pi & 1) * kSnapWords;
-                    launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
-                    ta.brow = snap + kSnapBrow;
-                    ta.rk = snap;
-                    const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
-                    TableApply t1 = ta;
-                    t1.cw1 = npw1;
-                    launch_table_apply(s, t1, g.nsm, erows);
-                    CK(cudaEventRecord(g.la_fork, s));
-                    CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
-                    panel_kernel(g.side, pi + 1, g.side_ctas);
-                    CK(cudaEventRecord(g.la_join, g.side));
-                    if (npw1 < nw) {
-                        TableApply t2 = ta;
-                        t2.cw0 = npw1;
-                        t2.bw0 = npw1;
-                        launch_table_apply(s, t2, g.nsm - g.side_ctas, erows, g.side_ctas);
-                    }
-                    CK(cudaStreamWaitEvent(s, g.la_join, 0));
-                } else {
+                {
                     // work is data dependent; filled in from the pivots after the call
                     LaunchTimer t(0, static_cast<double>(pi), -1.0);
-                    if (g.f4 && g.f4_ax && cw >= 256 && cw <= 1024) {  // panel_r, panel_kb are adjacent
+                    if (tune.f4 && g.f4_ax && cw >= 256 && cw <= 1024) {  // panel_r, panel_kb are adjacent
                         const F4Job fj = pls_f4_job(A, pw0, cw, pw1, nw, &g.st->panel_r, g.st->brow);
                         launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
                         launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
@@ -643,10 +637,10 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
                               static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
     if (rc) return rc;
-    if (g.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw)))) return rc;
+    if (tune.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw)))) return rc;
     cudaStream_t s = g.stream;
-    const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && !std::getenv("F2_NO_GRAPH");
-    g_evtl = !use_graph && std::getenv("F2_EVTL") != nullptr;
+    const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && tune.graph;
+    g_evtl = !use_graph && tune.evtl;
     if (use_graph) {
         const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
                          g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen &&
@@ -841,14 +835,14 @@ int f2_device_count(void) {
 }
 
 int f2_set_device(int device) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (g.init && device != g.device) return fail(F2_INVALID_ARGUMENT, "device already initialised");
     g.device = device;
     return ensure_init();
 }
 
 int f2_matrix_create(size_t nrows, size_t ncols, f2_matrix** out) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!out) return fail(F2_INVALID_ARGUMENT, "out is NULL");
     int rc = ensure_init();
     if (rc) return rc;
@@ -860,8 +854,8 @@ int f2_matrix_create(size_t nrows, size_t ncols, f2_matrix** out) {
 
 void f2_matrix_destroy(f2_matrix* a) {
     if (!a) return;
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (a->d) cudaFree(a->d);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (a->d && a->owns) cudaFree(a->d);
     delete a;
 }
 
@@ -871,7 +865,7 @@ size_t f2_matrix_stride(const f2_matrix* a) { return a ? a->stride : 0; }
 uint64_t* f2_matrix_device_ptr(f2_matrix* a) { return a ? a->d : nullptr; }
 
 int f2_matrix_upload(f2_matrix* a, const uint64_t* host, size_t host_stride_words) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!host && a->m)) return fail(F2_INVALID_ARGUMENT, "null argument");
     const size_t nw = (a->n + 63) / 64;
     if (host_stride_words < nw) return fail(F2_INVALID_ARGUMENT, "host stride shorter than a row");
@@ -889,7 +883,7 @@ int f2_matrix_upload(f2_matrix* a, const uint64_t* host, size_t host_stride_word
 }
 
 int f2_matrix_download(const f2_matrix* a, uint64_t* host, size_t host_stride_words) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!host && a->m)) return fail(F2_INVALID_ARGUMENT, "null argument");
     const size_t nw = (a->n + 63) / 64;
     if (host_stride_words < nw) return fail(F2_INVALID_ARGUMENT, "host stride shorter than a row");
@@ -901,7 +895,7 @@ int f2_matrix_download(const f2_matrix* a, uint64_t* host, size_t host_stride_wo
 }
 
 int f2_matrix_copy(f2_matrix* dst, const f2_matrix* src) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!dst || !src) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (dst->m != src->m || dst->n != src->n) return fail(F2_INVALID_ARGUMENT, "shape mismatch");
     if (src->m) CK(cudaMemcpyAsync(dst->d, src->d, src->m * src->stride * 8, cudaMemcpyDeviceToDevice, g.stream));
@@ -910,7 +904,7 @@ int f2_matrix_copy(f2_matrix* dst, const f2_matrix* src) {
 }
 
 int f2_matrix_clear(f2_matrix* a) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (a->m) CK(cudaMemsetAsync(a->d, 0, a->m * a->stride * 8, g.stream));
     CK(cudaStreamSynchronize(g.stream));
@@ -918,7 +912,7 @@ int f2_matrix_clear(f2_matrix* a) {
 }
 
 int f2_matrix_randomize(f2_matrix* a, double density, uint64_t seed) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!(density >= 0.0 && density <= 1.0))
         return fail(F2_INVALID_ARGUMENT, "randomize: density must be in [0, 1]");
@@ -930,8 +924,39 @@ int f2_matrix_randomize(f2_matrix* a, double density, uint64_t seed) {
     return F2_OK;
 }
 
+// Config 5's generator (the reference has none): one SplitMix64 stream
+// (prng.hpp:11-22) from `seed`; per row, draw next() % ncols and reject repeats until
+// the row has `weight` distinct ones.  Sequential by construction (a row's draw count
+// depends on its rejections), so it runs on the host and uploads the rows.
+int f2_matrix_fixed_weight(f2_matrix* a, size_t weight, uint64_t seed) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (weight > a->n) return fail(F2_INVALID_ARGUMENT, "fixed_weight: weight exceeds the column count");
+    if (a->m == 0 || a->n == 0) return F2_OK;
+    const size_t nw = (a->n + 63) / 64;
+    std::vector<uint64_t> rows(a->m * nw, 0);
+    uint64_t st = seed;
+    auto next = [&st]() {
+        uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    for (size_t i = 0; i < a->m; ++i) {
+        uint64_t* row = rows.data() + i * nw;
+        for (size_t got = 0; got < weight;) {
+            const size_t j = static_cast<size_t>(next() % a->n);
+            const uint64_t bit = 1ull << (j % 64);
+            if (row[j / 64] & bit) continue;
+            row[j / 64] |= bit;
+            ++got;
+        }
+    }
+    return f2_matrix_upload(a, rows.data(), nw);
+}
+
 int f2_matrix_digest(const f2_matrix* a, uint64_t* out) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || !out) return fail(F2_INVALID_ARGUMENT, "null argument");
     launch_digest(g.stream, mat_of(a), g.d_digest);
     unsigned long long h = 0;
@@ -976,7 +1001,7 @@ int f2_set_panel_bits(unsigned bits) {
 // identity-filled :87-88; empty -> 0 :89; k > 8 rejected after the fill :90.
 int f2_mmpf_pls(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen, unsigned k,
                 uint64_t* rank) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || !rank || (!p && plen) || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
@@ -1002,7 +1027,7 @@ int f2_mmpf_pls(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q
 // pls_recursive (pls.cpp:105-113): validate(cfg) :57-61, size check :110-111.
 int f2_pls_recursive(f2_matrix* a, f2_window w, uint64_t* p, size_t plen, uint64_t* q, size_t qlen,
                      const f2_elim_config* cfg, uint64_t* rank) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     f2_elim_config c0{0, 0, 0.15, F2_ALG_PLS};
     const f2_elim_config& cfg_ = cfg ? *cfg : c0;
     if (!a || !rank || (!p && plen) || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
@@ -1038,18 +1063,17 @@ static f2_matrix* g_host_mat = nullptr;
 
 static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols, size_t stride_words, uint64_t* p,
                     uint64_t* q, const f2_elim_config* cfg, unsigned k, uint64_t* rank) {
+    // held from the upload to the last download: concurrent callers share g_host_mat
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     int rc;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        if ((rc = ensure_init())) return rc;
-        if (!g_host_mat || g_host_mat->m != nrows || g_host_mat->n != ncols) {
-            if (g_host_mat) {
-                cudaFree(g_host_mat->d);
-                delete g_host_mat;
-                g_host_mat = nullptr;
-            }
-            if ((rc = alloc_matrix(nrows, ncols, &g_host_mat))) return rc;
+    if ((rc = ensure_init())) return rc;
+    if (!g_host_mat || g_host_mat->m != nrows || g_host_mat->n != ncols) {
+        if (g_host_mat) {
+            cudaFree(g_host_mat->d);
+            delete g_host_mat;
+            g_host_mat = nullptr;
         }
+        if ((rc = alloc_matrix(nrows, ncols, &g_host_mat))) return rc;
     }
     f2_matrix* a = g_host_mat;
     rc = f2_matrix_upload(a, words, stride_words);
@@ -1059,22 +1083,17 @@ static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols,
                         nrows > 0 && ncols > 0;
     cudaGetLastError();
     if (!rc) {
-        {
-            std::lock_guard<std::mutex> lk(g_mu);
-            g.dl_host = pinned ? words : nullptr;
-            g.dl_pitch = stride_words;
-            g.dl_done = -1;
-        }
+        g.dl_host = pinned ? words : nullptr;
+        g.dl_pitch = stride_words;
+        g.dl_done = -1;
         f2_window w{0, 0, nrows, ncols};
         rc = recursive ? f2_pls_recursive(a, w, p, nrows, q, ncols, cfg, rank)
                        : f2_mmpf_pls(a, w, p, nrows, q, ncols, k, rank);
-        std::lock_guard<std::mutex> lk(g_mu);
         g.dl_host = nullptr;
     }
     if (!rc) {
         const int64_t done = g.dl_done < 0 ? 0 : g.dl_done;
         if (done < static_cast<int64_t>(nrows)) {  // the rest (non-pivot rows, or every row after a fallback)
-            std::lock_guard<std::mutex> lk(g_mu);
             const size_t nw = (ncols + 63) / 64;
             CK(cudaMemcpy2DAsync(words + done * stride_words, stride_words * 8, a->d + done * a->stride, a->stride * 8,
                                  nw * 8, nrows - done, cudaMemcpyDeviceToHost, g.stream));
@@ -1095,7 +1114,7 @@ int f2_pls_recursive_host(uint64_t* words, size_t nrows, size_t ncols, size_t st
 }
 
 int f2_stats_enable(int enable) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     g.stats = enable != 0;
     return F2_OK;
 }
@@ -1111,7 +1130,7 @@ int f2_stats_get(int kind, uint64_t* launches, double* ms, double* bytes, double
 }
 
 int f2_stats_reset(void) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     for (auto& f : g.fam) f = Ctx::Family{};
     return F2_OK;
 }
@@ -1122,7 +1141,7 @@ uint64_t f2_last_graph_kernels(void) { return g.last_kernels; }
 // device timer on the library's stream (bench.py: CUDA events, not host clocks)
 static cudaEvent_t g_t0 = nullptr, g_t1 = nullptr;
 int f2_timer_start(void) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     int rc = ensure_init();
     if (rc) return rc;
     if (!g_t0) {
@@ -1133,7 +1152,7 @@ int f2_timer_start(void) {
     return F2_OK;
 }
 int f2_timer_stop(double* ms) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!g_t0 || !ms) return fail(F2_INVALID_ARGUMENT, "timer not started");
     CK(cudaEventRecord(g_t1, g.stream));
     CK(cudaEventSynchronize(g_t1));
@@ -1224,7 +1243,7 @@ void table_mul(const Mat& C, int64_t cr0, int64_t cw0, const Mat& A, int64_t ar0
                   2.0 * static_cast<double>(p) * static_cast<double>(s) * static_cast<double>(q));
     // tensor cores once the product is deep and wide enough to fill 128 x 256 x 1024 tiles
     // (F2_SCHUR_M4RM=1 keeps the SMEM table kernel); K is cut into chunks of <= 1024
-    if (g.f4 && s >= 256 && p >= 128 && q >= 256 && ensure_f4(static_cast<size_t>(p), static_cast<size_t>(ta.cw1 - cw0)) == F2_OK) {
+    if (tune.f4 && s >= 256 && p >= 128 && q >= 256 && ensure_f4(static_cast<size_t>(p), static_cast<size_t>(ta.cw1 - cw0)) == F2_OK) {
         for (int64_t k0 = 0; k0 < s; k0 += kF4MaxK) {
             F4Job j{};
             j.C = C;
@@ -1271,7 +1290,7 @@ void trsm_rec(const Mat& Lm, const Mat& Bm, int64_t o, int64_t r) {
 extern "C" {
 
 int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix* b, f2_window wb, unsigned k) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     (void)k;  // table width is an implementation choice; the product is exact for any k
     if (!a || !b || !c) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(a, wa) || !window_ok(b, wb) || !window_ok(c, wc))
@@ -1304,7 +1323,7 @@ int f2_addmul(f2_matrix* c, f2_window wc, f2_matrix* a, f2_window wa, f2_matrix*
 }
 
 int f2_mul_m4rm(const f2_matrix* a, const f2_matrix* b, unsigned k, f2_matrix** out) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || !b || !out) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (a->n != b->m) return fail(F2_INVALID_ARGUMENT, "mul_m4rm: dimension mismatch");
     if (k > 8) return fail(F2_INVALID_ARGUMENT, "mul_m4rm: k must be in 0..8");
@@ -1322,7 +1341,7 @@ int f2_mul_m4rm(const f2_matrix* a, const f2_matrix* b, unsigned k, f2_matrix** 
 }
 
 int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window wb) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!l || !b) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(l, wl) || !window_ok(b, wb)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     const size_t r = wl.r1 - wl.r0;
@@ -1346,7 +1365,7 @@ int f2_trsm_lower_left_unit(f2_matrix* l, f2_window wl, f2_matrix* b, f2_window 
 // B <- U^{-1} B, U unit upper triangular (its lower part ignored).  With R the row/column
 // reversal, U^{-1} B = R (R U R)^{-1} R B: the lower solver on reversed copies.
 int f2_trsm_upper_left_unit(f2_matrix* u, f2_window wu, f2_matrix* b, f2_window wb) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!u || !b) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(u, wu) || !window_ok(b, wb)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     const size_t r = wu.r1 - wu.r0;
@@ -1379,7 +1398,7 @@ int f2_trsm_upper_left_unit(f2_matrix* u, f2_window wu, f2_matrix* b, f2_window 
 }
 
 int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t qlen) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (rank > a->m || rank > qlen) return fail(F2_INVALID_ARGUMENT, "compress_columns: rank out of range");
     for (uint64_t j = 0; j < rank; ++j)
@@ -1400,7 +1419,7 @@ int f2_compress_columns(f2_matrix* a, uint64_t rank, const uint64_t* q, size_t q
 }
 
 int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int inverse) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!p && plen)) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     const size_t m = w.r1 - w.r0;
@@ -1434,124 +1453,293 @@ int f2_apply_rows(f2_matrix* a, f2_window w, const uint64_t* p, size_t plen, int
 
 }  // extern "C"
 
-// ---- column-sharded PLS building blocks (paper_1006_1744_b200/dist.py) ----------------
-// Rank k holds the panels p = k, k+N, k+2N, ... (W bits each) side by side in a local
-// matrix with all m rows.  Per panel: the owner factors it (leaf chain, virtual row
-// order), exports a header (pivots, re-mapped rows, P entries) and the panel's words
-// for rows >= r; both are broadcast; every rank then applies the panel to its own
-// trailing columns (row gather, panel TRSM, Schur multiply) reading L from the
-// broadcast words.  The packed result, P and the pivot columns equal the single-GPU
-// engine's (same pivot rule, same operations per column).
+// ---- column-sharded PLS (paper_1006_1744_b200/dist.py) --------------------------------
+// Rank k of N holds the panels p = k, k+N, ... (W bits each) side by side in a local
+// matrix with all m rows.  P, the pivot columns and every packed column equal the
+// single-GPU engine's (same pivot rule, same row operations per column).  Every call
+// below only ENQUEUES work on the caller's streams (torch streams in dist.py); nothing
+// waits on the GPU before f2_dist_finish, except f2_dist_header_rk, which dist.py calls
+// lagged by three panels.
+//   f2_dist_factor   owner of panel p: the panel kernel on its columns, then the header
+//                    and the panel's words of rows >= panel_r into an exchange buffer,
+//                    read through the virtual row order (the buffer can leave before
+//                    the owner's own row gather)
+//   -- dist.py broadcasts the buffer tail [r_lo * W/64, end) (NCCL over NVLink) --
+//   f2_dist_step     every rank, panel p: (non-owner) header -> state, P, Q prefix and
+//                    the L11^{-1} maps from the words; row gather over all local columns;
+//                    snapshot; panel TRSM + Schur update of the local trailing columns.
+//                    Look-ahead when this rank owns panel p+1: its columns first, then
+//                    f2_dist_factor(p+1) on the side stream beside the rest, exactly the
+//                    single-GPU engine's schedule (enqueue_engine)
+//   f2_dist_note     (kb, panel_r) of a buffer's header to pinned memory + an event, on
+//                    the stream where the buffer became valid
+namespace {
+struct DistState {
+    int64_t m = 0, ncols = 0;
+    unsigned W = 0;
+    int64_t npanels = 0;
+    int64_t* h_rk = nullptr;  // pinned [npanels][2]: (kb, panel_r)
+    size_t cap = 0;
+    std::vector<cudaEvent_t> ev;
+    struct Timed {  // stats: Schur launches of the timed schedule, work resolved at finish
+        int64_t p, c0, c1;
+        cudaEvent_t e0, e1;
+    };
+    std::vector<Timed> timed;
+};
+DistState gd;
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void dist_factor_enqueue(const Mat& A, int64_t pw0, unsigned width, int64_t col, uint64_t* buf, int ctas,
+                         cudaStream_t s) {
+    const int nleaves = static_cast<int>((width + 63) / 64);
+    launch_panel_pipe(s, A, pw0, static_cast<int>(width), pw0 + nleaves, g.st, g.P, g.Qp, g.pmap, col - 64 * pw0,
+                      g.bar, ctas, true);
+    launch_dist_export(s, A, pw0, nleaves, g.st, g.pmap, g.P, buf, static_cast<int>(gd.W), col, g.nsm);
+}
+}  // namespace
+
 extern "C" {
 
-size_t f2_dist_header_words(unsigned panel_bits) {
-    return 4 + 2 * static_cast<size_t>(panel_bits) + 2 * static_cast<size_t>(kMaxMoved);
+size_t f2_dist_buffer_words(size_t nrows, unsigned panel_bits) {
+    return nrows * (panel_bits / 64) + static_cast<size_t>(dist_header_words(static_cast<int>(panel_bits)));
 }
 
-int f2_dist_begin(f2_matrix* a) {
-    std::lock_guard<std::mutex> lk(g_mu);
+int f2_dist_begin(f2_matrix* a, unsigned panel_bits, size_t npanels, void* stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (panel_bits == 0 || panel_bits % 128 || panel_bits > 1024)
+        return fail(F2_INVALID_ARGUMENT, "panel bits must be a multiple of 128 and <= 1024");
     int rc = ensure_init();
     if (rc) return rc;
-    if ((rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride)))
-        return rc;
-    CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), g.stream));
-    launch_pmap_init(g.stream, g.pmap, static_cast<int64_t>(a->m));
-    CK(cudaStreamSynchronize(g.stream));
-    return F2_OK;
-}
-
-int f2_dist_factor_panel(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t r, uint64_t panel_col,
-                         uint64_t* hdr_dev, uint64_t* words_dev, size_t words_stride, uint64_t* kb_out) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!a || !hdr_dev || !words_dev || !kb_out) return fail(F2_INVALID_ARGUMENT, "null argument");
-    if (width_bits == 0 || width_bits > 1024 || (pw0 * 64 + width_bits) > a->n || r > a->m)
-        return fail(F2_INVALID_ARGUMENT, "panel out of range");
-    const int nleaves = static_cast<int>((width_bits + 63) / 64);
-    if (words_stride < static_cast<size_t>(nleaves)) return fail(F2_INVALID_ARGUMENT, "words stride too small");
-    int rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride);
-    if (rc) return rc;
-    const Mat A = mat_of(a);
-    const int64_t m = A.m, nw = (A.n + 63) / 64, pw1 = static_cast<int64_t>(pw0) + nleaves;
-    cudaStream_t s = g.stream;
-    launch_set_r(s, g.st, static_cast<int64_t>(r));
-    const int64_t qoff = static_cast<int64_t>(panel_col) - static_cast<int64_t>(pw0) * 64;
-    if (g.fused) {
-        launch_panel_leaves(s, A, static_cast<int64_t>(pw0), static_cast<int>(width_bits), pw1, g.st, g.P, g.Qp,
-                            g.pmap, qoff, g.bar, g.nsm);
-    } else {
-        for (int j = 0; j < nleaves; ++j) {
-            const int64_t wl = static_cast<int64_t>(pw0) + j;
-            const int lw = static_cast<int>(std::min<int64_t>(64, static_cast<int64_t>(width_bits) - 64 * j));
-            launch_leaf_pivot(s, A, wl, lw, j == 0, j, nleaves * 64, g.st, g.P, g.Qp, g.pmap, qoff);
-            launch_leaf_tables(s, g.st, j);
-            launch_leaf_update(s, A, wl, wl + 1, pw1, g.pmap, g.st);
-        }
+    const size_t m = std::max<size_t>(a->m, 1);
+    if ((rc = ensure_workspace(m, m, npanels + 1, static_cast<size_t>(kMaxMoved) * a->stride))) return rc;
+    if (tune.f4 && (rc = ensure_f4(m, (a->n + 63) / 64))) return rc;
+    if (npanels > gd.cap) {
+        cudaFreeHost(gd.h_rk);
+        gd.h_rk = nullptr;
+        gd.cap = 0;
+        CK(cudaMallocHost(&gd.h_rk, sizeof(int64_t) * 2 * npanels));
+        gd.cap = npanels;
     }
-    launch_dist_export(s, g.st, g.pmap, g.P, reinterpret_cast<int64_t*>(hdr_dev), nleaves * 64);
-    launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
-    if (static_cast<int64_t>(r) < m)
-        CK(cudaMemcpy2DAsync(words_dev + r * words_stride, words_stride * 8, A.w + static_cast<int64_t>(r) * A.stride + pw0,
-                             A.stride * 8, nleaves * 8, m - static_cast<int64_t>(r), cudaMemcpyDeviceToDevice, s));
-    int64_t kb = 0;
-    CK(cudaMemcpyAsync(&kb, &g.st->panel_kb, sizeof(kb), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    *kb_out = static_cast<uint64_t>(kb);
-    return F2_OK;
-}
-
-int f2_dist_apply_panel(f2_matrix* a, size_t tw0, unsigned width_bits, int owner, const uint64_t* hdr_dev,
-                        const uint64_t* words_dev, size_t words_stride) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!a || !hdr_dev || !words_dev) return fail(F2_INVALID_ARGUMENT, "null argument");
-    if (width_bits == 0 || width_bits > 1024) return fail(F2_INVALID_ARGUMENT, "panel width out of range");
-    const int nleaves = static_cast<int>((width_bits + 63) / 64);
-    int rc = ensure_workspace(a->m, std::max<size_t>(a->m, 1), 1, static_cast<size_t>(kMaxMoved) * a->stride);
-    if (rc) return rc;
-    const Mat A = mat_of(a);
-    const int64_t nw = (A.n + 63) / 64;
-    cudaStream_t s = g.stream;
-    if (!owner) {
-        launch_dist_import(s, g.st, g.pmap, reinterpret_cast<const int64_t*>(hdr_dev), nleaves * 64);
-        launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+    while (gd.ev.size() < npanels) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        gd.ev.push_back(e);
     }
-    if (static_cast<int64_t>(tw0) < nw) {
-        const Mat Cf{const_cast<uint64_t*>(words_dev), A.m, static_cast<int64_t>(width_bits),
-                     static_cast<int64_t>(words_stride)};
-        launch_panel_lmaps(s, Cf, 0, nleaves, g.st);
-        launch_panel_trsm(s, A, Cf, 0, nleaves, static_cast<int64_t>(tw0), nw, g.st);
-        TableApply ta{};
-        ta.C = A;
-        ta.c_r1 = A.m;
-        ta.cw0 = static_cast<int64_t>(tw0);
-        ta.cw1 = nw;
-        ta.A = Cf;
-        ta.aw0 = 0;
-        ta.kw = nleaves;
-        ta.kbits = width_bits;
-        ta.B = A;
-        ta.bw0 = static_cast<int64_t>(tw0);
-        ta.brow = g.st->brow;
-        ta.row_mode = ROWS_AFTER_PANEL;
-        ta.st = g.st;
-        if (g.f4 && width_bits >= 256 && ensure_f4(static_cast<size_t>(A.m), static_cast<size_t>(nw)) == F2_OK) {
-            // the panel's Schur update on the tensor cores (as in the single-GPU engine)
-            F4Job j = pls_f4_job(A, 0, width_bits, static_cast<int64_t>(tw0), nw, &g.st->panel_r, g.st->brow);
-            j.A = Cf;  // coefficients: the broadcast panel words
-            launch_schur_f4_expand_a(s, j, g.f4_ax, g.nsm);
-            launch_schur_f4(s, j, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
-        } else {
-            launch_table_apply(s, ta, g.nsm);
-        }
-    }
+    gd.m = static_cast<int64_t>(a->m);
+    gd.ncols = static_cast<int64_t>(a->n);
+    gd.W = panel_bits;
+    gd.npanels = static_cast<int64_t>(npanels);
+    cudaStream_t s = as_stream(stream);
+    CK(cudaMemsetAsync(g.st, 0, sizeof(PlsState), s));
+    launch_pmap_init(s, g.pmap, static_cast<int64_t>(a->m));
     CK(cudaGetLastError());
+    return F2_OK;
+}
+
+int f2_dist_factor(f2_matrix* a, size_t pw0, unsigned width_bits, uint64_t panel_col, uint64_t* buf, int ctas,
+                   void* stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!a || !buf) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (width_bits == 0 || width_bits > gd.W || (pw0 * 64 + width_bits) > a->n)
+        return fail(F2_INVALID_ARGUMENT, "panel out of range");
+    dist_factor_enqueue(mat_of(a), static_cast<int64_t>(pw0), width_bits, static_cast<int64_t>(panel_col), buf,
+                        ctas > 0 && ctas <= g.nsm ? ctas : g.nsm, as_stream(stream));
+    CK(cudaGetLastError());
+    return F2_OK;
+}
+
+int f2_dist_step(f2_matrix* a, int64_t p, int owner, size_t pw0, unsigned width_bits, const uint64_t* buf,
+                 size_t tw0, int lookahead, unsigned next_width, uint64_t next_col, uint64_t* next_buf, int side_ctas,
+                 void* main_stream, void* side_stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!a || !buf || (lookahead && !next_buf)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (width_bits == 0 || width_bits > gd.W || next_width > gd.W) return fail(F2_INVALID_ARGUMENT, "panel width out of range");
+    const Mat A = mat_of(a);
+    const int64_t m = A.m, nw = (A.n + 63) / 64, ws = gd.W / 64;
+    const int nleaves = static_cast<int>((width_bits + 63) / 64);
+    cudaStream_t s = as_stream(main_stream), sd = as_stream(side_stream);
+    const Mat Bw{const_cast<uint64_t*>(buf), m, static_cast<int64_t>(gd.W), ws};  // the broadcast words
+    const Mat Cf = owner ? A : Bw;                                                  // L of the panel
+    const int64_t cw0 = owner ? static_cast<int64_t>(pw0) : 0;
+    if (!owner) {
+        launch_dist_import(s, g.st, g.pmap, g.P, g.Qp, reinterpret_cast<const int64_t*>(buf + m * ws),
+                           static_cast<int>(gd.W));
+        launch_panel_lmaps(s, Cf, 0, nleaves, g.st);
+    }
+    launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+    const int64_t t0 = static_cast<int64_t>(tw0);
+    if (t0 >= nw) {
+        if (lookahead) return fail(F2_INVALID_ARGUMENT, "look-ahead without local trailing columns");
+        CK(cudaGetLastError());
+        return F2_OK;
+    }
+    int64_t* snap = g.snap + (p & 1) * kSnapWords;
+    const bool f4 = tune.f4 && g.f4_ax && width_bits >= 256;
+    F4Job fj = pls_f4_job(A, 0, width_bits, t0, nw, &g.st->panel_r, g.st->brow);
+    fj.A = Cf;
+    fj.aw0 = cw0;
+    if (f4) {  // L21 expanded beside the snapshot and the narrow TRSM (rk: the live state, stable until the fork)
+        CK(cudaEventRecord(g.ax_fork, s));
+        CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
+        launch_schur_f4_expand_a(g.aux, fj, g.f4_ax, g.nsm);
+        CK(cudaEventRecord(g.ax_join, g.aux));
+    }
+    launch_panel_snapshot(s, g.st, snap, nleaves, Cf, cw0);
+    fj.rk = snap;
+    fj.brow = snap + kSnapBrow;
+    TableApply ta{};
+    ta.C = A;
+    ta.c_r1 = m;
+    ta.A = Cf;
+    ta.aw0 = cw0;
+    ta.kw = nleaves;
+    ta.kbits = width_bits;
+    ta.B = A;
+    ta.brow = snap + kSnapBrow;
+    ta.rk = snap;
+    ta.row_mode = ROWS_AFTER_PANEL;
+    ta.st = g.st;
+    bool ax_waited = false;
+    auto schur = [&](int64_t c0, int64_t c1, int region) -> int {
+        if (c1 <= c0) return F2_OK;
+        DistState::Timed tm{p, c0, c1, nullptr, nullptr};
+        if (g.stats) {
+            CK(cudaEventCreate(&tm.e0));
+            CK(cudaEventCreate(&tm.e1));
+        }
+        if (tm.e0) CK(cudaEventRecord(tm.e0, s));
+        if (f4) {
+            if (!ax_waited) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+            ax_waited = true;
+            F4Job j = fj;
+            j.cw0 = j.bw0 = c0;
+            j.cw1 = c1;
+            launch_schur_f4(s, j, g.f4_ax, g.f4_bx + region * schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + region,
+                            g.nsm);
+        } else {
+            TableApply t = ta;
+            t.cw0 = t.bw0 = c0;
+            t.cw1 = c1;
+            launch_table_apply(s, t, g.nsm, m - std::min<int64_t>(m, static_cast<int64_t>(p + 1) * gd.W));
+        }
+        if (tm.e1) {
+            CK(cudaEventRecord(tm.e1, s));
+            gd.timed.push_back(tm);
+        }
+        return F2_OK;
+    };
+    int rc;
+    const int64_t nx = lookahead ? std::min<int64_t>(nw, t0 + (next_width + 63) / 64) : t0;  // next panel's words
+    const bool late = 100 * (p + 1) >= tune.late_pct * std::max<int64_t>(gd.npanels, 1);
+    const bool wide_early = lookahead && !late && tune.early_wide_trsm && nx < nw;
+    if (wide_early) {
+        CK(cudaEventRecord(g.tw_fork, s));
+        CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
+        launch_panel_trsm_snap(g.aux, A, snap, nleaves, nx, nw, 8);
+        CK(cudaEventRecord(g.tw_join, g.aux));
+    }
+    if (lookahead) {
+        launch_panel_trsm_snap(s, A, snap, nleaves, t0, nx, 1);
+        if ((rc = schur(t0, nx, 0))) return rc;
+        CK(cudaEventRecord(g.la_fork, s));
+        CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
+        const int ctas = side_ctas > 0 ? side_ctas
+                                       : (tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas);
+        dist_factor_enqueue(A, t0, next_width, static_cast<int64_t>(next_col), next_buf, std::min(ctas, g.nsm), sd);
+        CK(cudaEventRecord(g.la_join, sd));
+    }
+    if (wide_early) CK(cudaStreamWaitEvent(s, g.tw_join, 0));
+    else launch_panel_trsm_snap(s, A, snap, nleaves, nx, nw, 8);
+    if ((rc = schur(nx, nw, 1))) return rc;
+    if (f4 && !ax_waited) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+    if (lookahead) CK(cudaStreamWaitEvent(s, g.la_join, 0));
+    CK(cudaGetLastError());
+    return F2_OK;
+}
+
+int f2_dist_note(const uint64_t* buf, int64_t p, void* stream) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!buf || p < 0 || p >= gd.npanels) return fail(F2_INVALID_ARGUMENT, "panel out of range");
+    cudaStream_t s = as_stream(stream);
+    CK(cudaMemcpyAsync(gd.h_rk + 2 * p, buf + gd.m * (gd.W / 64), 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(gd.ev[p], s));
+    return F2_OK;
+}
+
+int f2_dist_header_rk(int64_t p, uint64_t* kb, uint64_t* r0) {
+    if (p < 0 || p >= gd.npanels || !kb || !r0) return fail(F2_INVALID_ARGUMENT, "panel out of range");
+    CK(cudaEventSynchronize(gd.ev[p]));
+    *kb = static_cast<uint64_t>(gd.h_rk[2 * p]);
+    *r0 = static_cast<uint64_t>(gd.h_rk[2 * p + 1]);
+    return F2_OK;
+}
+
+// rank, P (LAPACK transpositions, identity past the rank) and the pivot columns; waits
+// for `stream` (the caller joins its other streams into it first)
+int f2_dist_finish(f2_matrix* a, void* stream, uint64_t* rank, uint64_t* p, size_t plen, uint64_t* pivcols,
+                   size_t qcap) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!a || !rank || (!p && plen) || (!pivcols && qcap)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (plen != a->m) return fail(F2_INVALID_ARGUMENT, "P length must equal the row count");
+    cudaStream_t s = as_stream(stream);
+    int64_t r = 0;
+    CK(cudaMemcpyAsync(&r, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (static_cast<size_t>(r) > qcap) return fail(F2_INVALID_ARGUMENT, "pivot column buffer too small");
+    std::vector<int64_t> tmp(static_cast<size_t>(r));
+    for (size_t i = 0; i < plen; ++i) p[i] = i;
+    if (r) {
+        CK(cudaMemcpy(tmp.data(), g.P, sizeof(int64_t) * r, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < r; ++t) p[t] = static_cast<uint64_t>(tmp[t]);
+        CK(cudaMemcpy(tmp.data(), g.Qp, sizeof(int64_t) * r, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < r; ++t) pivcols[t] = static_cast<uint64_t>(tmp[t]);
+    }
+    *rank = static_cast<uint64_t>(r);
+    // stats: each timed Schur launch's work from its panel's header, 2 * rows * kb * columns
+    for (auto& tm : gd.timed) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
+        const int64_t kb = gd.h_rk[2 * tm.p], r0 = gd.h_rk[2 * tm.p + 1];
+        const double rows = static_cast<double>(gd.m - r0 - kb);
+        const double cols = static_cast<double>(std::min<int64_t>(64 * tm.c1, gd.ncols) - 64 * tm.c0);
+        auto& f = g.fam[0];
+        f.n += 1;
+        f.ms += ms;
+        f.bitops += 2.0 * rows * static_cast<double>(kb) * cols;
+        f.bytes += kb ? rows * 2.0 * 8.0 * static_cast<double>(tm.c1 - tm.c0) : 0.0;
+        cudaEventDestroy(tm.e0);
+        cudaEventDestroy(tm.e1);
+    }
+    gd.timed.clear();
+    return F2_OK;
+}
+
+// A non-owning matrix over caller device memory (e.g. a torch tensor of m x stride
+// int64 words; stride a multiple of 16 words): the sharded schedule's local shards
+int f2_matrix_view(uint64_t* dev, size_t nrows, size_t ncols, size_t stride_words, f2_matrix** out) {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!out || (!dev && nrows)) return fail(F2_INVALID_ARGUMENT, "null argument");
+    if (stride_words < (ncols + 63) / 64 || stride_words % 16)
+        return fail(F2_INVALID_ARGUMENT, "view stride must cover a row and be a multiple of 16 words");
+    int rc = ensure_init();
+    if (rc) return rc;
+    f2_matrix* v = new f2_matrix;
+    v->m = nrows;
+    v->n = ncols;
+    v->stride = stride_words;
+    v->d = dev;
+    v->device = g.device;
+    v->owns = false;
+    *out = v;
     return F2_OK;
 }
 
 // compress_columns of a packed PLS result given its pivot columns (k_compress)
 int f2_pls_compress(f2_matrix* a, uint64_t rank, const uint64_t* pivcols) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!pivcols && rank)) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (rank == 0) return F2_OK;
     int rc = ensure_init();
@@ -1573,29 +1761,6 @@ int f2_recursive_q(size_t m, size_t n, uint64_t cutoff, uint64_t rank, const uin
     if (!q && n) return fail(F2_INVALID_ARGUMENT, "null argument");
     std::vector<int64_t> piv(pivcols, pivcols + rank);
     replay_q(m, n, cutoff ? cutoff : default_cutoff(), piv.data(), static_cast<size_t>(rank), q);
-    return F2_OK;
-}
-
-void* f2_device_alloc(size_t bytes) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (ensure_init()) return nullptr;
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    cudaMemset(p, 0, std::max<size_t>(bytes, 8));
-    return p;
-}
-
-void f2_device_free(void* p) {
-    if (p) cudaFree(p);
-}
-
-int f2_device_copy(void* dst, const void* src, size_t bytes, int kind) {
-    // kind: 0 = device->device, 1 = host->device, 2 = device->host
-    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    CK(cudaMemcpy(dst, src, bytes, k));
     return F2_OK;
 }
 
@@ -1656,7 +1821,7 @@ extern "C" {
 // void rref_from_pls(MatrixWindow a, size_t rank, span<const size_t> q) — pls.cpp:128-155;
 // validation as pls.cpp:130-135.
 int f2_rref_from_pls(f2_matrix* a, f2_window w, uint64_t rank, const uint64_t* q, size_t qlen) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!a || (!q && qlen)) return fail(F2_INVALID_ARGUMENT, "null argument");
     if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
@@ -1677,7 +1842,7 @@ int f2_rref_from_pls(f2_matrix* a, f2_window w, uint64_t rank, const uint64_t* q
 int f2_rref(f2_matrix* a, f2_window w, const f2_elim_config* cfg, uint64_t* rank) {
     if (!a || !rank) return fail(F2_INVALID_ARGUMENT, "null argument");
     {
-        std::lock_guard<std::mutex> lk(g_mu);
+        std::lock_guard<std::recursive_mutex> lk(g_mu);
         if (!window_ok(a, w)) return fail(F2_OUT_OF_RANGE, "MatrixWindow: invalid bounds");
     }
     const size_t m = w.r1 - w.r0, n = w.c1 - w.c0;
@@ -1703,7 +1868,7 @@ int f2_m4ri_rref(f2_matrix* a, unsigned k, int full, uint64_t* rank) {
     int rc = f2_pls_recursive(a, w, p.data(), m, q.data(), n, nullptr, rank);
     if (rc) return rc;
     if (full) return f2_rref_from_pls(a, w, *rank, q.data(), static_cast<size_t>(*rank));
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     const int64_t r = static_cast<int64_t>(*rank);
     if ((rc = ensure_workspace(m, std::max<size_t>(m, *rank) + 1, 1, static_cast<size_t>(kMaxMoved) * a->stride)))
         return rc;

@@ -44,8 +44,6 @@ struct PlsState {
     uint64_t leaf_mask;                 // pivot columns within the leaf word
     uint64_t ustrict[64];               // leaf pivot words, bits <= pivot cleared
     uint64_t ufull[64];                 // leaf pivot words (L bits, leading 1, S bits)
-    uint64_t leaf_F[8][256];            // leaf finalize tables: correction of a word whose byte g reads v
-    uint8_t leaf_M[8][256];             // leaf group index maps (inverse 8x8 L blocks, see trsm.cu)
     uint64_t lmap[kMaxPanelBits / 64][8][256];  // per leaf of the panel: c -> c * L_leaf^{-1}, bytewise
     int32_t q[64];                      // leaf pivot bit positions (0..63)
     int32_t panel_q[kMaxPanelBits];     // panel pivot columns, relative to the panel
@@ -69,13 +67,6 @@ struct PlsState {
     unsigned long long tl[4][128];      // F2_TIMELINE builds: per panel start/end of the panel kernel and the Schur
 };
 
-// Leaf update geometry (leafupd.cu): kLuRPT rows per quarter-warp lane group, 1024-bit
-// column tiles; dynamic smem X[64][kLuTNW] | T[2][256][kLuTNW] | F[8][256] | cbuf | pbuf.
-constexpr int kLuRPT = 4;
-constexpr int kLuTNW = 16;
-constexpr size_t leaf_update_smem(int nthreads) {
-    return sizeof(uint64_t) * (64 * kLuTNW + 2 * 256 * kLuTNW + 8 * 256 + 2 * ((nthreads / 32) * 4 * kLuRPT));
-}
 
 // Loads of data other CTAs may have written during the same (persistent) kernel go
 // through L2 (ld.global.cg): the per-SM L1 is not coherent.

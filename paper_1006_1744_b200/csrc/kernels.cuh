@@ -30,23 +30,16 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // leaf.cu
-void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off);
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch);
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
-void launch_leaf_tables(cudaStream_t s, PlsState* st, int leaf_in_panel);
 void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves, PlsState* st);
-void launch_dist_export(cudaStream_t s, const PlsState* st, const int64_t* pmap, const int64_t* P, int64_t* hdr, int W);
-void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, const int64_t* hdr, int W);
-void launch_set_r(cudaStream_t s, PlsState* st, int64_t r);
+constexpr int64_t dist_header_words(int W) { return 4 + 2 * static_cast<int64_t>(W) + 2 * kMaxMoved; }
+void launch_dist_export(cudaStream_t s, const Mat& A, int64_t pw0, int nwp, const PlsState* st, const int64_t* pmap,
+                        const int64_t* P, uint64_t* buf, int W, int64_t col, int nsm);
+void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, int64_t* P, int64_t* Qp, const int64_t* hdr,
+                        int W);
 void setup_leaf_kernels();
 
-// leafupd.cu — one leaf's update of its panel (virtual row order via pmap):
-// finalize the leaf word of every row below the pivots (-> L coefficients),
-// solve the leaf pivot rows over the rest of the panel, table-apply the rest.
-void launch_leaf_update(cudaStream_t s, const Mat& A, int64_t wl, int64_t rw0, int64_t rw1, const int64_t* pmap,
-                        const PlsState* st);
-void setup_leafupd_kernels();
 
 // trsm.cu — forward substitution of pivot rows by 8-column groups with
 // Gray tables (the M4RI-style TRSM of mul.cpp:109-131, blocked for SMEM).
@@ -77,8 +70,6 @@ struct TableApply {
     const PlsState* st;
     int64_t row_tile0;     // first 1024-row tile of this launch (set by launch_table_apply)
     const int64_t* rk;     // ROWS_AFTER_PANEL from a snapshot {panel_r, panel_kb} instead of st (look-ahead)
-    int idle_ctas;         // > 0: grid rows with row_tile0 + y < 0 are placeholders; their first
-    int64_t idle_ns;       // idle_ctas CTAs hold their SM for idle_ns, then exit
 };
 // snapshot of a finished panel's row range and raw-column -> pivot-row map, so its Schur
 // update can run while the next panel's kernel rewrites the state
@@ -97,10 +88,7 @@ void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, in
 // (the next panel's kernel may be rewriting the state); strip = words per CTA (1 or 8)
 void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, int nleaves, int64_t tw0, int64_t tw1,
                             int strip);
-// idle_ctas > 0: the first idle_ctas CTAs of the launch hold their SMs for ~15 us and
-// exit, so a high-priority kernel launched next to this one (the look-ahead panel
-// kernel) is placed at once instead of after the first wave of tiles
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0, int idle_ctas = 0);
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows = 0);
 void setup_m4rm_kernels();
 // mmpf_apply.cu -- the HBM-streaming table-apply for K <= 64 (one coefficient word per row)
 void launch_mmpf_apply(cudaStream_t s, const TableApply& t, int nsm);
@@ -144,8 +132,6 @@ void launch_gather_rows(cudaStream_t s, const Mat& dst, const Mat& src, const in
 void launch_col_swaps(cudaStream_t s, const Mat& A, int64_t rank, const int64_t* q, int nsm);
 void setup_misc_kernels();
 // panel.cu: all leaves of a panel in one cooperative persistent kernel
-void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st,
-                         int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm);
 void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P,
                        int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm, bool cooperative = true);
 void setup_panel_kernels();

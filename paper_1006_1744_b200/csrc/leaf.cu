@@ -1,9 +1,12 @@
-// Leaf of the PLS engine: one 64-column word of the panel.
+// Panel bookkeeping kernels of the PLS engine (the pivot search itself is the
+// panel kernel, panel.cu):
 //
-//   k_leaf_pivot    exact Gaussian pivot search on the leaf word (1 CTA); the
-//                   leaf's transpositions only re-map positions (pmap)
-//   k_perm_save/put at the end of a panel, the panel's transpositions applied to
-//                   whole rows in one gather
+//   k_perm_save/put at the end of a panel, the panel's transpositions (which the
+//                   leaves only recorded as a re-mapped virtual row order, pmap)
+//                   applied to whole rows in one gather
+//   k_panel_lmaps   per-leaf L11^{-1} byte maps rebuilt from a panel's words (a
+//                   rank that imports a panel factored elsewhere)
+//   k_dist_*        the column-sharded exchange (export / import of a panel)
 //
 // Bit-exactness rests on the pivot rule of gauss_pls (proj/src/gauss.cpp:33-49):
 // the pivot is the leftmost column that has a nonzero at or below position r,
@@ -16,20 +19,8 @@
 
 #include "f2gpu.cuh"
 #include "kernels.cuh"
-#include "leaf_body.cuh"
 
 namespace f2g {
-
-__global__ void __launch_bounds__(1024, 1)
-k_leaf_pivot(Mat A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel, int panel_bits,
-             PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off) {
-    leaf_pivot_body(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off, wl + 1, nullptr);
-}
-
-__global__ void __launch_bounds__(256) k_leaf_tables(PlsState* st, int leaf_in_panel) {
-    (void)leaf_in_panel;
-    leaf_tables_body(st, blockIdx.x * 256 + threadIdx.x, 4096);
-}
 
 // Per leaf j of the finished panel (one CTA each, in parallel): the bytewise map
 // c -> c * L_jj^{-1} of the leaf's 64x64 unit lower block, for k_panel_trsm.
@@ -101,23 +92,25 @@ void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves,
 }
 
 // ---- column-sharded (multi-GPU) panel exchange --------------------------------------
-// Header of one factored panel (int64): [0] kb, [1] panel_r, [2] nmoved, [3] reserved,
-// [4, 4+W) pivot columns (panel-relative), then kMaxMoved re-mapped positions, then
-// their source rows (pmap values), then W entries P[panel_r + t].
+// Exchange buffer of one panel (api.cu, f2_dist_*): the panel's words of row x at
+// [x * ws, (x+1) * ws), then the header at m * ws (int64): [0] kb, [1] panel_r,
+// [2] nmoved, [3] the panel's global first column, [4, 4+W) pivot columns (panel
+// relative), [4+W, 4+2W) P entries P[panel_r + t], then kMaxMoved re-mapped
+// positions and kMaxMoved source rows (pmap values).
 __global__ void __launch_bounds__(256) k_dist_export(const PlsState* st, const int64_t* pmap, const int64_t* P,
-                                                    int64_t* hdr, int W) {
+                                                    int64_t* hdr, int W, int64_t col) {
     const int kb = static_cast<int>(st->panel_kb), nm = st->nmoved;
     const int64_t r0 = st->panel_r;
     int64_t* q = hdr + 4;
-    int64_t* mv = q + W;
+    int64_t* pp = q + W;
+    int64_t* mv = pp + W;
     int64_t* src = mv + kMaxMoved;
-    int64_t* pp = src + kMaxMoved;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     if (tid == 0) {
         hdr[0] = kb;
         hdr[1] = r0;
         hdr[2] = nm;
-        hdr[3] = 0;
+        hdr[3] = col;
     }
     for (int t = tid; t < kb; t += nth) {
         q[t] = st->panel_q[t];
@@ -129,13 +122,41 @@ __global__ void __launch_bounds__(256) k_dist_export(const PlsState* st, const i
     }
 }
 
+// The owner's panel words of every row >= panel_r, in the row order the panel's
+// gather will produce (position x reads physical row pmap[x]), so the broadcast can
+// leave before the owner's own gather runs; words past the panel's width are zero.
+__global__ void __launch_bounds__(256) k_dist_export_words(Mat A, int64_t pw0, int nwp, const PlsState* st,
+                                                          const int64_t* pmap, uint64_t* buf, int ws) {
+    const int64_t r0 = st->panel_r;
+    const int per = ws / 2;  // 16-byte chunks per row (ws is even: W is a multiple of 128)
+    const int64_t total = (A.m - r0) * per;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t x = r0 + i / per;
+        const int k = 2 * static_cast<int>(i % per);
+        const int64_t ph = pmap[x];
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (k + 1 < nwp) {
+            v = *reinterpret_cast<const uint4*>(A.w + ph * A.stride + pw0 + k);
+        } else if (k < nwp) {
+            const uint64_t w = A.w[ph * A.stride + pw0 + k];
+            v.x = static_cast<unsigned>(w);
+            v.y = static_cast<unsigned>(w >> 32);
+        }
+        *reinterpret_cast<uint4*>(buf + x * ws + k) = v;
+    }
+}
+
 // A rank that does not own the panel adopts the owner's header: pivot bookkeeping
-// for the TRSM/Schur kernels and the re-mapped positions for the row gather.
-__global__ void __launch_bounds__(1024) k_dist_import(PlsState* st, int64_t* pmap, const int64_t* hdr, int W) {
+// for the TRSM/Schur kernels, P and the pivot columns, and the re-mapped positions
+// for the row gather.
+__global__ void __launch_bounds__(1024) k_dist_import(PlsState* st, int64_t* pmap, int64_t* P, int64_t* Qp,
+                                                     const int64_t* hdr, int W) {
     const int kb = static_cast<int>(hdr[0]), nm = static_cast<int>(hdr[2]);
-    const int64_t r0 = hdr[1];
+    const int64_t r0 = hdr[1], col = hdr[3];
     const int64_t* q = hdr + 4;
-    const int64_t* mv = q + W;
+    const int64_t* pp = q + W;
+    const int64_t* mv = pp + W;
     const int64_t* src = mv + kMaxMoved;
     const int tid = threadIdx.x, nth = blockDim.x;
     for (int i = tid; i < W; i += nth) st->brow[i] = -1;
@@ -143,6 +164,8 @@ __global__ void __launch_bounds__(1024) k_dist_import(PlsState* st, int64_t* pma
     for (int t = tid; t < kb; t += nth) {
         st->panel_q[t] = static_cast<int32_t>(q[t]);
         st->brow[q[t]] = r0 + t;
+        P[r0 + t] = pp[t];
+        Qp[r0 + t] = col + q[t];
     }
     for (int i = tid; i < nm; i += nth) {
         st->moved[i] = mv[i];
@@ -156,19 +179,16 @@ __global__ void __launch_bounds__(1024) k_dist_import(PlsState* st, int64_t* pma
     }
 }
 
-__global__ void k_set_r(PlsState* st, int64_t r) {
-    st->r = r;
-    st->panel_kb = 0;
-    st->nmoved = 0;
+void launch_dist_export(cudaStream_t s, const Mat& A, int64_t pw0, int nwp, const PlsState* st, const int64_t* pmap,
+                        const int64_t* P, uint64_t* buf, int W, int64_t col, int nsm) {
+    const int ws = W / 64;
+    k_dist_export_words<<<nsm * 4, 256, 0, s>>>(A, pw0, nwp, st, pmap, buf, ws);
+    k_dist_export<<<32, 256, 0, s>>>(st, pmap, P, reinterpret_cast<int64_t*>(buf + A.m * ws), W, col);
 }
-
-void launch_dist_export(cudaStream_t s, const PlsState* st, const int64_t* pmap, const int64_t* P, int64_t* hdr, int W) {
-    k_dist_export<<<32, 256, 0, s>>>(st, pmap, P, hdr, W);
+void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, int64_t* P, int64_t* Qp, const int64_t* hdr,
+                        int W) {
+    k_dist_import<<<1, 1024, 0, s>>>(st, pmap, P, Qp, hdr, W);
 }
-void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, const int64_t* hdr, int W) {
-    k_dist_import<<<1, 1024, 0, s>>>(st, pmap, hdr, W);
-}
-void launch_set_r(cudaStream_t s, PlsState* st, int64_t r) { k_set_r<<<1, 1, 0, s>>>(st, r); }
 
 // Panel end, step 1: copy the rows that the panel's positions now refer to
 // (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
@@ -209,10 +229,6 @@ __global__ void k_pmap_init(int64_t* pmap, int64_t m) {
         pmap[i] = i;
 }
 
-void launch_leaf_pivot(cudaStream_t s, const Mat& A, int64_t wl, int lw, int first, int leaf_in_panel,
-                       int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off) {
-    k_leaf_pivot<<<1, 1024, 0, s>>>(A, wl, lw, first, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off);
-}
 
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch) {
     // rows are 128-byte aligned (stride % 16 words == 0): 16-byte accesses, ~1024 CTAs
@@ -222,9 +238,6 @@ void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* s
     launch_pdl(k_perm_put, grid, dim3(256), 0, s, A, nwords, st, pmap, static_cast<const uint64_t*>(scratch));
 }
 
-void launch_leaf_tables(cudaStream_t s, PlsState* st, int leaf_in_panel) {
-    k_leaf_tables<<<16, 256, 0, s>>>(st, leaf_in_panel);
-}
 
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {
     int64_t g = (m + 255) / 256;

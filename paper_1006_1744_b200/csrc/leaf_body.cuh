@@ -96,11 +96,8 @@ __device__ __forceinline__ int32_t pick(const int32_t (&v)[S], int s) {
 // past the window; otherwise the leaf falls back to the general search below
 // (rank-deficient / sparse inputs).
 //
-// With rw1 > wl + 1 the pivot rows are also solved over the rest of the panel
-// (words wl+1..rw1): U = L11^{-1} A12 (trsm_lower_left_unit, mul.cpp:109-131), with
-// L11 the pivot rows' L bits and A12 the pre-leaf words of the rows that became the
-// pivots (their pre-leaf slots), and written back.  Returns false (having written
-// nothing) when it falls back.
+// The panel kernel (panel.cu, pipe_fast_leaf) drives these warps on its carried
+// 128-row window and then solves the pivot rows over the rest of the panel.
 struct U128 {
     uint64_t lo, hi;
 };
@@ -405,10 +402,13 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                     C.lo ^= a ? elo : 0ull;
                     C.hi ^= a ? ehi : 0ull;
                 }
-                // (a no-op step writes slot t, which the next real step overwrites; readers
-                // only read below the published count)
-                F.step_m[t] = make_ulonglong2(clo, mhi);
-                F.step_c[t] = c;
+                // only real steps are stored (predicated, not branched): every lane then
+                // writes identical values, so a reader acquiring the count from any lane's
+                // release sees the step whichever lane's store it observes
+                if (!zero) {
+                    F.step_m[t] = make_ulonglong2(clo, mhi);
+                    F.step_c[t] = c;
+                }
                 t += zero ? 0 : 1;
                 tb = zero ? tb : tb << 1;
                 tm = zero ? tm : tm << 1;
@@ -460,207 +460,6 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
     }
 }
 
-static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, int lw, int first_in_panel,
-                                                    int leaf_in_panel, int panel_bits, PlsState* st, int64_t* P,
-                                                    int64_t* Qp, int64_t* pmap, int64_t qcol_off, int64_t rw1,
-                                                    uint64_t* scratch) {
-    constexpr int kFW = 128;
-    __shared__ FastSmem F;
-    // scratch (dynamic smem, >= (128 + 256) * 15 words when solving): window rows'
-    // pre-leaf rest words (row form), then the 4-bit tables over the pivot rows' ones
-    uint64_t* const Frest = scratch;
-    uint64_t* const Ft16 = scratch + 128 * 15;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t m = A.m, stride = A.stride;
-    const int64_t base = st->r;
-    const int64_t span = m - base;
-    const int nrest = (scratch && rw1 > wl + 1) ? static_cast<int>(rw1 - wl - 1) : 0;  // <= 15
-
-    if (tid < kFW) F.phys[tid] = tid < span ? ldi(pmap + base + tid) : -1;
-    __syncthreads();
-    F2_STAMP(st, 15);
-    if (warp < 8) {  // leaf word -> column form: task = (slot block rb, column half h)
-        const int rb = warp & 3, h = warp >> 2;
-        const int64_t ph = F.phys[rb * 32 + lane];
-        const uint64_t w = ph >= 0 ? ldw(A.w + ph * stride + wl) : 0ull;
-        F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
-    }
-    for (int i = tid; i < kFW * nrest; i += blockDim.x) {  // rest of the panel, row form
-        const int sl = i / nrest, k = i - sl * nrest;
-        const int64_t ph = F.phys[sl];
-        Frest[sl * 15 + k] = ph >= 0 ? ldw(A.w + ph * stride + wl + 1 + k) : 0ull;
-    }
-    __syncthreads();
-    F2_STAMP(st, 16);
-
-#ifdef F2_ONE_WARP_PIVOTS
-    if (warp == 0) warp0_pivots(F, lw, base + kFW < m, scratch != nullptr, st);
-#else
-    if (warp < 3) two_warp_pivots(F, lw, base + kFW < m, scratch != nullptr);
-#endif
-    __syncthreads();
-    F2_STAMP(st, 18);
-    const int kb = F.final_kb;
-    if (kb < 0) return false;
-
-#ifdef F2_ONE_WARP_PIVOTS
-    if (tid < kFW) {
-#else
-    if (false) {
-#endif
-        // slot sources: walk the transpositions backwards (LAPACK order, perm.cpp:8-16)
-        int x = tid;
-        for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
-            int pv[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pv[i] = F.step_p[u0 + i];
-#pragma unroll
-            for (int i = 7; i >= 0; --i) {
-                const int u = u0 + i;
-                if (u < kb) x = x == u ? pv[i] : (x == pv[i] ? u : x);
-            }
-        }
-        F.src[tid] = x;
-    } else if (tid < kFW + 64) {
-        // finalize basis for the update (see panel.cu): the elimination chain of byte
-        // group g (gauss.cpp:47-49) run on the single bit b
-        const int e = tid - kFW, g = e >> 3, b = e & 7;
-        int lo = 0, hi = kb;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (F.step_c[mid] < 8 * g) lo = mid + 1;
-            else hi = mid;
-        }
-        uint64_t x = 1ull << (8 * g + b), corr = 0;
-        for (int l = lo; l < kb && F.step_c[l] < 8 * g + 8; ++l) {
-            const int q = F.step_c[l];
-            if ((x >> q) & 1ull) {
-                const uint64_t ul = F.uf[l] & above(q);
-                x ^= ul;
-                corr ^= ul;
-            }
-        }
-        st->fbasis[e] = corr;
-    } else if (scratch && tid >= 320 && tid < 384) {
-        // rows of L11^{-1} in raw leaf-column coordinates (pivot index t -> column q_t)
-        const int l = tid - 320;
-        uint64_t r = 0;
-        if (l < kb) {
-            uint64_t lv = F.linv[l];
-            while (lv) {
-                const int tt = __ffsll(static_cast<long long>(lv)) - 1;
-                lv &= lv - 1;
-                r |= 1ull << F.step_c[tt];
-            }
-        }
-        F.rraw[l] = r;
-        F.posc[l] = -1;
-    } else if (tid >= 256 && tid < 320) {
-        const int l = tid - 256;
-        const bool in = l < kb;
-        const int q = in ? F.step_c[l] : 64;
-        st->ustrict[l] = in ? F.uf[l] & above(q) : 0ull;
-        st->ufull[l] = in ? F.uf[l] : 0ull;
-        st->q[l] = q;
-    }
-    if (first_in_panel)
-        for (int i = tid; i < panel_bits; i += blockDim.x) st->brow[i] = -1;
-    __syncthreads();
-    F2_STAMP(st, 19);
-    if (scratch) {
-        // the panel TRSM's bytewise map c -> c * L11^{-1} for this leaf (see trsm.cu):
-        // lmap[g][v] = xor over bits b of v of the L11^{-1} row of the pivot at column 8g+b
-        if (tid < kb) F.posc[F.step_c[tid]] = tid;
-        __syncthreads();
-        for (int i = tid; i < 8 * 256; i += blockDim.x) {
-            const int g = i >> 8, v = i & 255;
-            uint64_t x = 0;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int l = F.posc[8 * g + b];
-                if (((v >> b) & 1) && l >= 0) x ^= F.rraw[l];
-            }
-            st->lmap[leaf_in_panel][g][v] = x;
-        }
-    }
-    const int mv0 = first_in_panel ? 0 : static_cast<int>(st->nmoved);
-    const int64_t pkb = first_in_panel ? 0 : st->panel_kb;
-    // re-mapped positions (pre-leaf pmap values are in F.phys)
-    int moved = 0, off = 0;
-    if (warp < 4) {
-        const int s = tid;
-        moved = s < span && F.src[s] != s;
-        const unsigned bm = __ballot_sync(FULL, moved);
-        off = __popc(bm & ((1u << lane) - 1));
-        if (lane == 0) F.wcount[warp] = __popc(bm);
-    }
-    // pivot rows: final leaf word; P, Q; the panel's pivot bookkeeping
-    for (int l = tid; l < kb; l += blockDim.x) {
-        A.w[F.phys[F.src[l]] * stride + wl] = F.uf[l];
-        P[base + l] = base + F.step_p[l];
-        Qp[base + l] = qcol_off + wl * 64 + F.step_c[l];
-        st->panel_q[pkb + l] = leaf_in_panel * 64 + F.step_c[l];
-        st->brow[leaf_in_panel * 64 + F.step_c[l]] = base + l;
-    }
-    F2_STAMP(st, 21);
-    // solved rest words of the pivot rows: U_l = sum over t of Linv[l][t] A12_t with
-    // A12_t = the pre-leaf rest words of the row that became pivot t (slot src_t):
-    // sixteen 4-bit tables over A12 (T16[g][e] = xor of A12_{4g+b}, b in e), then 16
-    // independent lookups per output word
-    for (int i = tid; i < 16 * 16 * nrest; i += blockDim.x) {
-        const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
-        uint64_t v = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if (((e >> b) & 1) && 4 * g + b < kb) v ^= Frest[F.src[4 * g + b] * 15 + k];
-        Ft16[ge * 15 + k] = v;
-    }
-    __syncthreads();
-    for (int i = tid; i < kb * nrest; i += blockDim.x) {
-        const int l = i / nrest, k = i - l * nrest;
-        const uint64_t lv = F.linv[l];
-        uint64_t acc = 0;
-#pragma unroll
-        for (int g = 0; g < 16; ++g) acc ^= Ft16[((g << 4) | static_cast<int>((lv >> (4 * g)) & 15u)) * 15 + k];
-        A.w[F.phys[F.src[l]] * stride + wl + 1 + k] = acc;
-        st->uleaf[l][k] = acc;
-    }
-    F2_STAMP(st, 22);
-    __syncthreads();
-    F2_STAMP(st, 23);
-    if (warp < 4 && moved) {
-        int o = off;
-        for (int w2 = 0; w2 < warp; ++w2) o += F.wcount[w2];
-        pmap[base + tid] = F.phys[F.src[tid]];
-        st->moved[mv0 + o] = base + tid;
-    }
-    if (warp == 0) {
-        uint64_t mk = 0;
-        for (int l = lane; l < kb; l += 32) mk |= 1ull << F.step_c[l];
-        mk = warp_or64(mk);
-        int nm = 0;
-        for (int w2 = 0; w2 < 4; ++w2) nm += F.wcount[w2];
-        int hi = -1;  // highest re-mapped slot
-        for (int w2 = 3; w2 >= 0 && hi < 0; --w2)
-            if (F.wcount[w2]) hi = w2;
-        if (lane == 0) {
-            st->leaf_mask = mk;
-            st->nmoved = mv0 + nm;
-            const int64_t h = hi < 0 ? 0 : base + 32 * (hi + 1);
-            const int64_t prev = first_in_panel ? 0 : st->pmap_hi;
-            st->pmap_hi = h > prev ? h : prev;
-            st->leaf_r = base;
-            st->leaf_kb = kb;
-            st->r = base + kb;
-            if (first_in_panel) st->panel_r = base;
-            st->panel_kb = pkb + kb;
-        }
-    }
-    __syncthreads();
-    F2_STAMP(st, 20);
-    return true;
-}
-
 // One CTA of 1024 threads.  Warp 0 keeps a sliding window of 32 consecutive
 // positions (lane l holds position bb + l), eagerly eliminated, and finds pivots
 // there without block-level synchronisation:
@@ -675,14 +474,10 @@ static __device__ __noinline__ bool leaf_pivot_fast(const Mat& A, int64_t wl, in
 //
 // Positions are relative to base = st->r; `src` is the relative (pre-leaf)
 // position of the content a lane holds.  Rows are read through pmap.
-// Returns true when the fast path ran (and, for rw1 > wl + 1, also solved the pivot
-// rows over words wl+1..rw1); false after the general search.
-static __device__ __noinline__ bool leaf_pivot_body(const Mat& A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel,
+// The general search of the panel kernel (its fast window could not decide the leaf).
+static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel,
                                 int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap,
-                                int64_t qcol_off, int64_t rw1, uint64_t* scratch, bool try_fast = true) {
-    if (try_fast && leaf_pivot_fast(A, wl, lw, first_in_panel, leaf_in_panel, panel_bits, st, P, Qp, pmap, qcol_off,
-                                    rw1, scratch))
-        return true;
+                                int64_t qcol_off) {
     __syncthreads();
     __shared__ uint64_t s_u[64];
     __shared__ uint64_t s_uf[64];
@@ -1033,69 +828,6 @@ static __device__ __noinline__ bool leaf_pivot_body(const Mat& A, int64_t wl, in
         st->ustrict[l] = l < kb ? s_u[l] : 0ull;
         st->ufull[l] = l < kb ? s_uf[l] : 0ull;
         st->q[l] = l < kb ? s_q[l] : 64;
-    }
-    return false;
-}
-
-// Per 8-column group of the leaf word: the finalize table F[g][v] (correction the
-// group's pivots apply to a word whose byte g reads v, sequentially as gauss_pls
-// does) and the index map M[g][e] = xor_{b in e} R[b], R the rows of the group's
-// inverse 8x8 L block (see trsm.cu).  k_leaf_update consumes both.  One thread per
-// table entry: entries [e0, 4096) step `es` (thread-block `tid` order).
-static __device__ __noinline__ void leaf_tables_body(PlsState* st, int e0, int es) {
-    __shared__ uint64_t s_u[64], s_uf[64];
-    __shared__ int s_q[64];
-    __shared__ int s_gs[9];
-    const int tid = threadIdx.x;
-    const int kb = static_cast<int>(st->leaf_kb);
-    if (kb == 0) return;
-    if (tid < 64) {
-        s_u[tid] = st->ustrict[tid];
-        s_uf[tid] = st->ufull[tid];
-        s_q[tid] = st->q[tid];
-    }
-    __syncthreads();
-    F2_STAMP(st, 20);
-    if (tid <= 8) {
-        int lo = 0;
-        while (lo < kb && s_q[lo] < 8 * tid) ++lo;
-        s_gs[tid] = lo;
-    }
-    __syncthreads();
-    F2_STAMP(st, 21);
-
-    for (int i = e0; i < 4096; i += es) {
-    const int which = i >> 11, g = (i >> 8) & 7, v = i & 255;
-    const int g0 = s_gs[g], g1 = s_gs[g + 1];
-    if (which == 0) {
-        uint64_t x = static_cast<uint64_t>(v) << (8 * g), corr = 0;
-        for (int l = g0; l < g1; ++l)
-            if ((x >> s_q[l]) & 1ull) {
-                x ^= s_u[l];
-                corr ^= s_u[l];
-            }
-        st->leaf_F[g][v] = corr;
-    } else {
-        uint32_t Rb[8];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) Rb[b] = 0;
-        for (int l = g0; l < g1; ++l) {
-            const int sb = s_q[l] - 8 * g;
-            const uint32_t c = static_cast<uint32_t>(s_uf[l] >> (8 * g)) & ((1u << sb) - 1u);
-            uint32_t R = 1u << sb;
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                if ((c >> b) & 1u) R ^= Rb[b];
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                if (b == sb) Rb[b] = R;
-        }
-        uint32_t Mv = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-            if ((v >> b) & 1) Mv ^= Rb[b];
-        st->leaf_M[g][v] = static_cast<uint8_t>(Mv);
-    }
     }
 }
 

@@ -103,13 +103,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_table_apply(TableApply p) {
         if (pk == 0) return;
         c_r0 = a_r0 = pr + pk;
     }
-    if (p.idle_ctas > 0 && p.row_tile0 + static_cast<int64_t>(blockIdx.y) < 0) {  // placeholder rows: keep
-        if (static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) < p.idle_ctas) {  // the SM until the side kernel is queued
-            const unsigned long long t0 = gtimer();
-            while (gtimer() - t0 < static_cast<unsigned long long>(p.idle_ns)) __nanosleep(1000);
-        }
-        return;
-    }
     const int64_t row_base = c_r0 + (p.row_tile0 + static_cast<int64_t>(blockIdx.y)) * kTM;
 #ifdef F2_TIMELINE
     const int tl_slot = p.st ? static_cast<int>((p.aw0 / 16) & 127) : -1;  // panel index (W = 1024)
@@ -398,10 +391,9 @@ static size_t table_apply_smem() { return kSmem; }
 // across gridDim.z CTAs (atomic XOR into C) so the tail wave is short.  expect_rows
 // (the caller's estimate of the device-side row count; <= 0: unknown) only steers
 // the split; correctness never depends on it.
-void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows, int idle_ctas) {
+void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t expect_rows) {
     if (t.cw1 <= t.cw0 || t.kbits <= 0) return;
-    static const bool mmpf_stream = !std::getenv("F2_NO_MMPF_STREAM");
-    if (t.kw == 1 && idle_ctas == 0 && mmpf_stream) {  // K <= 64: HBM-streaming MMPF kernel
+    if (t.kw == 1) {  // K <= 64: HBM-streaming MMPF kernel
         launch_mmpf_apply(s, t, nsm);
         return;
     }
@@ -412,7 +404,7 @@ void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t ex
     const int64_t nrt = (rows + kTM - 1) / kTM;
     int64_t y0 = nrt;
     int splitk = 1;
-    if (expect_rows > 0 && nsm > 0 && t.kw >= 2 && !std::getenv("F2_NO_KSPLIT")) {
+    if (expect_rows > 0 && nsm > 0 && t.kw >= 2) {
         const int64_t ert = (expect_rows + kTM - 1) / kTM;  // expected row tiles
         const int64_t tiles = ert * nct;
         const int64_t full_waves = tiles / nsm;
@@ -430,23 +422,12 @@ void launch_table_apply(cudaStream_t s, const TableApply& t, int nsm, int64_t ex
     if (y0 > 0) {
         TableApply a = t;
         a.row_tile0 = 0;
-        a.idle_ctas = 0;
-        static const int64_t idle_ns = [] {
-            const char* e = std::getenv("F2_IDLE_NS");
-            return e ? std::atoll(e) : 15000ll;
-        }();
-        if (idle_ctas > 0 && idle_ns > 0) {  // extra leading grid rows of placeholders
-            a.row_tile0 = -((idle_ctas + nct - 1) / nct);
-            a.idle_ctas = idle_ctas;
-            a.idle_ns = idle_ns;
-        }
         k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(y0 - a.row_tile0), 1), kThreads,
                         table_apply_smem(), s>>>(a);
     }
     if (y0 < nrt) {
         TableApply b = t;
         b.row_tile0 = y0;
-        b.idle_ctas = 0;
         k_table_apply<<<dim3(static_cast<unsigned>(nct), static_cast<unsigned>(nrt - y0), static_cast<unsigned>(splitk)),
                         kThreads, table_apply_smem(), s>>>(b);
     }

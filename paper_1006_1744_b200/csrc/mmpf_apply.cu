@@ -185,13 +185,12 @@ __global__ void __launch_bounds__(k7Threads, 1) k_mmpf_apply7(TableApply p, int 
 }
 
 namespace {
-int g_mmpf_rblock = 0;  // F2_MMPF_RBLOCK: rows per work item (tuning experiments)
 
 template <int NB, int NTAB>
 void launch_k7n(cudaStream_t s, const TableApply& t, int nsm) {
     // rows per item: 2048 while the table rebuild is cheap (K <= 16: 5.5 vs 5.3 TB/s at
     // 8192), 8192 above (K = 64: 4.25 vs 3.60 TB/s at 2048), over a 1 GiB C
-    const int rb = g_mmpf_rblock > 0 ? g_mmpf_rblock : (NB * NTAB <= 16 ? 2048 : 8192);
+    const int rb = NB * NTAB <= 16 ? 2048 : 8192;  // rows per work item
     k_mmpf_apply7<NB, NTAB><<<nsm, k7Threads, k7Smem<NB>(NTAB), s>>>(t, rb);
 }
 template <int NB, int NTAB>
@@ -235,7 +234,6 @@ void setup_mmpf_apply_kernels() {
     setup_k7<7, 8>();
     setup_k7<7, 9>();
     setup_k7<7, 10>();
-    if (const char* e = std::getenv("F2_MMPF_RBLOCK")) g_mmpf_rblock = std::atoi(e);
 }
 
 }  // namespace f2g

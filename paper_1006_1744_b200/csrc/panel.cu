@@ -404,53 +404,6 @@ __device__ void publish_from_state(const PlsState* st, PlsState::Packet* pk) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kPT, 1)
-k_panel_leaves(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* P, int64_t* Qp,
-               int64_t* pmap, int64_t qcol_off, unsigned* bar) {
-    extern __shared__ __align__(16) uint64_t dsm[];
-    __shared__ LeafInfo L;
-    uint64_t* tab = dsm;  // CTA 0's fallback solve table, or T4
-    uint64_t* X = tab + kTab;
-    uint64_t* F = X + 64 * kW;
-    const int nleaves = (width + 63) / 64;
-    unsigned target = 0;
-    for (int j = 0; j < nleaves; ++j) {
-        const int64_t wl = pw0 + j;
-        const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
-#ifdef F2_PANEL_PROFILE
-        if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = (pw0 == 0 && j == 1);
-        __syncthreads();
-#endif
-        F2_STAMP(st, 0);
-        if (blockIdx.x == 0) {
-            const bool solved = leaf_pivot_body(A, wl, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1, dsm);
-            __syncthreads();
-            F2_STAMP(st, 1);
-            if (!solved) {  // the general search ran: basis, panel-TRSM map and solve here
-                load_leaf(st, L);
-                if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];
-                leaf_lmap(st, L, j, X);
-                solve_pivot_rows(A, wl + 1, pw1, pmap, L, X, tab, st);
-            }
-            F2_STAMP(st, 2);
-            publish_from_state(st, &st->pk[0]);
-        }
-        grid_barrier(bar, target);
-        F2_STAMP(st, 3);
-        if (__ldcg(reinterpret_cast<const long long*>(&st->pk[0].kb)) != 0) {
-            worker_prep(&st->pk[0], L, X, F, tab);
-            F2_STAMP(st, 4);
-            const int64_t rows = A.m - L.lo;
-            const int ntiles = rows > 0 ? static_cast<int>((rows + kRows - 1) / kRows) : 0;
-            for (int ty = blockIdx.x; ty < ntiles; ty += gridDim.x) update_tile(A, wl, pw1, pmap, L, ty, F, tab, st);
-        }
-        F2_STAMP(st, 5);
-#ifdef F2_PANEL_PROFILE
-        if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = 0;
-#endif
-        grid_barrier(bar, target);
-    }
-}
 
 
 // ---- pipelined schedule (k_panel_pipe) --------------------------------------------------
@@ -873,8 +826,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 }
             } else if (state == S_GENERAL) {
                 const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
-                leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off, pw1, nullptr,
-                                false);
+                leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off);
                 __syncthreads();
                 load_leaf(st, L);
                 if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];
@@ -943,24 +895,8 @@ void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int
     cudaLaunchKernelEx(&cfg, k_panel_pipe, A, pw0, width, pw1, st, P, Qp, pmap, qcol_off, bar);
 }
 
-void launch_panel_leaves(cudaStream_t s, const Mat& A, int64_t pw0, int width, int64_t pw1, PlsState* st,
-                         int64_t* P, int64_t* Qp, int64_t* pmap, int64_t qcol_off, unsigned* bar, int nsm) {
-    cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(nsm));
-    cfg.blockDim = dim3(kPT);
-    cfg.dynamicSmemBytes = kSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_panel_leaves, A, pw0, width, pw1, st, P, Qp, pmap, qcol_off, bar);
-}
 
 void setup_panel_kernels() {
-    cudaFuncSetAttribute(k_panel_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
     cudaFuncSetAttribute(k_panel_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem));
 }
 

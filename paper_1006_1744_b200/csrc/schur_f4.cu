@@ -206,12 +206,10 @@ struct F4Walk {
     }
 };
 
-// dbg: bits 16+ = tiles per claimed chunk (0: from the launch size; F2_F4_CHUNK), bits 8-15 =
-// the largest chunk of the launch-size rule (0: 64; F2_F4_CHUNK_CAP)
 template <int kFRing, int EPW>
 __global__ void __launch_bounds__(f4_threads(EPW), 1)
 k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__ Bx, unsigned* __restrict__ claim,
-           unsigned long long* tl, int dbg) {
+           unsigned long long* tl) {
     pdl_wait();
     constexpr int NST = kFMaxStages;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -234,10 +232,9 @@ k_schur_f4(F4Job jb, const uint8_t* __restrict__ Ax, const uint8_t* __restrict__
     // chunk: k = ceil(tiles per CTA / cap) chunks per CTA of equal size <= cap (long runs on one
     // B tile, at most one tile of imbalance when the grid divides the work evenly)
     const int64_t per_cta = (T + gridDim.x - 1) / gridDim.x;
-    const int cap = (dbg >> 8) & 255 ? (dbg >> 8) & 255 : 64;
+    constexpr int cap = 64;
     const int64_t kch = (per_cta + cap - 1) / cap;
-    int chunk = static_cast<int>((T + gridDim.x * kch - 1) / (gridDim.x * kch));
-    if (dbg >> 16) chunk = dbg >> 16;
+    const int chunk = static_cast<int>((T + gridDim.x * kch - 1) / (gridDim.x * kch));
     const int64_t nchunks = (T + chunk - 1) / chunk;
 
     if (warp == 0) {
@@ -430,8 +427,7 @@ size_t schur_f4_b_bytes(int64_t words) {
     return static_cast<size_t>((2 * words + kFHW - 1) / kFHW) * kFMaxStages * kFBStage;
 }
 
-int g_f4_ring = 6, g_f4_dbg = 0, g_f4_epw = 1;
-bool g_pdl = !std::getenv("F2_NO_PDL");  // kernels.cuh: launch_pdl
+bool g_pdl = true;  // kernels.cuh: launch_pdl (Tuning::pdl)
 
 // K is always padded to kFMaxStages stages (zero nibbles): the B ring then spans exactly
 // one tile, which the loader's B-reload waits rely on (one mbarrier phase per tile)
@@ -443,30 +439,13 @@ void launch_schur_f4(cudaStream_t s, const F4Job& jb, const uint8_t* Ax, uint8_t
                      unsigned long long* tl) {
     if (jb.cw1 <= jb.cw0) return;
     launch_pdl(k_f4_expand_b, dim3(nsm * 8), dim3(256), 0, s, jb, Bx, kFMaxStages, claim);
-    const int r6 = g_f4_ring == 6, e1 = g_f4_epw == 1;
-    if (r6 && e1)
-        launch_pdl(k_schur_f4<6, 1>, dim3(nsm), dim3(f4_threads(1)), f4_smem(6), s, jb, Ax,
-                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
-    else if (r6)
-        launch_pdl(k_schur_f4<6, 4>, dim3(nsm), dim3(f4_threads(4)), f4_smem(6), s, jb, Ax,
-                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
-    else if (e1)
-        launch_pdl(k_schur_f4<4, 1>, dim3(nsm), dim3(f4_threads(1)), f4_smem(4), s, jb, Ax,
-                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
-    else
-        launch_pdl(k_schur_f4<4, 4>, dim3(nsm), dim3(f4_threads(4)), f4_smem(4), s, jb, Ax,
-                   static_cast<const uint8_t*>(Bx), claim, tl, g_f4_dbg);
+    // 6-deep A ring, 16 epilogue warps (4-deep and 4 tiles per epilogue warp measured slower)
+    launch_pdl(k_schur_f4<6, 1>, dim3(nsm), dim3(f4_threads(1)), f4_smem(6), s, jb, Ax, static_cast<const uint8_t*>(Bx),
+               claim, tl);
 }
 
 void setup_schur_f4_kernels() {
-    cudaFuncSetAttribute(k_schur_f4<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(4)));
-    cudaFuncSetAttribute(k_schur_f4<6, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
-    cudaFuncSetAttribute(k_schur_f4<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(4)));
     cudaFuncSetAttribute(k_schur_f4<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f4_smem(6)));
-    if (const char* e = std::getenv("F2_F4_EPW")) g_f4_epw = std::atoi(e);
-    if (const char* e = std::getenv("F2_F4_CHUNK")) g_f4_dbg |= std::atoi(e) << 16;
-    if (const char* e = std::getenv("F2_F4_CHUNK_CAP")) g_f4_dbg |= (std::atoi(e) & 255) << 8;
-    if (const char* e = std::getenv("F2_F4_RING")) g_f4_ring = std::atoi(e);
 }
 
 }  // namespace f2g

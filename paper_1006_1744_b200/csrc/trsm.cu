@@ -216,150 +216,16 @@ void launch_pivot_trsm(cudaStream_t s, const Mat& A, int64_t coef_w0, int coef_w
 
 
 // Panel TRSM by leaf blocks.  The panel's pivot rows form 64-pivot blocks (one per
-// leaf); k_leaf_tables left, per leaf j, the bytewise map c -> c * L_jj^{-1}
+// leaf); the panel kernel (or k_panel_lmaps) left, per leaf j, the bytewise map c -> c * L_jj^{-1}
 // (st->lmap[j]).  Block step j: 8 tables over block j's rows as they are now (raw
 // positions 64j..64j+63), then every row t of block j and after it adds
 // xor_g T_g[byte_g(M)] with M = c_t * L_jj^{-1} (c_t = its coefficients for block j,
 // masked below its own pivot inside block j).  That equals forward substitution with
 // the whole block (the block's rows come out solved, later rows get the block's
 // solved rows), so the panel needs one step per leaf instead of one per 8 pivots.
-namespace {
-constexpr int kPTW = 4;  // target words per CTA
-}
-
-__global__ void __launch_bounds__(512, 1)
-k_panel_trsm(Mat A, Mat Cf, int64_t coef_w0, int nleaves, int64_t tw0, int64_t tw1, const PlsState* st) {
-    extern __shared__ __align__(16) uint64_t smem[];
-    const int rows_cap = nleaves * 64;
-    uint64_t* X = smem;                                   // [rows_cap][kPTW]
-    uint64_t* T = X + rows_cap * kPTW;                    // [8][256][kPTW]
-    uint64_t* Lm = T + 8 * 256 * kPTW;                    // [8][256]
-    uint64_t* cw = Lm + 8 * 256;                          // [rows_cap]
-    int32_t* sq = reinterpret_cast<int32_t*>(cw + rows_cap);   // [rows_cap]
-    int16_t* posrow = reinterpret_cast<int16_t*>(sq + rows_cap);  // [rows_cap] raw col -> pivot index
-    int32_t* bstart = reinterpret_cast<int32_t*>(posrow + rows_cap);  // [nleaves + 1]
-
-    const int nk = static_cast<int>(st->panel_kb);
-    const int64_t r0 = st->panel_r;
-    if (nk <= 1) return;
-    const int64_t tb = tw0 + static_cast<int64_t>(blockIdx.x) * kPTW;
-    if (tb >= tw1) return;
-    const int ntw = static_cast<int>(tw1 - tb < kPTW ? tw1 - tb : kPTW);
-    const int tid = threadIdx.x, nth = blockDim.x;
-
-    for (int t = tid; t < nk; t += nth) sq[t] = st->panel_q[t];
-    for (int i = tid; i < rows_cap; i += nth) posrow[i] = -1;
-    for (int i0 = tid; i0 < nk * kPTW; i0 += 4 * nth) {
-        uint64_t v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = i0 + u * nth, t = i / kPTW, j = i % kPTW;
-            v[u] = (i < nk * kPTW && j < ntw) ? A.w[(r0 + t) * A.stride + tb + j] : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i0 + u * nth < nk * kPTW) X[i0 + u * nth] = v[u];
-    }
-    __syncthreads();
-    for (int t = tid; t < nk; t += nth) posrow[sq[t]] = static_cast<int16_t>(t);
-    for (int j = tid; j <= nleaves; j += nth) {
-        int lo = 0, hi = nk;  // first t with sq[t] >= 64j
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (sq[mid] < 64 * j) lo = mid + 1;
-            else hi = mid;
-        }
-        bstart[j] = lo;
-    }
-    __syncthreads();
-
-    // block j's inverse map and every row's coefficient word for the block, loaded
-    // into registers one block ahead (4 + 2 words per thread at 512 threads)
-    constexpr int kLmPer = 8 * 256 / 512, kCwPer = kMaxTrsmBits / 512;
-    uint64_t pf_lm[kLmPer], pf_cw[kCwPer];
-    auto prefetch = [&](int j) {
-        if (j >= nleaves) return;
-        const int t0 = bstart[j];
-#pragma unroll
-        for (int u = 0; u < kLmPer; ++u) pf_lm[u] = (&st->lmap[j][0][0])[tid + u * 512];
-#pragma unroll
-        for (int u = 0; u < kCwPer; ++u) {
-            const int t = t0 + tid + u * 512;
-            pf_cw[u] = t < nk ? Cf.w[(r0 + t) * Cf.stride + coef_w0 + j] : 0ull;
-        }
-    };
-    prefetch(0);
-    for (int j = 0; j < nleaves; ++j) {
-        const int t0 = bstart[j], t1 = bstart[j + 1];
-        if (t0 == t1) {
-            prefetch(j + 1);
-            continue;
-        }
-#pragma unroll
-        for (int u = 0; u < kLmPer; ++u) Lm[tid + u * 512] = pf_lm[u];
-#pragma unroll
-        for (int u = 0; u < kCwPer; ++u) {
-            const int t = t0 + tid + u * 512;
-            if (t < nk) cw[t] = pf_cw[u];
-        }
-        prefetch(j + 1);
-        // 8 tables over block j's rows as they are now: thread = (table g, word w, low nibble)
-        {
-            const int g = tid >> 6, w = (tid >> 4) & 3, el = tid & 15;
-            uint64_t v[8];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int l = posrow[64 * j + 8 * g + b];
-                v[b] = l >= 0 ? X[l * kPTW + w] : 0ull;
-            }
-            uint64_t x = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((el >> b) & 1) x ^= v[b];
-            uint64_t* tg = T + g * 256 * kPTW + w;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (k) x ^= v[4 + ((k & 1) ? 0 : ((k & 2) ? 1 : ((k & 4) ? 2 : 3)))];
-                const int eh = k ^ (k >> 1);
-                tg[(eh * 16 + el) * kPTW] = x;
-            }
-        }
-        __syncthreads();
-        for (int t = t0 + tid; t < nk; t += nth) {
-            uint64_t c = cw[t];
-            if (t < t1) c &= (1ull << (sq[t] - 64 * j)) - 1ull;
-            uint64_t M = 0;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) M ^= Lm[g * 256 + ((c >> (8 * g)) & 0xffu)];
-            uint4 a0 = *reinterpret_cast<uint4*>(X + t * kPTW), a1 = *reinterpret_cast<uint4*>(X + t * kPTW + 2);
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const uint64_t* e = T + (g * 256 + ((M >> (8 * g)) & 0xffu)) * kPTW;
-                const uint4 b0 = *reinterpret_cast<const uint4*>(e), b1 = *reinterpret_cast<const uint4*>(e + 2);
-                a0.x ^= b0.x; a0.y ^= b0.y; a0.z ^= b0.z; a0.w ^= b0.w;
-                a1.x ^= b1.x; a1.y ^= b1.y; a1.z ^= b1.z; a1.w ^= b1.w;
-            }
-            *reinterpret_cast<uint4*>(X + t * kPTW) = a0;
-            *reinterpret_cast<uint4*>(X + t * kPTW + 2) = a1;
-        }
-        __syncthreads();
-    }
-    for (int i = tid; i < nk * kPTW; i += nth) {
-        const int t = i / kPTW, jj = i % kPTW;
-        if (jj < ntw) A.w[(r0 + t) * A.stride + tb + jj] = X[i];
-    }
-}
-
-static size_t panel_trsm_smem(int nleaves) {
-    const size_t rows = static_cast<size_t>(nleaves) * 64;
-    return sizeof(uint64_t) * (rows * kPTW + 8 * 256 * kPTW + 8 * 256 + rows) + sizeof(int32_t) * rows +
-           sizeof(int16_t) * rows + sizeof(int32_t) * (nleaves + 8);
-}
-
-
-// The same panel TRSM on 512-bit column strips (kPTW8 = 8 words): one wave of CTAs
-// at 64K columns, and every table entry / row slice is 64 B read by 4 lanes with
-// 16-byte accesses (the 4-word version's 32-B entries read by single lanes conflict).
+// 512-bit column strips (kPTW8 = 8 words): one wave of CTAs at 64K columns, and every
+// table entry / row slice is 64 B read by 4 lanes with 16-byte accesses (a 4-word
+// version's 32-B entries read by single lanes conflicted).
 namespace {
 constexpr int kPTW8 = 8;
 }
@@ -500,14 +366,8 @@ static size_t panel_trsm8_smem(int nleaves) {
 void launch_panel_trsm(cudaStream_t s, const Mat& A, const Mat& Cf, int64_t coef_w0, int nleaves, int64_t tw0,
                        int64_t tw1, const PlsState* st) {
     if (tw1 <= tw0) return;
-    static const bool narrow = std::getenv("F2_TRSM4") != nullptr;
-    if (narrow) {
-        const int grid = static_cast<int>((tw1 - tw0 + kPTW - 1) / kPTW);
-        k_panel_trsm<<<grid, 512, panel_trsm_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
-    } else {
-        const int grid = static_cast<int>((tw1 - tw0 + kPTW8 - 1) / kPTW8);
-        k_panel_trsm8<<<grid, 512, panel_trsm8_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
-    }
+    const int grid = static_cast<int>((tw1 - tw0 + kPTW8 - 1) / kPTW8);
+    k_panel_trsm8<<<grid, 512, panel_trsm8_smem(nleaves), s>>>(A, Cf, coef_w0, nleaves, tw0, tw1, st);
 }
 
 // The panel TRSM from a snapshot (look-ahead schedule): the M words come precomputed
@@ -682,8 +542,6 @@ void setup_trsm_kernels() {
                          static_cast<int>(panel_trsm_snap_smem<1>(kMaxTrsmBits / 64)));
     cudaFuncSetAttribute(k_panel_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(panel_trsm8_smem(kMaxTrsmBits / 64)));
-    cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(panel_trsm_smem(kMaxTrsmBits / 64)));
     cudaFuncSetAttribute(k_pivot_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(trsm_smem(kMaxTrsmBits / 64)));
 }
