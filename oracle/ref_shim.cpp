@@ -14,6 +14,7 @@
 //   mul_m4rm / addmul   (proj/src/mul.cpp:90-107)
 //   trsm_*_left_unit    (proj/src/mul.cpp:109-157)
 //   BitMatrix::randomize(proj/src/bitmat.cpp:136-154)
+//   Permutation::apply_rows[_inverse], compress_columns (proj/src/perm.cpp:25-60)
 // Host arrays use the reference's packing: row-major, stride = ceil(ncols/64)
 // 64-bit words, LSB = lowest column (bitmat.hpp:3-6).
 #include <cstdint>
@@ -61,6 +62,12 @@ int guard(F&& f) {
     } catch (...) {
         return 9;
     }
+}
+
+Permutation perm_of(const uint64_t* v, size_t len) {
+    Permutation p = Permutation::identity(len);
+    for (size_t i = 0; i < len; ++i) p[i] = static_cast<std::size_t>(v[i]);
+    return p;
 }
 
 } // namespace
@@ -235,6 +242,24 @@ int ref_read_permutation(const char* path, uint64_t* p, size_t cap, size_t* len)
         *len = q.size();
         if (p && q.size() <= cap)
             for (size_t i = 0; i < q.size(); ++i) p[i] = q[i];
+    });
+}
+
+int ref_apply_rows(uint64_t* w, size_t m, size_t n, const uint64_t* v, size_t len, int inverse) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        const Permutation p = perm_of(v, len);
+        if (inverse) p.apply_rows_inverse(a);
+        else p.apply_rows(a);
+        store(a, w);
+    });
+}
+
+int ref_compress_columns(uint64_t* w, size_t m, size_t n, size_t rank, const uint64_t* q, size_t qlen) {
+    return guard([&] {
+        BitMatrix a = load(w, m, n);
+        compress_columns(a, rank, perm_of(q, qlen));
+        store(a, w);
     });
 }
 

@@ -405,10 +405,15 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 // only real steps are stored (predicated, not branched): every lane then
                 // writes identical values, so a reader acquiring the count from any lane's
                 // release sees the step whichever lane's store it observes
-                if (!zero) {
-                    F.step_m[t] = make_ulonglong2(clo, mhi);
-                    F.step_c[t] = c;
-                }
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.u32 p, %0, 0;\n\t"
+                    "@p st.shared.v2.u64 [%1], {%2, %3};\n\t"
+                    "@p st.shared.u32 [%4], %5;\n\t}"
+                    ::"r"(static_cast<unsigned>(!zero)),
+                    "r"(static_cast<unsigned>(__cvta_generic_to_shared(&F.step_m[t]))), "l"(clo), "l"(mhi),
+                    "r"(static_cast<unsigned>(__cvta_generic_to_shared(&F.step_c[t]))), "r"(c)
+                    : "memory");
                 t += zero ? 0 : 1;
                 tb = zero ? tb : tb << 1;
                 tm = zero ? tm : tm << 1;
