@@ -153,6 +153,8 @@ class RefLib:
         L.ref_trsm_lower_left_unit.argtypes = [u64p, sz, u64p, sz]
         L.ref_trsm_upper_left_unit.argtypes = [u64p, sz, u64p, sz]
         L.ref_default_cutoff_bytes.restype = sz
+        L.ref_apply_rows.argtypes = [u64p, sz, sz, u64p, sz, C.c_int]
+        L.ref_compress_columns.argtypes = [u64p, sz, sz, sz, u64p, sz]
         L.ref_auto_table_bits.argtypes = [sz]
         L.ref_auto_table_bits.restype = C.c_uint
 
@@ -160,6 +162,20 @@ class RefLib:
         w = np.zeros((m, words(n)), dtype=np.uint64)
         assert self.lib.ref_randomize(ptr(w), m, n, density, seed) == 0
         return w
+
+    def apply_rows(self, w, n, v, inverse=False):
+        """Permutation::apply_rows[_inverse] (perm.cpp:25-38); returns (status, rows)."""
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        v = np.ascontiguousarray(v, dtype=np.uint64)
+        rc = self.lib.ref_apply_rows(ptr(w), w.shape[0], n, ptr(v) if v.size else None, v.size, int(inverse))
+        return rc, w
+
+    def compress_columns(self, w, n, rank, q):
+        """compress_columns(BitMatrix&, rank, Permutation) (perm.cpp:55-60); returns (status, matrix)."""
+        w = np.array(w, dtype=np.uint64, copy=True, order="C")
+        q = np.ascontiguousarray(q, dtype=np.uint64)
+        rc = self.lib.ref_compress_columns(ptr(w), w.shape[0], n, rank, ptr(q) if q.size else None, q.size)
+        return rc, w
 
     def _pls(self, fn, w, n, *extra):
         w = np.array(w, dtype=np.uint64, copy=True, order="C")
