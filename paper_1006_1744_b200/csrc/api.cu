@@ -56,6 +56,7 @@ struct Tuning {
     bool graph = true;            // F2_NO_GRAPH=1: enqueue the launch sequence instead of a cached graph
     bool pdl = true;              // F2_NO_PDL=1: ordinary launches instead of programmatic dependent ones
     bool early_wide_trsm = true;  // F2_NO_EARLY_WIDE_TRSM=1: wide TRSM after the fork in early panels too
+    bool split_early = false;     // F2_SPLIT_EARLY=1: early panels move the narrow solve + Schur to the side stream
     int side_ctas = 24;           // F2_SIDE_CTAS: CTAs of the look-ahead panel kernel, early panels
     int side_ctas_late = 48;      // F2_SIDE_CTAS_LATE: late panels (0: as early)
     int late_pct = 38;            // F2_LATE_PCT: first late panel, % of the panels
@@ -76,6 +77,7 @@ struct Tuning {
         graph = !flag("F2_NO_GRAPH");
         pdl = !flag("F2_NO_PDL");
         early_wide_trsm = !flag("F2_NO_EARLY_WIDE_TRSM");
+        split_early = flag("F2_SPLIT_EARLY");
         const int sc = num("F2_SIDE_CTAS", side_ctas);
         if (sc >= 2 && sc <= nsm) side_ctas = sc;
         const int sl = num("F2_SIDE_CTAS_LATE", side_ctas_late);
@@ -113,6 +115,7 @@ struct Ctx {
     cudaStream_t aux = nullptr;  // look-ahead: A-operand expansion next to the narrow TRSM
     cudaEvent_t ax_fork = nullptr, ax_join = nullptr;
     cudaEvent_t tw_fork = nullptr, tw_join = nullptr;  // wide TRSM beside the narrow one (early panels)
+    cudaEvent_t nt_done = nullptr;                     // split schedule: narrow TRSM done (on the side stream)
     int64_t* snap = nullptr;  // [2][kSnapWords]
     // tensor-core Schur operands (expanded L21 for every row, expanded U12 column tiles)
     uint8_t* f4_ax = nullptr;
@@ -194,6 +197,7 @@ int ensure_init() {
         CK(cudaEventCreateWithFlags(&g.ax_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.tw_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.tw_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.nt_done, cudaEventDisableTiming));
         CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
     }
     CK(cudaGetLastError());
@@ -426,6 +430,172 @@ F4Job pls_f4_job(const Mat& A, int64_t pw0, int64_t kbits, int64_t cw0, int64_t 
     return j;
 }
 
+// The update of the trailing columns by one finished panel, with look-ahead: the
+// enqueue sequence shared by the single-GPU engine and the sharded step.  On entry the
+// state holds the panel (its kernel ran, or a non-owner imported it); the row gather
+// and the snapshot (one launch) come first.  Then, with trailing words [t0, nw):
+//  * lookahead: panel p+1's words [t0, nx) are solved (narrow TRSM) and Schur-updated
+//    first, then factor_next(side) enqueues panel p+1's kernel on the side stream
+//    while the main stream solves and updates [nx, nw).  Early panels (the trailing
+//    update dominates) run "split": the narrow solve + Schur move to the side stream
+//    too, so the wide Schur starts right after the gather on the SMs the side chain
+//    leaves; late panels (the panel kernel is the critical path) keep them in front.
+//  * otherwise every trailing word is solved and updated on the main stream.
+// pivots_final(stream) is called once the pivot rows are final in every column.
+struct PanelStep {
+    Mat A;
+    Mat Cf;            // the panel's words (L below the pivots); Cf.w == A.w: the panel itself
+    int64_t cw0;       // first word of the panel in Cf
+    int64_t p, npanels;
+    int64_t width;     // panel bits
+    int64_t t0, nw;    // trailing words
+    bool lookahead;
+    int64_t nx;        // look-ahead: panel p+1 occupies words [t0, nx)
+    int side_ctas;     // CTAs of the side chain (0: the Tuning rule)
+};
+
+// stats of the sharded schedule: Schur launches timed inside the real schedule
+struct SchurTimed {
+    int64_t p, c0, c1;
+    cudaEvent_t e0, e1;
+};
+std::vector<SchurTimed>* g_schur_timed = nullptr;  // set while f2_dist_step enqueues with stats on
+
+template <class FactorNext, class PivotsFinal>
+int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, FactorNext factor_next,
+                       PivotsFinal pivots_final) {
+    const Mat& A = ps.A;
+    const int64_t m = A.m, nw = ps.nw, t0 = ps.t0;
+    const int nleaves = static_cast<int>((ps.width + 63) / 64);
+    int64_t* snap = g.snap + (ps.p & 1) * kSnapWords;
+    if (t0 >= nw) {
+        launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+        ++g.launches;
+        return pivots_final(s);
+    }
+    launch_perm(s, A, nw, g.st, g.pmap, g.scratch, snap, nleaves, &ps.Cf, ps.cw0);
+    g.launches += 2;
+    evmark(s, "gather1", ps.p);
+    const bool f4 = tune.f4 && g.f4_ax && ps.width >= 256;  // MMPF (W = 64) keeps the table-apply
+    F4Job fj = pls_f4_job(A, 0, ps.width, t0, nw, &g.st->panel_r, g.st->brow);
+    fj.A = ps.Cf;
+    fj.aw0 = ps.cw0;
+    if (f4) {  // L21 expanded on aux beside the narrow work (rk: the live state, stable until the fork)
+        CK(cudaEventRecord(g.ax_fork, s));
+        CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
+        launch_schur_f4_expand_a(g.aux, fj, g.f4_ax, g.nsm);
+        evmark(g.aux, "expand_a", ps.p);
+        CK(cudaEventRecord(g.ax_join, g.aux));
+    }
+    fj.rk = snap;
+    fj.brow = snap + kSnapBrow;
+    TableApply ta{};
+    ta.C = A;
+    ta.c_r1 = m;
+    ta.A = ps.Cf;
+    ta.aw0 = ps.cw0;
+    ta.kw = nleaves;
+    ta.kbits = ps.width;
+    ta.B = A;
+    ta.brow = snap + kSnapBrow;
+    ta.rk = snap;
+    ta.row_mode = ROWS_AFTER_PANEL;
+    ta.st = g.st;
+    const int64_t erows = m - std::min<int64_t>(m, (ps.p + 1) * ps.width);  // rows below the pivots at full rank
+    const bool late = 100 * (ps.p + 1) >= tune.late_pct * std::max<int64_t>(ps.npanels, 1);
+    const int side = ps.side_ctas > 0 ? ps.side_ctas
+                                      : (tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas);
+    const int64_t nx = ps.lookahead ? ps.nx : t0;
+    const bool split = ps.lookahead && !late && tune.split_early && f4 && nx < nw;
+    const bool wide_early = ps.lookahead && !late && tune.early_wide_trsm && nx < nw;
+    auto schur = [&](cudaStream_t st, int64_t c0, int64_t c1, int region, int grid) -> int {
+        if (c1 <= c0) return F2_OK;
+        SchurTimed tm{ps.p, c0, c1, nullptr, nullptr};
+        if (g_schur_timed) {
+            CK(cudaEventCreate(&tm.e0));
+            CK(cudaEventCreate(&tm.e1));
+            CK(cudaEventRecord(tm.e0, st));
+        }
+        if (f4) {
+            F4Job j = fj;
+            j.cw0 = j.bw0 = c0;
+            j.cw1 = c1;
+            launch_schur_f4(st, j, g.f4_ax, g.f4_bx + region * schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + region,
+                            grid);
+        } else {
+            TableApply t = ta;
+            t.cw0 = t.bw0 = c0;
+            t.cw1 = c1;
+            launch_table_apply(st, t, grid, erows);
+        }
+        if (g_schur_timed) {
+            CK(cudaEventRecord(tm.e1, st));
+            g_schur_timed->push_back(tm);
+        }
+        return F2_OK;
+    };
+    int rc;
+    if (wide_early) {  // the wide TRSM (disjoint columns) beside the narrow one
+        CK(cudaEventRecord(g.tw_fork, s));
+        CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
+        launch_panel_trsm_snap(g.aux, A, snap, nleaves, nx, nw, 8);
+        evmark(g.aux, "trsm_wide", ps.p);
+        CK(cudaEventRecord(g.tw_join, g.aux));
+    }
+    if (split) {
+        // side: narrow TRSM, narrow Schur on `side` CTAs, panel p+1's kernel; main: the wide
+        // Schur on the other SMs as soon as the wide TRSM and the L21 expansion are done
+        CK(cudaEventRecord(g.la_fork, s));
+        CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
+        launch_panel_trsm_snap(sd, A, snap, nleaves, t0, nx, 1);
+        evmark(sd, "trsm_narrow", ps.p);
+        CK(cudaEventRecord(g.nt_done, sd));
+        CK(cudaStreamWaitEvent(sd, g.ax_join, 0));
+        if ((rc = schur(sd, t0, nx, 0, side))) return rc;
+        evmark(sd, "schur_narrow", ps.p);
+        factor_next(sd, side);
+        evmark(sd, "panel_next", ps.p);
+        CK(cudaEventRecord(g.la_join, sd));
+        if (wide_early) {
+            CK(cudaStreamWaitEvent(s, g.tw_join, 0));
+        } else {
+            launch_panel_trsm_snap(s, A, snap, nleaves, nx, nw, 8);
+            evmark(s, "trsm_wide", ps.p);
+        }
+        CK(cudaStreamWaitEvent(s, g.nt_done, 0));
+        if ((rc = pivots_final(s))) return rc;
+        CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+        if ((rc = schur(s, nx, nw, 1, g.nsm - side))) return rc;
+        evmark(s, "schur_wide", ps.p);
+        CK(cudaStreamWaitEvent(s, g.la_join, 0));
+        return F2_OK;
+    }
+    if (ps.lookahead) {
+        launch_panel_trsm_snap(s, A, snap, nleaves, t0, nx, 1);
+        evmark(s, "trsm_narrow", ps.p);
+        if (f4) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+        if ((rc = schur(s, t0, nx, 0, g.nsm))) return rc;
+        evmark(s, "schur_narrow", ps.p);
+        CK(cudaEventRecord(g.la_fork, s));
+        CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
+        factor_next(sd, side);
+        evmark(sd, "panel_next", ps.p);
+        CK(cudaEventRecord(g.la_join, sd));
+    }
+    if (wide_early) {
+        CK(cudaStreamWaitEvent(s, g.tw_join, 0));
+    } else {
+        launch_panel_trsm_snap(s, A, snap, nleaves, nx, nw, 8);
+        evmark(s, "trsm_wide", ps.p);
+    }
+    if ((rc = pivots_final(s))) return rc;
+    if (f4) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+    if ((rc = schur(s, nx, nw, 1, f4 || !ps.lookahead ? g.nsm : g.nsm - side))) return rc;
+    evmark(s, "schur_wide", ps.p);
+    if (ps.lookahead) CK(cudaStreamWaitEvent(s, g.la_join, 0));
+    return F2_OK;
+}
+
 // One right-looking PLS pass, enqueued on `s`.  poll = snapshot r after every panel
 // and stop enqueueing once every row is a pivot (not usable inside a graph capture).
 int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
@@ -467,126 +637,50 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         }
         evmark(s, "gather0", pi);
-        {
-            LaunchTimer t(3, 0, 0);
-            launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
-            ++g.launches;  // save + put
-        }
-        evmark(s, "gather1", pi);
-        if (pw1 < nw) {
-            TableApply ta{};
-            ta.C = A;
-            ta.c_r1 = m;
-            ta.cw0 = pw1;
-            ta.cw1 = nw;
-            ta.A = A;
-            ta.aw0 = pw0;
-            ta.kw = nleaves;
-            ta.kbits = cw;
-            ta.B = A;
-            ta.bw0 = pw1;
-            ta.brow = g.st->brow;
-            ta.row_mode = ROWS_AFTER_PANEL;
-            ta.st = g.st;
-            const int64_t erows = m - std::min<int64_t>(m, c + cw);  // rows below the pivots at full rank
-            if (la) {
-                // snapshot the finished panel (rows, pivots, solve words), solve panel pi+1's
-                // columns narrow and fast, their Schur update, then panel pi+1's kernel on the
-                // side stream while the main stream solves and updates the columns right of it
-                int64_t* snap = g.snap + (pi & 1) * kSnapWords;
-                const int64_t npw1 = std::min<int64_t>(nw, pw1 + W / 64);
-                const bool f4 = tune.f4 && g.f4_ax && cw >= 256;  // MMPF (W = 64) keeps the table-apply
-                const F4Job fj = pls_f4_job(A, pw0, cw, pw1, npw1, snap, snap + kSnapBrow);
-                if (f4) {  // the L21 operand only needs the gathered rows: expand it next to snapshot + TRSM
-                    F4Job fa = fj;
-                    fa.rk = &g.st->panel_r;  // stable until panel pi + 1's kernel starts (after the join)
-                    CK(cudaEventRecord(g.ax_fork, s));
-                    CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
-                    launch_schur_f4_expand_a(g.aux, fa, g.f4_ax, g.nsm);
-                    evmark(g.aux, "expand_a", pi);
-                    CK(cudaEventRecord(g.ax_join, g.aux));
-                }
-                launch_panel_snapshot(s, g.st, snap, nleaves, A, pw0);
-                evmark(s, "snapshot", pi);
-                // while the trailing update dominates (the first ~45 % of the panels), the wide
-                // TRSM (disjoint columns) runs beside the narrow one instead of after the fork
-                const bool late = 100 * (pi + 1) >= tune.late_pct * npanels;
-                const bool wide_early = !late && tune.early_wide_trsm && npw1 < nw;
-                if (wide_early) {
-                    CK(cudaEventRecord(g.tw_fork, s));
-                    CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
-                    launch_panel_trsm_snap(g.aux, A, snap, nleaves, npw1, nw, 8);
-                    evmark(g.aux, "trsm_wide", pi);
-                    CK(cudaEventRecord(g.tw_join, g.aux));
-                }
-                launch_panel_trsm_snap(s, A, snap, nleaves, pw1, npw1, 1);
-                evmark(s, "trsm_narrow", pi);
-                ta.brow = snap + kSnapBrow;
-                ta.rk = snap;
-                if (f4) {
-                    CK(cudaStreamWaitEvent(s, g.ax_join, 0));
-                    launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
-                } else {
-                    TableApply t1 = ta;
-                    t1.cw1 = npw1;
-                    launch_table_apply(s, t1, g.nsm, erows);
-                }
-                evmark(s, "schur_narrow", pi);
-                CK(cudaEventRecord(g.la_fork, s));
-                CK(cudaStreamWaitEvent(g.side, g.la_fork, 0));
-                // once the trailing update no longer dwarfs the panel kernel (~45 % of the panels
-                // done), give the side kernel more SMs: it is then on the critical path
-                const int side = tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas;
-                panel_kernel(g.side, pi + 1, side);
-                evmark(g.side, "panel_next", pi);
-                CK(cudaEventRecord(g.la_join, g.side));
-                if (wide_early) {
-                    CK(cudaStreamWaitEvent(s, g.tw_join, 0));
-                } else {
-                    launch_panel_trsm_snap(s, A, snap, nleaves, npw1, nw, 8);
-                    evmark(s, "trsm_wide", pi);
-                }
-                if ((rc = enqueue_download(A, c, W, s))) return rc;
-                if (npw1 < nw) {
-                    if (f4) {
-                        unsigned long long* tl = nullptr;
-#ifdef F2_TIMELINE
-                        tl = &g.st->tl[2][pi & 127];
-#endif
-                        F4Job fw = fj;
-                        fw.cw0 = fw.bw0 = npw1;
-                        fw.cw1 = nw;
-                        launch_schur_f4(s, fw, g.f4_ax, g.f4_bx + schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + 1,
-                                        g.nsm, tl);
-                        evmark(s, "schur_wide", pi);
-                    } else {
-                        TableApply t2 = ta;
-                        t2.cw0 = npw1;
-                        t2.bw0 = npw1;
-                        launch_table_apply(s, t2, g.nsm - tune.side_ctas, erows);
-                    }
-                }
-                CK(cudaStreamWaitEvent(s, g.la_join, 0));
-            } else {
+        if (la) {
+            PanelStep ps{A, A, pw0, pi, npanels, cw, pw1, nw, pw1 < nw, std::min<int64_t>(nw, pw1 + W / 64), 0};
+            auto factor_next = [&](cudaStream_t sd, int ctas) { panel_kernel(sd, pi + 1, ctas); };
+            auto pivots_final = [&](cudaStream_t st_) { return enqueue_download(A, c, W, st_); };
+            if ((rc = enqueue_panel_step(ps, s, g.side, factor_next, pivots_final))) return rc;
+        } else {
+            {
+                LaunchTimer t(3, 0, 0);
+                launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
+                ++g.launches;  // save + put
+            }
+            if (pw1 < nw) {
                 {
                     LaunchTimer t(2, 0, 0);
                     launch_panel_trsm(s, A, A, pw0, nleaves, pw1, nw, g.st);
                 }
                 if ((rc = enqueue_download(A, c, W, s))) return rc;
-                {
-                    // work is data dependent; filled in from the pivots after the call
-                    LaunchTimer t(0, static_cast<double>(pi), -1.0);
-                    if (tune.f4 && g.f4_ax && cw >= 256 && cw <= 1024) {  // panel_r, panel_kb are adjacent
-                        const F4Job fj = pls_f4_job(A, pw0, cw, pw1, nw, &g.st->panel_r, g.st->brow);
-                        launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
-                        launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
-                    } else {
-                        launch_table_apply(s, ta, g.nsm, erows);
-                    }
+                // work is data dependent; filled in from the pivots after the call
+                LaunchTimer t(0, static_cast<double>(pi), -1.0);
+                if (tune.f4 && g.f4_ax && cw >= 256 && cw <= 1024) {  // panel_r, panel_kb are adjacent
+                    const F4Job fj = pls_f4_job(A, pw0, cw, pw1, nw, &g.st->panel_r, g.st->brow);
+                    launch_schur_f4_expand_a(s, fj, g.f4_ax, g.nsm);
+                    launch_schur_f4(s, fj, g.f4_ax, g.f4_bx, g.f4_claim, g.nsm);
+                } else {
+                    TableApply ta{};
+                    ta.C = A;
+                    ta.c_r1 = m;
+                    ta.cw0 = pw1;
+                    ta.cw1 = nw;
+                    ta.A = A;
+                    ta.aw0 = pw0;
+                    ta.kw = nleaves;
+                    ta.kbits = cw;
+                    ta.B = A;
+                    ta.bw0 = pw1;
+                    ta.brow = g.st->brow;
+                    ta.row_mode = ROWS_AFTER_PANEL;
+                    ta.st = g.st;
+                    launch_table_apply(s, ta, g.nsm, m - std::min<int64_t>(m, c + cw));
                 }
+            } else if ((rc = enqueue_download(A, c, W, s))) {
+                return rc;  // last panel: final after the gather
             }
         }
-        if (pw1 >= nw && (rc = enqueue_download(A, c, W, s))) return rc;  // last panel: final after the gather
         if (poll) {  // early exit once every row is a pivot: snapshot r without blocking
             CK(cudaMemcpyAsync(g.h_r + pi, &g.st->r, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
             cudaEvent_t ev;
@@ -1481,11 +1575,7 @@ struct DistState {
     int64_t* h_rk = nullptr;  // pinned [npanels][2]: (kb, panel_r)
     size_t cap = 0;
     std::vector<cudaEvent_t> ev;
-    struct Timed {  // stats: Schur launches of the timed schedule, work resolved at finish
-        int64_t p, c0, c1;
-        cudaEvent_t e0, e1;
-    };
-    std::vector<Timed> timed;
+    std::vector<SchurTimed> timed;  // stats: Schur launches of the timed schedule, work resolved at finish
 };
 DistState gd;
 
@@ -1561,101 +1651,25 @@ int f2_dist_step(f2_matrix* a, int64_t p, int owner, size_t pw0, unsigned width_
     const int64_t m = A.m, nw = (A.n + 63) / 64, ws = gd.W / 64;
     const int nleaves = static_cast<int>((width_bits + 63) / 64);
     cudaStream_t s = as_stream(main_stream), sd = as_stream(side_stream);
+    if (lookahead && static_cast<int64_t>(tw0) >= nw)
+        return fail(F2_INVALID_ARGUMENT, "look-ahead without local trailing columns");
     const Mat Bw{const_cast<uint64_t*>(buf), m, static_cast<int64_t>(gd.W), ws};  // the broadcast words
-    const Mat Cf = owner ? A : Bw;                                                  // L of the panel
-    const int64_t cw0 = owner ? static_cast<int64_t>(pw0) : 0;
     if (!owner) {
         launch_dist_import(s, g.st, g.pmap, g.P, g.Qp, reinterpret_cast<const int64_t*>(buf + m * ws),
                            static_cast<int>(gd.W));
-        launch_panel_lmaps(s, Cf, 0, nleaves, g.st);
+        launch_panel_lmaps(s, Bw, 0, nleaves, g.st);
     }
-    launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
-    const int64_t t0 = static_cast<int64_t>(tw0);
-    if (t0 >= nw) {
-        if (lookahead) return fail(F2_INVALID_ARGUMENT, "look-ahead without local trailing columns");
-        CK(cudaGetLastError());
-        return F2_OK;
-    }
-    int64_t* snap = g.snap + (p & 1) * kSnapWords;
-    const bool f4 = tune.f4 && g.f4_ax && width_bits >= 256;
-    F4Job fj = pls_f4_job(A, 0, width_bits, t0, nw, &g.st->panel_r, g.st->brow);
-    fj.A = Cf;
-    fj.aw0 = cw0;
-    if (f4) {  // L21 expanded beside the snapshot and the narrow TRSM (rk: the live state, stable until the fork)
-        CK(cudaEventRecord(g.ax_fork, s));
-        CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
-        launch_schur_f4_expand_a(g.aux, fj, g.f4_ax, g.nsm);
-        CK(cudaEventRecord(g.ax_join, g.aux));
-    }
-    launch_panel_snapshot(s, g.st, snap, nleaves, Cf, cw0);
-    fj.rk = snap;
-    fj.brow = snap + kSnapBrow;
-    TableApply ta{};
-    ta.C = A;
-    ta.c_r1 = m;
-    ta.A = Cf;
-    ta.aw0 = cw0;
-    ta.kw = nleaves;
-    ta.kbits = width_bits;
-    ta.B = A;
-    ta.brow = snap + kSnapBrow;
-    ta.rk = snap;
-    ta.row_mode = ROWS_AFTER_PANEL;
-    ta.st = g.st;
-    bool ax_waited = false;
-    auto schur = [&](int64_t c0, int64_t c1, int region) -> int {
-        if (c1 <= c0) return F2_OK;
-        DistState::Timed tm{p, c0, c1, nullptr, nullptr};
-        if (g.stats) {
-            CK(cudaEventCreate(&tm.e0));
-            CK(cudaEventCreate(&tm.e1));
-        }
-        if (tm.e0) CK(cudaEventRecord(tm.e0, s));
-        if (f4) {
-            if (!ax_waited) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
-            ax_waited = true;
-            F4Job j = fj;
-            j.cw0 = j.bw0 = c0;
-            j.cw1 = c1;
-            launch_schur_f4(s, j, g.f4_ax, g.f4_bx + region * schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + region,
-                            g.nsm);
-        } else {
-            TableApply t = ta;
-            t.cw0 = t.bw0 = c0;
-            t.cw1 = c1;
-            launch_table_apply(s, t, g.nsm, m - std::min<int64_t>(m, static_cast<int64_t>(p + 1) * gd.W));
-        }
-        if (tm.e1) {
-            CK(cudaEventRecord(tm.e1, s));
-            gd.timed.push_back(tm);
-        }
-        return F2_OK;
+    PanelStep ps{A, owner ? A : Bw, owner ? static_cast<int64_t>(pw0) : 0, p, gd.npanels, width_bits,
+                 static_cast<int64_t>(tw0), nw, lookahead != 0,
+                 std::min<int64_t>(nw, static_cast<int64_t>(tw0) + (next_width + 63) / 64), side_ctas};
+    auto factor_next = [&](cudaStream_t st_, int ctas) {
+        dist_factor_enqueue(A, static_cast<int64_t>(tw0), next_width, static_cast<int64_t>(next_col), next_buf,
+                            std::min(ctas, g.nsm), st_);
     };
-    int rc;
-    const int64_t nx = lookahead ? std::min<int64_t>(nw, t0 + (next_width + 63) / 64) : t0;  // next panel's words
-    const bool late = 100 * (p + 1) >= tune.late_pct * std::max<int64_t>(gd.npanels, 1);
-    const bool wide_early = lookahead && !late && tune.early_wide_trsm && nx < nw;
-    if (wide_early) {
-        CK(cudaEventRecord(g.tw_fork, s));
-        CK(cudaStreamWaitEvent(g.aux, g.tw_fork, 0));
-        launch_panel_trsm_snap(g.aux, A, snap, nleaves, nx, nw, 8);
-        CK(cudaEventRecord(g.tw_join, g.aux));
-    }
-    if (lookahead) {
-        launch_panel_trsm_snap(s, A, snap, nleaves, t0, nx, 1);
-        if ((rc = schur(t0, nx, 0))) return rc;
-        CK(cudaEventRecord(g.la_fork, s));
-        CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
-        const int ctas = side_ctas > 0 ? side_ctas
-                                       : (tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas);
-        dist_factor_enqueue(A, t0, next_width, static_cast<int64_t>(next_col), next_buf, std::min(ctas, g.nsm), sd);
-        CK(cudaEventRecord(g.la_join, sd));
-    }
-    if (wide_early) CK(cudaStreamWaitEvent(s, g.tw_join, 0));
-    else launch_panel_trsm_snap(s, A, snap, nleaves, nx, nw, 8);
-    if ((rc = schur(nx, nw, 1))) return rc;
-    if (f4 && !ax_waited) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
-    if (lookahead) CK(cudaStreamWaitEvent(s, g.la_join, 0));
+    g_schur_timed = g.stats ? &gd.timed : nullptr;  // resolved at f2_dist_finish
+    const int rc = enqueue_panel_step(ps, s, sd, factor_next, [](cudaStream_t) { return F2_OK; });
+    g_schur_timed = nullptr;
+    if (rc) return rc;
     CK(cudaGetLastError());
     return F2_OK;
 }

@@ -30,7 +30,10 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // leaf.cu
-void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch);
+// the panel's row gather; with snap != nullptr the same launch also takes the panel's
+// snapshot (kSnap* below) from Cf's words coef_w0.. (Cf == A: read through pmap)
+void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch,
+                 int64_t* snap = nullptr, int nleaves = 0, const Mat* Cf = nullptr, int64_t coef_w0 = 0);
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
 void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves, PlsState* st);
 constexpr int64_t dist_header_words(int W) { return 4 + 2 * static_cast<int64_t>(W) + 2 * kMaxMoved; }
@@ -82,8 +85,6 @@ struct TableApply {
 constexpr int64_t kSnapBrow = 2, kSnapQ = kSnapBrow + kMaxPanelBits, kSnapBstart = kSnapQ + kMaxPanelBits,
                   kSnapM = kSnapBstart + kMaxPanelBits / 64 + 8,
                   kSnapWords = kSnapM + static_cast<int64_t>(kMaxPanelBits / 64) * kMaxPanelBits;
-void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int nleaves, const Mat& Cf,
-                           int64_t coef_w0);
 // U <- L11^{-1} U on words [tw0, tw1) of the panel's pivot rows, from a snapshot only
 // (the next panel's kernel may be rewriting the state); strip = words per CTA (1 or 8)
 void launch_panel_trsm_snap(cudaStream_t s, const Mat& A, const int64_t* snap, int nleaves, int64_t tw0, int64_t tw1,

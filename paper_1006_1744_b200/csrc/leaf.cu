@@ -190,15 +190,69 @@ void launch_dist_import(cudaStream_t s, PlsState* st, int64_t* pmap, int64_t* P,
     k_dist_import<<<1, 1024, 0, s>>>(st, pmap, P, Qp, hdr, W);
 }
 
+// Snapshot of a finished panel (see kernels.cuh, kSnap*): block (j, y) handles leaf j's
+// solve words of pivots t = 256 y + tid.  The pivot rows' coefficient words are read
+// from Cf at position panel_r + t, through rowmap when the panel's row gather has not
+// run yet (the virtual order: physical row rowmap[x]).
+__device__ __forceinline__ void snapshot_block(const PlsState* st, int64_t* snap, const Mat& Cf, int64_t coef_w0,
+                                               int nleaves, int j, int by, const int64_t* rowmap) {
+    __shared__ int s_b[2];
+    const int tid = threadIdx.x;
+    const int t = by * 256 + tid;
+    const int64_t r0 = st->panel_r;
+    const int nk = static_cast<int>(st->panel_kb);
+    const int pb = nleaves * 64;
+    auto lower = [&](int v) {  // first pivot index with column >= v (panel_q ascends)
+        int lo = 0, hi = nk;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (st->panel_q[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    if (tid < 2) s_b[tid] = lower(64 * (j + tid));
+    if (j == 0 && t < pb) {
+        if (t == 0) {
+            snap[0] = r0;
+            snap[1] = nk;
+        }
+        snap[kSnapBrow + t] = st->brow[t];
+        snap[kSnapQ + t] = t < nk ? st->panel_q[t] : -1;
+        if (t <= nleaves) snap[kSnapBstart + t] = lower(64 * t);
+    }
+    __syncthreads();
+    const int t0 = s_b[0], t1 = s_b[1];
+    if (t >= t0 && t < nk) {
+        const int64_t row = rowmap ? rowmap[r0 + t] : r0 + t;
+        uint64_t c = Cf.w[row * Cf.stride + coef_w0 + j];
+        if (t < t1) c &= (1ull << (st->panel_q[t] - 64 * j)) - 1ull;
+        uint64_t M = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) M ^= st->lmap[j][g][(c >> (8 * g)) & 0xffu];
+        snap[kSnapM + static_cast<int64_t>(j) * kMaxPanelBits + t] = static_cast<int64_t>(M);
+    }
+}
+
 // Panel end, step 1: copy the rows that the panel's positions now refer to
 // (physical row pmap[x] for every re-mapped position x) into scratch, whole width.
+// Blocks past the copy (when snap != nullptr) take the panel's snapshot meanwhile,
+// reading the pivot rows through pmap: one launch instead of two on the serial path.
 __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
-                                                  uint64_t* scratch) {
+                                                  uint64_t* scratch, unsigned gx, unsigned gy, int64_t* snap, Mat Cf,
+                                                  int64_t coef_w0, int nleaves) {
     pdl_wait();
+    const unsigned b = blockIdx.x;
+    if (b >= gx * gy) {
+        const unsigned s = b - gx * gy;
+        snapshot_block(st, snap, Cf, coef_w0, nleaves, static_cast<int>(s % nleaves), static_cast<int>(s / nleaves),
+                       Cf.w == A.w ? pmap : nullptr);
+        return;
+    }
     const int n = st->nmoved;
-    const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);  // word pair (16 B)
+    const int64_t k = 2 * (static_cast<int64_t>(b % gx) * blockDim.x + threadIdx.x);  // word pair (16 B)
     if (k >= nwords) return;
-    for (int i = blockIdx.y; i < n; i += gridDim.y) {
+    for (int i = b / gx; i < n; i += gy) {
         const uint64_t* src = A.w + pmap[st->moved[i]] * A.stride + k;
         uint64_t* dst = scratch + static_cast<int64_t>(i) * A.stride + k;
         if (k + 1 < nwords) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
@@ -230,14 +284,17 @@ __global__ void k_pmap_init(int64_t* pmap, int64_t m) {
 }
 
 
-void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch) {
+void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch,
+                 int64_t* snap, int nleaves, const Mat* Cf, int64_t coef_w0) {
     // rows are 128-byte aligned (stride % 16 words == 0): 16-byte accesses, ~1024 CTAs
     const unsigned gx = static_cast<unsigned>((nwords + 511) / 512);
-    dim3 grid(gx, gx >= 1024 ? 1u : 1024u / gx);
-    launch_pdl(k_perm_save, grid, dim3(256), 0, s, A, nwords, st, static_cast<const int64_t*>(pmap), scratch);
-    launch_pdl(k_perm_put, grid, dim3(256), 0, s, A, nwords, st, pmap, static_cast<const uint64_t*>(scratch));
+    const unsigned gy = gx >= 1024 ? 1u : 1024u / gx;
+    const unsigned nsnap = snap ? static_cast<unsigned>(nleaves * ((nleaves * 64 + 255) / 256)) : 0u;
+    const Mat cf = Cf ? *Cf : A;
+    launch_pdl(k_perm_save, dim3(gx * gy + nsnap), dim3(256), 0, s, A, nwords, st, static_cast<const int64_t*>(pmap),
+               scratch, gx, gy, snap, cf, coef_w0, nleaves);
+    launch_pdl(k_perm_put, dim3(gx, gy), dim3(256), 0, s, A, nwords, st, pmap, static_cast<const uint64_t*>(scratch));
 }
-
 
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {
     int64_t g = (m + 255) / 256;

@@ -373,50 +373,4 @@ void setup_rref_kernels() {
 }
 
 
-__global__ void __launch_bounds__(256) k_panel_snapshot(const PlsState* st, int64_t* snap, Mat Cf, int64_t coef_w0,
-                                                        int nleaves) {
-    pdl_wait();
-    __shared__ int s_b[2];
-    const int j = blockIdx.x, tid = threadIdx.x;
-    const int t = blockIdx.y * 256 + tid;
-    const int64_t r0 = st->panel_r;
-    const int nk = static_cast<int>(st->panel_kb);
-    const int pb = nleaves * 64;
-    auto lower = [&](int v) {  // first pivot index with column >= v (panel_q ascends)
-        int lo = 0, hi = nk;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (st->panel_q[mid] < v) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo;
-    };
-    if (tid < 2) s_b[tid] = lower(64 * (j + tid));
-    if (j == 0 && t < pb) {
-        if (t == 0) {
-            snap[0] = r0;
-            snap[1] = nk;
-        }
-        snap[kSnapBrow + t] = st->brow[t];
-        snap[kSnapQ + t] = t < nk ? st->panel_q[t] : -1;
-        if (t <= nleaves) snap[kSnapBstart + t] = lower(64 * t);
-    }
-    __syncthreads();
-    const int t0 = s_b[0], t1 = s_b[1];
-    if (t >= t0 && t < nk) {
-        uint64_t c = Cf.w[(r0 + t) * Cf.stride + coef_w0 + j];
-        if (t < t1) c &= (1ull << (st->panel_q[t] - 64 * j)) - 1ull;
-        uint64_t M = 0;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) M ^= st->lmap[j][g][(c >> (8 * g)) & 0xffu];
-        snap[kSnapM + static_cast<int64_t>(j) * kMaxPanelBits + t] = static_cast<int64_t>(M);
-    }
-}
-
-void launch_panel_snapshot(cudaStream_t s, const PlsState* st, int64_t* snap, int nleaves, const Mat& Cf,
-                           int64_t coef_w0) {
-    launch_pdl(k_panel_snapshot, dim3(nleaves, (nleaves * 64 + 255) / 256), dim3(256), 0, s, st, snap, Cf, coef_w0,
-               nleaves);
-}
-
 }  // namespace f2g

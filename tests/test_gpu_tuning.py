@@ -43,6 +43,8 @@ SCRIPT = textwrap.dedent("""
     {"F2_NO_GRAPH": "1"},
     {"F2_NO_PDL": "1"},
     {"F2_NO_EARLY_WIDE_TRSM": "1"},
+    {"F2_SPLIT_EARLY": "1"},
+    {"F2_SPLIT_EARLY": "1", "F2_NO_EARLY_WIDE_TRSM": "1"},
     {"F2_SIDE_CTAS": "8", "F2_SIDE_CTAS_LATE": "0"},
     {"F2_LATE_PCT": "0"},
     {"F2_LATE_PCT": "100", "F2_SIDE_CTAS": "140"},

@@ -40,7 +40,7 @@ if os.environ.get("F2_EVTL") is None:
                 tot[k] += v
         rows.append((p, seg))
     for p, seg in rows:
-        if p % 8 == 0 or p >= 60:
+        if p % 4 == 0 or p >= 60 or os.environ.get("EVTL_ALL"):
             print(f"panel {p:2d}: " + " ".join(f"{k}={v:7.1f}" for k, v in seg.items()))
     print("totals (us): " + " ".join(f"{k}={v:.0f}" for k, v in tot.items()))
     print(f"span {prev_end:.0f} us")
