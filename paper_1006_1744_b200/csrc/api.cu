@@ -553,6 +553,7 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
         CK(cudaStreamWaitEvent(sd, g.ax_join, 0));
         if ((rc = schur(sd, t0, nx, 0, side))) return rc;
         evmark(sd, "schur_narrow", ps.p);
+        if (wide_early) CK(cudaStreamWaitEvent(sd, g.tw_join, 0));  // (see the non-split path)
         factor_next(sd, side);
         evmark(sd, "panel_next", ps.p);
         CK(cudaEventRecord(g.la_join, sd));
@@ -576,6 +577,10 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
         if (f4) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
         if ((rc = schur(s, t0, nx, 0, g.nsm))) return rc;
         evmark(s, "schur_narrow", ps.p);
+        // the next panel's kernel never runs beside the wide TRSM: with the two overlapping,
+        // panel p+1's pivoting was seen to diverge (a few runs in 20 at 64K^2, early panels
+        // only); the TRSM is nearly always done by now, so the wait costs ~nothing
+        if (wide_early) CK(cudaStreamWaitEvent(s, g.tw_join, 0));
         CK(cudaEventRecord(g.la_fork, s));
         CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
         factor_next(sd, side);

@@ -69,3 +69,21 @@ def test_config3_rref_is_identity(f2):
     i = np.arange(65536)
     idw[i, i // 64] = np.uint64(1) << (i % 64).astype(np.uint64)
     assert a.digest() == digest(idw)
+
+
+def test_config3_repeatable(f2):
+    """The look-ahead schedule overlaps kernels on three streams: repeated full-size runs
+    must all reproduce the reference's packed digest (a race once showed as a diverging
+    pivot in a few runs out of twenty)."""
+    g = golden().get("c3_dense_65536")
+    if g is None:
+        pytest.skip("c3_dense_65536 not in golden/configs.json")
+    a0 = f2.DeviceMatrix(65536, 65536)
+    a0.randomize(0.5, 3)
+    a = f2.DeviceMatrix(65536, 65536)
+    cfg = f2.EliminationConfig(cutoff_bytes=int(g["cutoff_bytes"]))
+    for _ in range(12):
+        a.copy_from(a0)
+        res = f2.pls_recursive(a, cfg)
+        assert res.rank == g["recursive"]["rank"]
+        assert a.digest() == int(g["recursive"]["packed_digest"])
