@@ -44,9 +44,10 @@ BITOPS = 2.0 * N ** 3 / 3.0
 METRIC = "GF(2) PLS effective Gbit-op/s (2n^3/3 per decomposition), 64K^2 dense"
 UNIT = "Gbit-op/s"
 SAMPLE_N = 16384  # CPU sample size (reference arm / cpu_baseline)
-# tcgen05.mma kind::mxf4 128x224x64 with SMEM-resident operands on all 148 SMs (tools/micro/umma_f4,
-# profiles/r1_umma_f4_peak.txt): the ceiling of the tensor-core Schur kernel, in fp4 TFLOP/s
-F4_MMA_PEAK_TFLOPS = 7500.0
+# tcgen05.mma kind::mxf4 128x224x64 with SMEM-resident operands on all 148 SMs, issued without
+# draining the pipe (tools/micro/umma_f4_pair, profiles/r2_umma_f4_pair_peak.txt): the ceiling of
+# the tensor-core Schur kernel's data path, in fp4 TFLOP/s
+F4_MMA_PEAK_TFLOPS = 8880.0
 F4_NOMINAL_TFLOPS = 9000.0  # fp4 dense, B200_PROFILING.md (MEASURED_PEAKS.json has no fp4 figure)
 try:
     PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -211,8 +212,9 @@ def schur_roofline(fam0, total_ms, note):
                         "figure; 4 x its bf16 burst = %.0f)" % (4 * PEAKS.get("bf16_tflops", 0.0)),
          "measured_mma_ceiling": F4_MMA_PEAK_TFLOPS,
          "frac_of_measured_mma_ceiling": achieved / F4_MMA_PEAK_TFLOPS,
-         "measured_mma_ceiling_source": "tcgen05.mma kind::mxf4 128x224x64 issue rate with SMEM-resident operands "
-                                        "on 148 SMs at 1965 MHz (tools/micro/umma_f4, profiles/r1_umma_f4_peak.txt)",
+         "measured_mma_ceiling_source": "tcgen05.mma kind::mxf4 128x224x64 back to back with SMEM-resident operands "
+                                        "on 148 SMs at 1965 MHz, no pipe drain (tools/micro/umma_f4_pair, "
+                                        "profiles/r2_umma_f4_pair_peak.txt; the CTA-pair form measures the same)",
          "unit_note": "1 GF(2) bit-op = 1 fp4 flop: each AND-count term is one MMA multiply-add",
          "per_unit": "2 * rows * pivots * columns bit-ops per Schur launch (rows below the panel's pivots, the "
                      "panel's pivots, the trailing columns), summed from the pivot list",

@@ -37,7 +37,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr) {
     return (uint64_t((addr >> 4) & 0x3FFF)) | (uint64_t(128 >> 4) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46);
 }
 template <int M>
-constexpr uint32_t idesc() {
+__host__ __device__ constexpr uint32_t idesc() {
     return (1u << 7) | (1u << 10) | (1u << 23) | (uint32_t(N_ >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -161,8 +161,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 }
 
 // MMA-only rate: random operands resident in smem, iters x 16 MMAs, one commit at the end
-template <int M>
-__global__ void __launch_bounds__(128, 1) k_peak(int iters, int* sink) {
+template <int M, int READERS>
+__global__ void __launch_bounds__(256, 1) k_peak(int iters, int* sink) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tbase_s;
@@ -202,6 +202,26 @@ __global__ void __launch_bounds__(128, 1) k_peak(int iters, int* sink) {
     if (M == 256) cluster_sync();
     else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
+    __shared__ volatile int done;
+    if (threadIdx.x == 0) done = 0;
+    __syncthreads();
+    if (READERS && warp >= 4) {  // epilogue-like TMEM reads of the lane quarter warp & 3, as fast as possible
+        uint32_t acc = 0;
+        while (!done) {
+            uint32_t v[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+                  "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+                  "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                  "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(tbase + (uint32_t((warp & 3) * 32) << 16) + 2 * N_ - 32 * ((acc & 3) + 1)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            for (int i = 0; i < 32; ++i) acc += v[i];
+        }
+        if (acc == 12345u) *sink = acc;
+    }
     if (rank == 0 && threadIdx.x == 0) {
         const uint32_t a = su32(sm), b = a + 128 * 512;
         for (int it = 0; it < iters; ++it) issue_k<M>(tbase, (it & 1) ? N_ : 0, a, b, brows);
@@ -212,7 +232,11 @@ __global__ void __launch_bounds__(128, 1) k_peak(int iters, int* sink) {
         else
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(&mbar)));
     }
-    wait_parity(&mbar, 0);
+    if (warp < 4) {
+        wait_parity(&mbar, 0);
+        if (threadIdx.x == 0) done = 1;
+    }
+    __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     if (warp == 0) {
         uint32_t v;
@@ -275,15 +299,29 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    auto run = [&](auto kern, int smem, const char* name) {
+    auto run = [&](auto kern, int smem, const char* name, int cl) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         const int iters = 4000;
-        kern<<<nsm, 128, smem>>>(10, sink);
+        auto launch = [&](int it) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(nsm);
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, kern, it, sink));
+        };
+        launch(10);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(e0);
-            kern<<<nsm, 128, smem>>>(iters, sink);
+            launch(iters);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             float t;
@@ -292,7 +330,9 @@ int main() {
             printf("%s: %.3f ms, %.2f P bit-op/s (%d SMs)\n", name, t, 2 * macs / (t / 1e3) / 1e15, nsm);
         }
     };
-    run(k_peak<128>, (128 + N_) * 512, "1-SM  M=128 N=224 (no drain)");
-    run(k_peak<256>, (128 + N_ / 2) * 512, "pair  M=256 N=224 (cta_group::2)");
+    run(k_peak<128, 0>, (128 + N_) * 512, "1-SM  M=128 N=224 (no drain)", 1);
+    run(k_peak<128, 1>, (128 + N_) * 512, "1-SM  M=128 N=224 + TMEM readers", 1);
+    run(k_peak<256, 0>, (128 + N_ / 2) * 512, "pair  M=256 N=224 (cta_group::2)", 2);
+    run(k_peak<256, 1>, (128 + N_ / 2) * 512, "pair  M=256 N=224 + TMEM readers", 2);
     return bad != 0;
 }

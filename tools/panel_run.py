@@ -1,4 +1,4 @@
-"""A 65536 x 2048 pls_recursive (two panels) for profiling k_panel_leaves."""
+"""A 65536 x 2048 pls_recursive (two panels) for profiling the panel kernel (k_panel_pipe)."""
 import sys
 
 sys.path.insert(0, ".")
