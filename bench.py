@@ -466,7 +466,9 @@ def run_sharded(args, ws, rank, local):
     del full_t
     a_t = torch.zeros_like(a0_t)
     a = f2.DeviceMatrix.from_torch(a_t, ncols)
-    ops, comm = D.GpuOps(f2), D.TorchComm()
+    # from N = 2 on the per-rank trailing update no longer hides the panel kernel, which is then
+    # the critical path from the first panel: give it the late schedule's CTA count throughout
+    ops, comm = D.GpuOps(f2, side_ctas=48 if ws > 1 else 0), D.TorchComm()
     barrier, max_over_ranks = barrier_and_max(dist)
 
     def step():

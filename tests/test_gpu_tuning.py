@@ -49,6 +49,9 @@ SCRIPT = textwrap.dedent("""
     {"F2_LATE_PCT": "0"},
     {"F2_LATE_PCT": "100", "F2_SIDE_CTAS": "140"},
     {"F2_NO_GRAPH": "1", "F2_EVTL": "1"},
+    {"F2_MMPF_PANEL_BITS": "64"},
+    {"F2_MMPF_PANEL_BITS": "64", "F2_NO_LOOKAHEAD": "1"},
+    {"F2_MMPF_PANEL_BITS": "256"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_tuning_switch_stays_exact(env):
     full = dict(os.environ, **env)
