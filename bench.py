@@ -221,15 +221,22 @@ def schur_roofline(fam0, total_ms, note):
          "share_of_step": fam0["ms"] / total_ms if total_ms else None,
          "launches": fam0["launches"], "avg_launch_ms": fam0["ms"] / max(fam0["launches"], 1),
          "timing": note, "traffic": None}
-    prof = os.path.join(ROOT, "profiles", "r1_ncu_schur_f4_config3_raw.json")
+    prof = os.path.join(ROOT, "profiles", "r2_ncu_schur_f4_config3_raw.json")
     if os.path.exists(prof):
         raw = json.load(open(prof))
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         r["traffic"] = sum(float(raw[k][0]) * scale.get(raw[k][1], 1.0)
                            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         r["traffic_note"] = ("dram read+write bytes of the first wide k_schur_f4 launch of config 3 (ncu --set full, "
-                             "profiles/r1_ncu_schur_f4_config3_raw.json); its algorithmic bytes (C read+write once) "
+                             "profiles/r2_ncu_schur_f4_config3_raw.json); its algorithmic bytes (C read+write once) "
                              "are %.4g" % (64512 * 63488 / 8 * 2))
+        clk = float(raw.get("sm__cycles_elapsed.avg.per_second", ["0"])[0] or 0)
+        if clk:
+            r["sustained_clock_ghz"] = clk
+            r["frac_of_mma_ceiling_at_sustained_clock"] = (
+                8.39e12 / (float(raw["gpu__time_duration.sum"][0]) * 1e-3) / 1e12 / (F4_MMA_PEAK_TFLOPS * clk / 1.965))
+            r["clock_note"] = ("under sustained fp4 load the kernel runs power-capped (ncu: %.2f GHz); at that clock the "
+                               "launch profiled reaches the fraction above of the MMA-only ceiling" % clk)
     return r
 
 

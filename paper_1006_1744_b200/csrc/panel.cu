@@ -438,12 +438,28 @@ struct PipeStatic {  // CTA 0's persistent window bookkeeping
     int cs[kPW];
 };
 
+// Leaf `leafp`'s update of words [k0, k1) of every window slot: the combination of its
+// solved rows selected by the slot's coefficient word (S.t16 scratch), through the tables T.
+// Threads tid, tid + nth, ... of one (slot, word) item each.
+__device__ __forceinline__ void pipe_phase2(PipeSmem& S, int pb, int leafp, int k0, int k1, int tid, int nth) {
+    const int nk = k1 - k0;
+    if (nk <= 0) return;
+    for (int i = tid; i < kPW * nk; i += nth) {
+        const int sl = i / nk, k = k0 + (i - sl * nk);
+        const uint64_t c = S.t16[sl];
+        uint64_t v = S.win[pb][sl][k];
+#pragma unroll
+        for (int g4 = 0; g4 < 16; ++g4) v ^= S.T[(g4 * 16 + ((c >> (4 * g4)) & 15u)) * kW + (k - leafp)];
+        S.win[pb][sl][k] = v;
+    }
+}
+
 // Window for leaf `leaf` into buffer `pb`: fresh from the global matrix (every leaf
 // before it applied there), or carried from buffer pb^1 (leaf-1's window, kbp pivots,
 // srcprev) plus new rows, with leaf-1's update applied by CTA 0.
 __device__ void pipe_build_window(const Mat& A, int64_t pw0, int nwp, const int64_t* pmap, PlsState* st,
                                   PipeSmem& S, PipeStatic& Z, int pb, bool carry, int kbp, int leafp,
-                                  int64_t pmap_hi) {
+                                  int64_t pmap_hi, bool all_words) {
     const int tid = threadIdx.x;
     const int64_t base = st->r;  // position of slot 0
     const int64_t m = A.m;
@@ -479,15 +495,13 @@ __device__ void pipe_build_window(const Mat& A, int64_t pw0, int nwp, const int6
         reinterpret_cast<uint64_t*>(S.t16)[tid] = x;  // coefficient words (scratch)
     }
     __syncthreads();
-    // phase 2: the words right of leaf-1 add the combination of its solved rows
-    for (int i = tid; i < kPW * 16; i += kPT) {
-        const int sl = i >> 4, k = i & 15;
-        if (k <= leafp || k >= nwp) continue;
-        const uint64_t c = S.t16[sl];
-        uint64_t v = S.win[pb][sl][k];
-#pragma unroll
-        for (int g4 = 0; g4 < 16; ++g4) v ^= S.T[(g4 * 16 + ((c >> (4 * g4)) & 15u)) * kW + (k - leafp)];
-        S.win[pb][sl][k] = v;
+    // phase 2: the words right of leaf-1 add the combination of its solved rows -- here only
+    // the next leaf's word, which its search reads; pipe_fast_leaf's idle warps update the
+    // others beside the search (pipe_phase2), unless all_words (the final write-back)
+    if (all_words) {
+        pipe_phase2(S, pb, leafp, leafp + 1, nwp, tid, kPT);
+    } else if (tid < kPW && leafp + 1 < nwp) {
+        pipe_phase2(S, pb, leafp, leafp + 1, leafp + 2, tid, kPT);
     }
     __syncthreads();
 }
@@ -543,7 +557,7 @@ __device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSm
 // and the carry tables, and returns kb; -1 when the window cannot decide a column.
 __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int lw, PlsState* st, int64_t* P,
                               int64_t* Qp, int64_t* pmap, int64_t qcol_off, PipeSmem& S, PipeStatic& Z, int pb,
-                              PlsState::Packet* pk, int nleaves) {
+                              PlsState::Packet* pk, int nleaves, bool carried) {
     __shared__ FastSmem F;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = A.m, stride = A.stride;
@@ -565,6 +579,10 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
 #else
     if (warp < 3) two_warp_pivots(F, lw, base + kPW < m, false);
 #endif
+    // meanwhile the other warps finish the carried window: the previous leaf's update of
+    // the words right of this leaf's (pipe_build_window did this leaf's word)
+    // (warps 3, 7, ..., 31 only: the fourth scheduler, away from the selecting warps 0 and 1)
+    if ((warp & 3) == 3 && carried) pipe_phase2(S, pb, leaf - 1, leaf + 1, nwp, (warp >> 2) * 32 + (tid & 31), kPT / 4);
     __syncthreads();
     F2_CLK(if (clk) { st->dbg[20] = clock64() - c0; st->dbg[29] = F.clk[0][1] - F.clk[0][0]; st->dbg[31] = F.clk[1][1] - F.clk[1][0]; })
     F2_STAMP(st, 18);
@@ -800,7 +818,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
             if (state == S_FRESH || state == S_CARRY || state == S_FINAL) {
                 F2_CLK(const long long cb = clock64();)
                 pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
-                                  j == 0 ? 0 : st->pmap_hi);
+                                  j == 0 ? 0 : st->pmap_hi, state == S_FINAL);
                 F2_CLK(if (pw0 == 0 && j == 2 && threadIdx.x == 0) st->dbg[22] = clock64() - cb;)
                 F2_STAMP(st, 1);
                 if (state == S_FINAL) {
@@ -809,7 +827,8 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 } else {
                     const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
                     PlsState::Packet* pk = &st->pk[pkc & 1];
-                    const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves);
+                    const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves,
+                                                  state == S_CARRY);
                     F2_STAMP(st, 2);
                     if (kb >= 0) {
                         kbprev = kb;
