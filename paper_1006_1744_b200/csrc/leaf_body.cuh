@@ -359,13 +359,17 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
                 }
             }
         }
-        if (ok) {
+        // Written whatever this warp's own `ok` says: the tracker may read the progress word
+        // only after the other warp has started publishing phase 1, apply some of those steps
+        // before leaving phase 0, and then undercount phase 1 -- its `ok` is not authoritative
+        // (warp 0's final_kb is), while its masks, having applied every step in order, are.
+        // (Gating this store on the tracker's `ok` once left stale slot sources behind, so a
+        // leaf's pivot rows went to the wrong physical rows in rare runs.)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t m = k < 2 ? C.lo : C.hi;
-                const uint32_t piece = static_cast<uint32_t>(m >> (32 * (k & 1)));
-                F.src[32 * k + lane] = static_cast<int>(warp_transpose32(piece, lane) & 127u);
-            }
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t m = k < 2 ? C.lo : C.hi;
+            const uint32_t piece = static_cast<uint32_t>(m >> (32 * (k & 1)));
+            F.src[32 * k + lane] = static_cast<int>(warp_transpose32(piece, lane) & 127u);
         }
     } else
     for (int phase = 0; phase < 2; ++phase) {
