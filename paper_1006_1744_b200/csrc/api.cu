@@ -50,6 +50,10 @@ std::recursive_mutex g_mu;
 // Schedule tuning.  The defaults are the measured best on B200; the
 // environment overrides exist for A/B runs, are read once at initialisation, and every
 // alternative path they select is exercised by tests/test_gpu_tuning.py.
+constexpr int kSnapRing = 16;     // panel snapshots in flight (look-ahead: 2; streamed upload: its panels + 2)
+constexpr int kUpGroups = 8;      // column groups of a streamed upload
+constexpr int kUpMaxPanels = 12;  // panels factored while the upload runs (<= kSnapRing - 2)
+
 struct Tuning {
     bool lookahead = true;        // F2_NO_LOOKAHEAD=1: panel kernels in stream order, no side stream
     bool f4 = true;               // F2_SCHUR_M4RM=1: Schur update on the SMEM table kernel, not tcgen05
@@ -64,6 +68,9 @@ struct Tuning {
     // blocking, and 1024-column panels are 3-6x faster on dense inputs than the paper's
     // 64-column MMPF schedule (F2_MMPF_PANEL_BITS=64: panel kernel + HBM-streaming table-apply)
     unsigned mmpf_bits = 1024;    // F2_MMPF_PANEL_BITS
+    // host-buffer entry points: upload in column groups inside the engine, the first
+    // panels factoring while the rest of the matrix is still crossing PCIe
+    bool stream_upload = true;    // F2_NO_STREAM_UPLOAD=1: upload everything first
     bool evtl = false;            // F2_EVTL=1 (no graph): per-panel event timeline on stderr
     bool evtl_sync = false;       // F2_EVTL_SYNC=1: synchronise at every timeline mark
 
@@ -89,6 +96,7 @@ struct Tuning {
         late_pct = num("F2_LATE_PCT", late_pct);
         const int mb = num("F2_MMPF_PANEL_BITS", static_cast<int>(mmpf_bits));
         if (mb >= 64 && mb <= 1024 && mb % 64 == 0) mmpf_bits = static_cast<unsigned>(mb);
+        stream_upload = !flag("F2_NO_STREAM_UPLOAD");
         evtl = flag("F2_EVTL");
         evtl_sync = flag("F2_EVTL_SYNC");
     }
@@ -122,7 +130,18 @@ struct Ctx {
     cudaEvent_t ax_fork = nullptr, ax_join = nullptr;
     cudaEvent_t tw_fork = nullptr, tw_join = nullptr;  // wide TRSM beside the narrow one (early panels)
     cudaEvent_t nt_done = nullptr;                     // split schedule: narrow TRSM done (on the side stream)
-    int64_t* snap = nullptr;  // [2][kSnapWords]
+    int64_t* snap = nullptr;  // [kSnapRing][kSnapWords], panel p in slot p % kSnapRing
+    // streamed upload (host-buffer entry points, see enqueue_engine): ul_host set = the
+    // engine uploads the matrix itself, column group g on `up` (event up_ev[g]); groups
+    // 1.. are updated by the streaming panels on their own low-priority streams grp[g]
+    const uint64_t* ul_host = nullptr;
+    size_t ul_pitch = 0;  // words
+    bool ul_used = false;  // the engine ran with ul_host (else the matrix was never uploaded)
+    cudaStream_t up = nullptr;
+    cudaStream_t grp[kUpGroups] = {};
+    cudaEvent_t up_fork = nullptr, gathered = nullptr;
+    cudaEvent_t up_ev[kUpGroups] = {}, grp_ev[kUpGroups] = {};
+    int64_t* plans = nullptr;  // [kUpMaxPanels][kPlanWords]
     // tensor-core Schur operands (expanded L21 for every row, expanded U12 column tiles)
     uint8_t* f4_ax = nullptr;
     uint8_t* f4_bx = nullptr;
@@ -204,7 +223,16 @@ int ensure_init() {
         CK(cudaEventCreateWithFlags(&g.tw_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.tw_join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g.nt_done, cudaEventDisableTiming));
-        CK(cudaMalloc(&g.snap, sizeof(int64_t) * 2 * kSnapWords));
+        CK(cudaMalloc(&g.snap, sizeof(int64_t) * kSnapRing * kSnapWords));
+        CK(cudaStreamCreateWithFlags(&g.up, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&g.up_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g.gathered, cudaEventDisableTiming));
+        for (int i = 0; i < kUpGroups; ++i) {
+            CK(cudaStreamCreateWithPriority(&g.grp[i], cudaStreamNonBlocking, lo));
+            CK(cudaEventCreateWithFlags(&g.up_ev[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&g.grp_ev[i], cudaEventDisableTiming));
+        }
+        CK(cudaMalloc(&g.plans, sizeof(int64_t) * kUpMaxPanels * kPlanWords));
     }
     CK(cudaGetLastError());
     g.init = true;
@@ -250,9 +278,11 @@ int ensure_workspace(size_t m, size_t nq, size_t npanels, size_t scratch_words) 
 
 // expanded operands of the tensor-core Schur: A for every row, B for the trailing
 // columns plus the next panel's (t1 and t2 of one panel use disjoint regions)
-int ensure_f4(size_t m, size_t nw) {
-    const size_t a = schur_f4_a_bytes(static_cast<int64_t>(m));
-    const size_t b = schur_f4_b_bytes(static_cast<int64_t>(nw)) + schur_f4_b_bytes(kMaxPanelBits / 64);
+// (streamed upload: aslots expanded A operands, one per streaming panel, and extra_b
+// bytes of B regions for the column groups)
+int ensure_f4(size_t m, size_t nw, size_t aslots = 1, size_t extra_b = 0) {
+    const size_t a = schur_f4_a_bytes(static_cast<int64_t>(m)) * aslots;
+    const size_t b = schur_f4_b_bytes(static_cast<int64_t>(nw)) + schur_f4_b_bytes(kMaxPanelBits / 64) + extra_b;
     if (a > g.cap_f4a || b > g.cap_f4b) ++g_ws_gen;
     if (a > g.cap_f4a) {
         cudaFree(g.f4_ax);
@@ -268,7 +298,7 @@ int ensure_f4(size_t m, size_t nw) {
         CK(cudaMalloc(&g.f4_bx, b));
         g.cap_f4b = b;
     }
-    if (!g.f4_claim) CK(cudaMalloc(&g.f4_claim, 4 * sizeof(unsigned)));
+    if (!g.f4_claim) CK(cudaMalloc(&g.f4_claim, (2 + kUpGroups) * sizeof(unsigned)));
     return F2_OK;
 }
 
@@ -458,6 +488,13 @@ struct PanelStep {
     bool lookahead;
     int64_t nx;        // look-ahead: panel p+1 occupies words [t0, nx)
     int side_ctas;     // CTAs of the side chain (0: the Tuning rule)
+    // streamed upload: the column groups' streams consume the panel too -- the snapshot
+    // and the expanded L21 are made even when no trailing word is in [t0, nw), the
+    // gather is recorded in plan, and `gathered` is recorded after it
+    bool ext = false;
+    uint8_t* ax = nullptr;  // expanded L21 (nullptr: g.f4_ax)
+    int64_t* plan = nullptr;
+    cudaEvent_t gathered = nullptr;
 };
 
 // stats of the sharded schedule: Schur launches timed inside the real schedule
@@ -473,25 +510,31 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
     const Mat& A = ps.A;
     const int64_t m = A.m, nw = ps.nw, t0 = ps.t0;
     const int nleaves = static_cast<int>((ps.width + 63) / 64);
-    int64_t* snap = g.snap + (ps.p & 1) * kSnapWords;
-    if (t0 >= nw) {
+    int64_t* snap = g.snap + (ps.p % kSnapRing) * kSnapWords;
+    if (t0 >= nw && !ps.ext) {
         launch_perm(s, A, nw, g.st, g.pmap, g.scratch);
         ++g.launches;
         return pivots_final(s);
     }
-    launch_perm(s, A, nw, g.st, g.pmap, g.scratch, snap, nleaves, &ps.Cf, ps.cw0);
+    launch_perm(s, A, nw, g.st, g.pmap, g.scratch, snap, nleaves, &ps.Cf, ps.cw0, ps.plan);
     g.launches += 2;
+    if (ps.gathered) CK(cudaEventRecord(ps.gathered, s));
     evmark(s, "gather1", ps.p);
     const bool f4 = tune.f4 && g.f4_ax && ps.width >= 256;  // MMPF (W = 64) keeps the table-apply
+    uint8_t* const ax = ps.ax ? ps.ax : g.f4_ax;
     F4Job fj = pls_f4_job(A, 0, ps.width, t0, nw, &g.st->panel_r, g.st->brow);
     fj.A = ps.Cf;
     fj.aw0 = ps.cw0;
     if (f4) {  // L21 expanded on aux beside the narrow work (rk: the live state, stable until the fork)
         CK(cudaEventRecord(g.ax_fork, s));
         CK(cudaStreamWaitEvent(g.aux, g.ax_fork, 0));
-        launch_schur_f4_expand_a(g.aux, fj, g.f4_ax, g.nsm);
+        launch_schur_f4_expand_a(g.aux, fj, ax, g.nsm);
         evmark(g.aux, "expand_a", ps.p);
         CK(cudaEventRecord(g.ax_join, g.aux));
+    }
+    if (t0 >= nw) {  // (ext) nothing of the panel's own columns is left to update
+        if (f4) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
+        return pivots_final(s);
     }
     fj.rk = snap;
     fj.brow = snap + kSnapBrow;
@@ -526,7 +569,7 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
             F4Job j = fj;
             j.cw0 = j.bw0 = c0;
             j.cw1 = c1;
-            launch_schur_f4(st, j, g.f4_ax, g.f4_bx + region * schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + region,
+            launch_schur_f4(st, j, ax, g.f4_bx + region * schur_f4_b_bytes(kMaxPanelBits / 64), g.f4_claim + region,
                             grid);
         } else {
             TableApply t = ta;
@@ -607,6 +650,45 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
     return F2_OK;
 }
 
+// Streamed upload plan (host-buffer entry points).  Column group 0 = the first `ps`
+// panels, groups 1..ng-1 split the rest at panel boundaries.  While groups 1.. are still
+// crossing PCIe, panels 0..ps-1 factor inside group 0 (look-ahead schedule on words
+// [0, gb[1])) and each group's stream applies every streaming panel to its own words as
+// soon as they have landed (row gather from the recorded plan, wide TRSM, Schur); the
+// streams join before panel ps.  Needs the tensor-core look-ahead engine, n % 64 == 0 (no
+// tail word to mask) and more rows than the streaming panels can pivot.
+struct UpPlan {
+    bool on = false;
+    int ps = 0, ng = 0;
+    int64_t gb[kUpGroups + 1] = {};
+};
+
+UpPlan upload_plan(int64_t m, int64_t n, unsigned W) {
+    UpPlan u;
+    const int64_t npanels = (n + W - 1) / W;
+    if (!tune.stream_upload || !tune.lookahead || !tune.f4 || g.stats || W < 256 || n % 64 || npanels < 16) return u;
+    const int ps = static_cast<int>(std::min<int64_t>(kUpMaxPanels, npanels / 8));
+    if (m <= (ps + 1) * static_cast<int64_t>(W)) return u;
+    const int64_t pwords = W / 64, nw = n / 64;
+    const int64_t per = (npanels - ps + kUpGroups - 2) / (kUpGroups - 1);
+    u.on = true;
+    u.ps = ps;
+    u.gb[1] = ps * pwords;
+    u.ng = 1;
+    while (u.ng < kUpGroups && u.gb[u.ng] < nw) {
+        u.gb[u.ng + 1] = std::min(nw, u.gb[u.ng] + per * pwords);
+        ++u.ng;
+    }
+    return u;
+}
+
+// B regions of the column groups' Schur launches, after the narrow and wide ones
+size_t upload_b_offset(const UpPlan& u, int i) {
+    size_t o = schur_f4_b_bytes(kMaxPanelBits / 64) + schur_f4_b_bytes(u.gb[u.ng]);
+    for (int k = 1; k < i; ++k) o += schur_f4_b_bytes(u.gb[k + 1] - u.gb[k]);
+    return o;
+}
+
 // One right-looking PLS pass, enqueued on `s`.  poll = snapshot r after every panel
 // and stop enqueueing once every row is a pivot (not usable inside a graph capture).
 int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
@@ -620,6 +702,20 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
     CK(cudaMemsetAsync(&g.st->tl[2][0], 0xff, sizeof(g.st->tl[2]), s));
 #endif
     launch_pmap_init(s, g.pmap, m);
+    const UpPlan upl = g.ul_host ? upload_plan(m, n, W) : UpPlan{};
+    if (g.ul_host && !upl.on) return fail(F2_INVALID_ARGUMENT, "streamed upload requested outside its plan");
+    if (upl.on) {  // column groups on the upload stream; group 0 gates panel 0
+        CK(cudaEventRecord(g.up_fork, s));
+        CK(cudaStreamWaitEvent(g.up, g.up_fork, 0));
+        for (int i = 0; i < upl.ng; ++i) {
+            const int64_t w0 = upl.gb[i], w1 = upl.gb[i + 1];
+            CK(cudaMemcpy2DAsync(A.w + w0, A.stride * 8, g.ul_host + w0, g.ul_pitch * 8, (w1 - w0) * 8, m,
+                                 cudaMemcpyHostToDevice, g.up));
+            CK(cudaEventRecord(g.up_ev[i], g.up));
+        }
+        CK(cudaStreamWaitEvent(s, g.up_ev[0], 0));
+        for (int i = 1; i < upl.ng; ++i) CK(cudaStreamWaitEvent(g.grp[i], g.up_ev[i], 0));
+    }
     std::vector<cudaEvent_t> evs;
     int64_t checked = 0;
     bool stop = false;
@@ -648,7 +744,39 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         }
         evmark(s, "gather0", pi);
-        if (la) {
+        if (upl.on && pi < upl.ps) {
+            // streaming panel: its own update covers words [0, E) only; the groups' streams
+            // take the rest from the snapshot, the expanded L21 in slot pi and the gather plan
+            const int64_t E = upl.gb[1];
+            PanelStep ps{A, A, pw0, pi, npanels, cw, pw1, E, pw1 < E, std::min<int64_t>(E, pw1 + W / 64), 0};
+            ps.ext = true;
+            ps.ax = g.f4_ax + static_cast<size_t>(pi) * schur_f4_a_bytes(m);
+            ps.plan = g.plans + pi * kPlanWords;
+            ps.gathered = g.gathered;
+            auto factor_next = [&](cudaStream_t sd, int ctas) { panel_kernel(sd, pi + 1, ctas); };
+            if ((rc = enqueue_panel_step(ps, s, g.side, factor_next, [](cudaStream_t) { return F2_OK; }))) return rc;
+            const int64_t* snap = g.snap + (pi % kSnapRing) * kSnapWords;
+            for (int i = 1; i < upl.ng; ++i) {
+                cudaStream_t gs = g.grp[i];
+                const int64_t w0 = upl.gb[i], w1 = upl.gb[i + 1];
+                CK(cudaStreamWaitEvent(gs, g.gathered, 0));
+                CK(cudaStreamWaitEvent(gs, g.ax_join, 0));
+                launch_plan_perm(gs, A, w0, w1, ps.plan, g.scratch);
+                launch_panel_trsm_snap(gs, A, snap, nleaves, w0, w1, 8);
+                const F4Job j = pls_f4_job(A, pw0, cw, w0, w1, snap, snap + kSnapBrow);
+                launch_schur_f4(gs, j, ps.ax, g.f4_bx + upload_b_offset(upl, i), g.f4_claim + 2 + i, g.nsm);
+                g.launches += 5;
+            }
+            if (pi == upl.ps - 1) {  // join; the streaming panels' rows are final now
+                for (int i = 1; i < upl.ng; ++i) {
+                    CK(cudaEventRecord(g.grp_ev[i], g.grp[i]));
+                    CK(cudaStreamWaitEvent(s, g.grp_ev[i], 0));
+                }
+                for (int64_t k = 0; k < upl.ps; ++k)
+                    if ((rc = enqueue_download(A, k * W, W, s))) return rc;
+                if (pi + 1 < npanels) panel_kernel(s, pi + 1, g.nsm);
+            }
+        } else if (la) {
             PanelStep ps{A, A, pw0, pi, npanels, cw, pw1, nw, pw1 < nw, std::min<int64_t>(nw, pw1 + W / 64), 0};
             auto factor_next = [&](cudaStream_t sd, int ctas) { panel_kernel(sd, pi + 1, ctas); };
             auto pivots_final = [&](cudaStream_t st_) { return enqueue_download(A, c, W, st_); };
@@ -723,6 +851,8 @@ struct GraphCache {
     uint64_t* w = nullptr;
     uint64_t* dl_host = nullptr;
     size_t dl_pitch = 0;
+    const uint64_t* ul_host = nullptr;
+    size_t ul_pitch = 0;
     int64_t m = 0, n = 0, stride = 0;
     unsigned W = 0;
     uint64_t gen = 0;
@@ -742,14 +872,19 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     int rc = ensure_workspace(static_cast<size_t>(m), static_cast<size_t>(std::min(m, n)), static_cast<size_t>(npanels),
                               static_cast<size_t>(kMaxMoved) * static_cast<size_t>(A.stride));
     if (rc) return rc;
-    if (tune.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw)))) return rc;
+    const UpPlan upl = g.ul_host ? upload_plan(m, A.n, W) : UpPlan{};
+    if (g.ul_host) g.ul_used = true;
+    if (tune.f4 && (rc = ensure_f4(static_cast<size_t>(m), static_cast<size_t>(nw), upl.on ? upl.ps : 1,
+                                   upl.on ? upload_b_offset(upl, upl.ng) - upload_b_offset(upl, 1) : 0)))
+        return rc;
     cudaStream_t s = g.stream;
     const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && tune.graph;
     g_evtl = !use_graph && tune.evtl;
     if (use_graph) {
         const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
                          g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen &&
-                         g_graph.dl_host == g.dl_host && g_graph.dl_pitch == g.dl_pitch;
+                         g_graph.dl_host == g.dl_host && g_graph.dl_pitch == g.dl_pitch &&
+                         g_graph.ul_host == g.ul_host && g_graph.ul_pitch == g.ul_pitch;
         if (!hit) {
             if (g_graph.exec) cudaGraphExecDestroy(g_graph.exec);
             g_graph.exec = nullptr;
@@ -779,6 +914,8 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             g_graph.w = A.w;
             g_graph.dl_host = g.dl_host;
             g_graph.dl_pitch = g.dl_pitch;
+            g_graph.ul_host = g.ul_host;
+            g_graph.ul_pitch = g.ul_pitch;
             g_graph.m = m;
             g_graph.n = n;
             g_graph.stride = A.stride;
@@ -1181,20 +1318,31 @@ static int pls_host(bool recursive, uint64_t* words, size_t nrows, size_t ncols,
         if ((rc = alloc_matrix(nrows, ncols, &g_host_mat))) return rc;
     }
     f2_matrix* a = g_host_mat;
-    rc = f2_matrix_upload(a, words, stride_words);
-    // pinned host buffer: finished pivot rows stream back while later panels compute
+    // pinned host buffer: finished pivot rows stream back while later panels compute, and
+    // (upload_plan) the engine uploads the matrix itself, factoring the first panels while
+    // the rest is still in flight
     cudaPointerAttributes pa{};
     const bool pinned = cudaPointerGetAttributes(&pa, words) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
                         nrows > 0 && ncols > 0;
     cudaGetLastError();
+    const unsigned W = recursive ? g.panel_bits : tune.mmpf_bits;
+    const bool streamed = pinned && stride_words >= (ncols + 63) / 64 &&
+                          upload_plan(static_cast<int64_t>(nrows), static_cast<int64_t>(ncols), W).on;
+    rc = streamed ? F2_OK : f2_matrix_upload(a, words, stride_words);
     if (!rc) {
         g.dl_host = pinned ? words : nullptr;
         g.dl_pitch = stride_words;
         g.dl_done = -1;
+        g.ul_host = streamed ? words : nullptr;
+        g.ul_pitch = stride_words;
+        g.ul_used = false;
         f2_window w{0, 0, nrows, ncols};
         rc = recursive ? f2_pls_recursive(a, w, p, nrows, q, ncols, cfg, rank)
                        : f2_mmpf_pls(a, w, p, nrows, q, ncols, k, rank);
         g.dl_host = nullptr;
+        g.ul_host = nullptr;
+        // (an argument error before the engine: the host matrix stays as it was)
+        if (streamed && !g.ul_used) return rc;
     }
     if (!rc) {
         const int64_t done = g.dl_done < 0 ? 0 : g.dl_done;

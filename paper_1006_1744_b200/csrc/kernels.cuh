@@ -33,7 +33,12 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // the panel's row gather; with snap != nullptr the same launch also takes the panel's
 // snapshot (kSnap* below) from Cf's words coef_w0.. (Cf == A: read through pmap)
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch,
-                 int64_t* snap = nullptr, int nleaves = 0, const Mat* Cf = nullptr, int64_t coef_w0 = 0);
+                 int64_t* snap = nullptr, int nleaves = 0, const Mat* Cf = nullptr, int64_t coef_w0 = 0,
+                 int64_t* plan = nullptr);
+// plan (1 + 2 * kMaxMoved words): the gather's {count, (destination, source) rows...}, so
+// launch_plan_perm can repeat it later on words [w0, w1) (w0 even: 16-byte accesses)
+constexpr int64_t kPlanWords = 1 + 2 * static_cast<int64_t>(kMaxMoved);
+void launch_plan_perm(cudaStream_t s, const Mat& A, int64_t w0, int64_t w1, const int64_t* plan, uint64_t* scratch);
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m);
 void launch_panel_lmaps(cudaStream_t s, const Mat& Cf, int64_t pw0, int nleaves, PlsState* st);
 constexpr int64_t dist_header_words(int W) { return 4 + 2 * static_cast<int64_t>(W) + 2 * kMaxMoved; }

@@ -240,7 +240,7 @@ __device__ __forceinline__ void snapshot_block(const PlsState* st, int64_t* snap
 // reading the pivot rows through pmap: one launch instead of two on the serial path.
 __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const PlsState* st, const int64_t* pmap,
                                                   uint64_t* scratch, unsigned gx, unsigned gy, int64_t* snap, Mat Cf,
-                                                  int64_t coef_w0, int nleaves) {
+                                                  int64_t coef_w0, int nleaves, int64_t* plan) {
     pdl_wait();
     const unsigned b = blockIdx.x;
     if (b >= gx * gy) {
@@ -250,6 +250,14 @@ __global__ void __launch_bounds__(256) k_perm_save(Mat A, int64_t nwords, const 
         return;
     }
     const int n = st->nmoved;
+    if (plan && b == 0) {  // the gather as (destination, source) row pairs, for k_plan_save/put
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int64_t x = st->moved[i];
+            plan[1 + 2 * i] = x;
+            plan[2 + 2 * i] = pmap[x];
+        }
+        if (threadIdx.x == 0) plan[0] = n;
+    }
     const int64_t k = 2 * (static_cast<int64_t>(b % gx) * blockDim.x + threadIdx.x);  // word pair (16 B)
     if (k >= nwords) return;
     for (int i = b / gx; i < n; i += gy) {
@@ -277,6 +285,34 @@ __global__ void __launch_bounds__(256) k_perm_put(Mat A, int64_t nwords, const P
     }
 }
 
+// The same gather on words [w0, w1) only, from a plan k_perm_save recorded: the columns
+// a streamed upload delivers after the panel's own gather ran (api.cu, enqueue_engine).
+__global__ void __launch_bounds__(256) k_plan_save(Mat A, int64_t w0, int64_t w1, const int64_t* plan,
+                                                  uint64_t* scratch, unsigned gx, unsigned gy) {
+    const int n = static_cast<int>(plan[0]);
+    const int64_t k = w0 + 2 * (static_cast<int64_t>(blockIdx.x % gx) * blockDim.x + threadIdx.x);
+    if (k >= w1) return;
+    for (int i = blockIdx.x / gx; i < n; i += gy) {
+        const uint64_t* src = A.w + plan[2 + 2 * i] * A.stride + k;
+        uint64_t* dst = scratch + static_cast<int64_t>(i) * A.stride + k;
+        if (k + 1 < w1) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        else dst[0] = src[0];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_plan_put(Mat A, int64_t w0, int64_t w1, const int64_t* plan,
+                                                 const uint64_t* scratch, unsigned gx, unsigned gy) {
+    const int n = static_cast<int>(plan[0]);
+    const int64_t k = w0 + 2 * (static_cast<int64_t>(blockIdx.x % gx) * blockDim.x + threadIdx.x);
+    if (k >= w1) return;
+    for (int i = blockIdx.x / gx; i < n; i += gy) {
+        const uint64_t* src = scratch + static_cast<int64_t>(i) * A.stride + k;
+        uint64_t* dst = A.w + plan[1 + 2 * i] * A.stride + k;
+        if (k + 1 < w1) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        else dst[0] = src[0];
+    }
+}
+
 __global__ void k_pmap_init(int64_t* pmap, int64_t m) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -285,15 +321,23 @@ __global__ void k_pmap_init(int64_t* pmap, int64_t m) {
 
 
 void launch_perm(cudaStream_t s, const Mat& A, int64_t nwords, const PlsState* st, int64_t* pmap, uint64_t* scratch,
-                 int64_t* snap, int nleaves, const Mat* Cf, int64_t coef_w0) {
+                 int64_t* snap, int nleaves, const Mat* Cf, int64_t coef_w0, int64_t* plan) {
     // rows are 128-byte aligned (stride % 16 words == 0): 16-byte accesses, ~1024 CTAs
     const unsigned gx = static_cast<unsigned>((nwords + 511) / 512);
     const unsigned gy = gx >= 1024 ? 1u : 1024u / gx;
     const unsigned nsnap = snap ? static_cast<unsigned>(nleaves * ((nleaves * 64 + 255) / 256)) : 0u;
     const Mat cf = Cf ? *Cf : A;
     launch_pdl(k_perm_save, dim3(gx * gy + nsnap), dim3(256), 0, s, A, nwords, st, static_cast<const int64_t*>(pmap),
-               scratch, gx, gy, snap, cf, coef_w0, nleaves);
+               scratch, gx, gy, snap, cf, coef_w0, nleaves, plan);
     launch_pdl(k_perm_put, dim3(gx, gy), dim3(256), 0, s, A, nwords, st, pmap, static_cast<const uint64_t*>(scratch));
+}
+
+void launch_plan_perm(cudaStream_t s, const Mat& A, int64_t w0, int64_t w1, const int64_t* plan, uint64_t* scratch) {
+    if (w1 <= w0) return;
+    const unsigned gx = static_cast<unsigned>((w1 - w0 + 511) / 512);
+    const unsigned gy = gx >= 1024 ? 1u : 1024u / gx;
+    k_plan_save<<<gx * gy, 256, 0, s>>>(A, w0, w1, plan, scratch, gx, gy);
+    k_plan_put<<<gx * gy, 256, 0, s>>>(A, w0, w1, plan, static_cast<const uint64_t*>(scratch), gx, gy);
 }
 
 void launch_pmap_init(cudaStream_t s, int64_t* pmap, int64_t m) {

@@ -207,3 +207,37 @@ def test_host_entry_points_streamed_download(f2, oracle, pinned):
                 qq = q
             assert res.rank == r and (res.P == p).all() and (res.Q == qq).all(), (m, n, recursive)
             assert (h == w).all(), (m, n, recursive, "packed")
+
+
+@pytest.mark.parametrize("m,n,kind", [(4096, 16384, "dense"), (5000, 16384, "xy"), (3500, 16448, "sparse"),
+                                      (12288, 32768, "dense"), (10000, 20480, "xy")])
+def test_host_streamed_upload(f2, oracle, m, n, kind):
+    """Pinned host buffers with >= 16 panels: the engine uploads the matrix itself in
+    column groups and factors the first panels while the rest is in flight (api.cu,
+    upload_plan).  Small cases against the Gaussian oracle, large ones against the same
+    decomposition of a device matrix (no streamed upload), which the oracle pins elsewhere."""
+    if kind == "xy":
+        inner = m // 2
+        a = oracle.mul(oracle.randomize(m, inner, 0.5, 5), inner, oracle.randomize(inner, n, 0.5, 6), n)
+    elif kind == "sparse":
+        a = oracle.fixed_weight(m, n, 4, 7)
+    else:
+        a = oracle.randomize(m, n, 0.5, m + n)
+    cfg = f2.EliminationConfig(cutoff_bytes=4096)
+    if m * n <= 5000 * 16448:
+        w, p, q, r = oracle.gauss_pls(a, n)
+        qr = oracle.recursive_q(m, n, 4096, q[:r])
+    else:
+        d = f2.DeviceMatrix.from_host(a, n)
+        res = f2.pls_recursive(d, cfg)
+        w, p, qr, r = d.download(), res.P, res.Q, res.rank
+        d2 = f2.DeviceMatrix.from_host(a, n)
+        q = f2.mmpf_pls(d2).Q
+    for recursive in (True, False):
+        for rep in range(2):  # the second call replays the cached graph
+            h = f2.pinned_empty(a.shape)
+            np.copyto(h, a)
+            res = f2.pls_recursive_host(h, n, cfg) if recursive else f2.mmpf_pls_host(h, n)
+            assert res.rank == r and (res.P == p).all(), (m, n, kind, recursive, rep)
+            assert (res.Q == (qr if recursive else q)).all(), (m, n, kind, recursive, rep, "Q")
+            assert (h == w).all(), (m, n, kind, recursive, rep, "packed")

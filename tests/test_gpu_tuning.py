@@ -33,6 +33,14 @@ SCRIPT = textwrap.dedent("""
         res = f2.mmpf_pls(d)
         assert res.rank == r and (res.P == p).all() and (res.Q == q).all() and (d.download() == w).all(), \\
             ("mmpf", m, n)
+    # host buffers past the streamed-upload threshold (16 panels)
+    m, n = 4096, 16384
+    a = o.randomize(m, n, 0.5, 9)
+    w, p, q, r = o.gauss_pls(a, n)
+    h = f2.pinned_empty(a.shape)
+    np.copyto(h, a)
+    res = f2.pls_recursive_host(h, n, f2.EliminationConfig(cutoff_bytes=4096))
+    assert res.rank == r and (res.P == p).all() and (h == w).all(), "host"
     print("ok")
 """)
 
@@ -52,6 +60,8 @@ SCRIPT = textwrap.dedent("""
     {"F2_MMPF_PANEL_BITS": "64"},
     {"F2_MMPF_PANEL_BITS": "64", "F2_NO_LOOKAHEAD": "1"},
     {"F2_MMPF_PANEL_BITS": "256"},
+    {"F2_NO_STREAM_UPLOAD": "1"},
+    {"F2_NO_GRAPH": "1", "F2_NO_EARLY_WIDE_TRSM": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_tuning_switch_stays_exact(env):
     full = dict(os.environ, **env)
