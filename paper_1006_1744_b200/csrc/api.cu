@@ -51,8 +51,8 @@ std::recursive_mutex g_mu;
 // environment overrides exist for A/B runs, are read once at initialisation, and every
 // alternative path they select is exercised by tests/test_gpu_tuning.py.
 constexpr int kSnapRing = 16;     // panel snapshots in flight (look-ahead: 2; streamed upload: its panels + 2)
-constexpr int kUpGroups = 8;      // column groups of a streamed upload
-constexpr int kUpMaxPanels = 12;  // panels factored while the upload runs (<= kSnapRing - 2)
+constexpr int kUpGroups = 11;     // column groups of a streamed upload
+constexpr int kUpMaxPanels = 14;  // panels factored while the upload runs (<= kSnapRing - 2)
 
 struct Tuning {
     bool lookahead = true;        // F2_NO_LOOKAHEAD=1: panel kernels in stream order, no side stream
@@ -71,6 +71,12 @@ struct Tuning {
     // host-buffer entry points: upload in column groups inside the engine, the first
     // panels factoring while the rest of the matrix is still crossing PCIe
     bool stream_upload = true;    // F2_NO_STREAM_UPLOAD=1: upload everything first
+    // its plan (upload_plan): group 0 = up_g0 panels, the rest in up_groups - 1 equal
+    // groups; streaming panels 0 .. up_ps - 2, their look-ahead kernels on up_side CTAs
+    int up_g0 = 8;                // F2_UP_G0
+    int up_ps = 9;                // F2_UP_PS (<= kUpMaxPanels)
+    int up_groups = 8;            // F2_UP_GROUPS (<= kUpGroups)
+    int up_side = 48;             // F2_UP_SIDE
     bool evtl = false;            // F2_EVTL=1 (no graph): per-panel event timeline on stderr
     bool evtl_sync = false;       // F2_EVTL_SYNC=1: synchronise at every timeline mark
 
@@ -97,6 +103,11 @@ struct Tuning {
         const int mb = num("F2_MMPF_PANEL_BITS", static_cast<int>(mmpf_bits));
         if (mb >= 64 && mb <= 1024 && mb % 64 == 0) mmpf_bits = static_cast<unsigned>(mb);
         stream_upload = !flag("F2_NO_STREAM_UPLOAD");
+        up_g0 = std::max(1, num("F2_UP_G0", up_g0));
+        up_ps = std::min(kUpMaxPanels, std::max(2, num("F2_UP_PS", up_ps)));
+        up_groups = std::min(kUpGroups, std::max(2, num("F2_UP_GROUPS", up_groups)));
+        const int us = num("F2_UP_SIDE", up_side);
+        if (us >= 2 && us <= nsm) up_side = us;
         evtl = flag("F2_EVTL");
         evtl_sync = flag("F2_EVTL_SYNC");
     }
@@ -650,13 +661,15 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
     return F2_OK;
 }
 
-// Streamed upload plan (host-buffer entry points).  Column group 0 = the first `ps`
-// panels, groups 1..ng-1 split the rest at panel boundaries.  While groups 1.. are still
-// crossing PCIe, panels 0..ps-1 factor inside group 0 (look-ahead schedule on words
-// [0, gb[1])) and each group's stream applies every streaming panel to its own words as
-// soon as they have landed (row gather from the recorded plan, wide TRSM, Schur); the
-// streams join before panel ps.  Needs the tensor-core look-ahead engine, n % 64 == 0 (no
-// tail word to mask) and more rows than the streaming panels can pivot.
+// Streamed upload plan (host-buffer entry points).  The matrix crosses PCIe in column
+// groups at panel boundaries: group 0 = the first up_g0 panels, the rest in equal groups.
+// Panels 0 .. ps-2 are "streaming": panel p's own update covers the main region -- the
+// groups already joined into the main stream -- and every other group's stream applies
+// the panel to its own words once they have landed (row gather from the recorded plan,
+// wide TRSM, Schur, from the panel's snapshot and its own expanded L21).  A group joins
+// the main stream when the chain reaches it (before the step whose look-ahead factors
+// the group's first panel); all of them join before panel ps-1's step.  Needs the
+// tensor-core look-ahead engine and n % 64 == 0 (no tail word to mask).
 struct UpPlan {
     bool on = false;
     int ps = 0, ng = 0;
@@ -666,19 +679,20 @@ struct UpPlan {
 UpPlan upload_plan(int64_t m, int64_t n, unsigned W) {
     UpPlan u;
     const int64_t npanels = (n + W - 1) / W;
-    if (!tune.stream_upload || !tune.lookahead || !tune.f4 || g.stats || W < 256 || n % 64 || npanels < 16) return u;
-    const int ps = static_cast<int>(std::min<int64_t>(kUpMaxPanels, npanels / 8));
-    if (m <= (ps + 1) * static_cast<int64_t>(W)) return u;
-    const int64_t pwords = W / 64, nw = n / 64;
-    const int64_t per = (npanels - ps + kUpGroups - 2) / (kUpGroups - 1);
+    if (!tune.stream_upload || !tune.lookahead || !tune.f4 || g.stats || W < 256 || n % 64 || npanels < 16 ||
+        m < 2 * static_cast<int64_t>(W))
+        return u;
+    const int64_t pwords = W / 64, nw = n / 64, g0 = std::min<int64_t>(tune.up_g0, npanels / 2);
+    const int64_t per = (npanels - g0 + tune.up_groups - 2) / (tune.up_groups - 1);
     u.on = true;
-    u.ps = ps;
-    u.gb[1] = ps * pwords;
+    u.ps = static_cast<int>(std::min<int64_t>(tune.up_ps, npanels - 2));
+    u.gb[1] = g0 * pwords;
     u.ng = 1;
-    while (u.ng < kUpGroups && u.gb[u.ng] < nw) {
+    while (u.ng < tune.up_groups && u.gb[u.ng] < nw) {
         u.gb[u.ng + 1] = std::min(nw, u.gb[u.ng] + per * pwords);
         ++u.ng;
     }
+    u.gb[u.ng] = nw;
     return u;
 }
 
@@ -712,10 +726,12 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             CK(cudaMemcpy2DAsync(A.w + w0, A.stride * 8, g.ul_host + w0, g.ul_pitch * 8, (w1 - w0) * 8, m,
                                  cudaMemcpyHostToDevice, g.up));
             CK(cudaEventRecord(g.up_ev[i], g.up));
+            evmark(g.up, "uploaded", i);
         }
         CK(cudaStreamWaitEvent(s, g.up_ev[0], 0));
         for (int i = 1; i < upl.ng; ++i) CK(cudaStreamWaitEvent(g.grp[i], g.up_ev[i], 0));
     }
+    int joined = upl.on ? 1 : 0;  // groups [0, joined) form the main region
     std::vector<cudaEvent_t> evs;
     int64_t checked = 0;
     bool stop = false;
@@ -744,19 +760,34 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             launch_panel_pipe(s, A, pw0, static_cast<int>(cw), pw1, g.st, g.P, g.Qp, g.pmap, 0, g.bar, g.nsm);
         }
         evmark(s, "gather0", pi);
-        if (upl.on && pi < upl.ps) {
-            // streaming panel: its own update covers words [0, E) only; the groups' streams
-            // take the rest from the snapshot, the expanded L21 in slot pi and the gather plan
-            const int64_t E = upl.gb[1];
+        if (upl.on && joined < upl.ng) {
+            // join the groups the chain has reached: panel pi+1 (factored during this step)
+            // must lie in the main region; past the streaming panels, every group
+            const int64_t nxw = pi + 1 < npanels && pi < upl.ps - 1 ? (pi + 1) * (W / 64) : nw;
+            while (joined < upl.ng && upl.gb[joined] <= nxw) {
+                CK(cudaEventRecord(g.grp_ev[joined], g.grp[joined]));
+                CK(cudaStreamWaitEvent(s, g.grp_ev[joined], 0));
+                evmark(s, "joined", joined);
+                ++joined;
+            }
+            if (joined == upl.ng)  // the streaming panels' rows are final in every column now
+                for (int64_t k = 0; k < pi; ++k)
+                    if ((rc = enqueue_download(A, k * W, W, s))) return rc;
+        }
+        if (upl.on && joined < upl.ng) {
+            // streaming panel: its own update covers the main region [0, E); the other
+            // groups' streams take the rest from the snapshot, L21 in slot pi and the plan
+            const int64_t E = upl.gb[joined];
             PanelStep ps{A, A, pw0, pi, npanels, cw, pw1, E, pw1 < E, std::min<int64_t>(E, pw1 + W / 64), 0};
             ps.ext = true;
             ps.ax = g.f4_ax + static_cast<size_t>(pi) * schur_f4_a_bytes(m);
             ps.plan = g.plans + pi * kPlanWords;
             ps.gathered = g.gathered;
+            ps.side_ctas = tune.up_side;
             auto factor_next = [&](cudaStream_t sd, int ctas) { panel_kernel(sd, pi + 1, ctas); };
             if ((rc = enqueue_panel_step(ps, s, g.side, factor_next, [](cudaStream_t) { return F2_OK; }))) return rc;
             const int64_t* snap = g.snap + (pi % kSnapRing) * kSnapWords;
-            for (int i = 1; i < upl.ng; ++i) {
+            for (int i = joined; i < upl.ng; ++i) {
                 cudaStream_t gs = g.grp[i];
                 const int64_t w0 = upl.gb[i], w1 = upl.gb[i + 1];
                 CK(cudaStreamWaitEvent(gs, g.gathered, 0));
@@ -766,15 +797,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
                 const F4Job j = pls_f4_job(A, pw0, cw, w0, w1, snap, snap + kSnapBrow);
                 launch_schur_f4(gs, j, ps.ax, g.f4_bx + upload_b_offset(upl, i), g.f4_claim + 2 + i, g.nsm);
                 g.launches += 5;
-            }
-            if (pi == upl.ps - 1) {  // join; the streaming panels' rows are final now
-                for (int i = 1; i < upl.ng; ++i) {
-                    CK(cudaEventRecord(g.grp_ev[i], g.grp[i]));
-                    CK(cudaStreamWaitEvent(s, g.grp_ev[i], 0));
-                }
-                for (int64_t k = 0; k < upl.ps; ++k)
-                    if ((rc = enqueue_download(A, k * W, W, s))) return rc;
-                if (pi + 1 < npanels) panel_kernel(s, pi + 1, g.nsm);
+                evmark(gs, i == upl.ng - 1 ? "group_last" : "group", pi);
             }
         } else if (la) {
             PanelStep ps{A, A, pw0, pi, npanels, cw, pw1, nw, pw1 < nw, std::min<int64_t>(nw, pw1 + W / 64), 0};
@@ -827,7 +850,7 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
             CK(cudaEventRecord(ev, s));
             evs.push_back(ev);
             while (checked < static_cast<int64_t>(evs.size()) && cudaEventQuery(evs[checked]) == cudaSuccess) {
-                if (g.h_r[checked] >= m) stop = true;
+                if (g.h_r[checked] >= m && !(upl.on && joined < upl.ng)) stop = true;
                 ++checked;
             }
         }

@@ -61,6 +61,7 @@ SCRIPT = textwrap.dedent("""
     {"F2_MMPF_PANEL_BITS": "64", "F2_NO_LOOKAHEAD": "1"},
     {"F2_MMPF_PANEL_BITS": "256"},
     {"F2_NO_STREAM_UPLOAD": "1"},
+    {"F2_UP_G0": "2", "F2_UP_PS": "14", "F2_UP_GROUPS": "11", "F2_UP_SIDE": "148"},
     {"F2_NO_GRAPH": "1", "F2_NO_EARLY_WIDE_TRSM": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_tuning_switch_stays_exact(env):
