@@ -837,6 +837,12 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                         ++pkc;
                         nstate = j + 1 < nleaves ? S_CARRY : S_FINAL;
                         nleaf = j + 1;
+                        // every row is a pivot (r = m, e.g. a wide matrix past its rank): the
+                        // remaining leaves have no rows to pivot or update -- straight to the
+                        // final step (the workers still take this leaf's packet: CTA 1 builds
+                        // its TRSM map there), so the empty panels after full row rank cost
+                        // one leaf instead of sixteen
+                        if (st->r >= A.m) nstate = S_FINAL;
                     } else {  // undecidable in the window: hand the window back, search globally
                         pipe_write_back(A, pw0, nwp, S, Z, pb);
                         nstate = S_GENERAL;
