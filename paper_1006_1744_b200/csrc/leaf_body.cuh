@@ -484,9 +484,19 @@ __device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, 
 // Positions are relative to base = st->r; `src` is the relative (pre-leaf)
 // position of the content a lane holds.  Rows are read through pmap.
 // The general search of the panel kernel (its fast window could not decide the leaf).
+//
+// Sparse leaves (a column's candidates scattered over the whole matrix, so nearly every
+// column needs a scan): the first scan of the leaf visits every position past the window
+// and keeps each row whose caught-up leaf word is nonzero in a compact list in `cmem`
+// (cap entries: position, source, word, pivots applied).  A row whose leaf word is zero is
+// never touched by the leaf's eliminations and never becomes a candidate, so the later
+// scans of the leaf visit the list only (in SMEM, catching each entry up on the new
+// pivots), with the same keys -- (column, position) minimum -- as the full scan.  An
+// outside pivot's position receives the window row it swaps with; its entry is
+// updated in place.  More nonzero rows than cap: full scans, as without a list.
 static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, int lw, int first_in_panel, int leaf_in_panel,
                                 int panel_bits, PlsState* st, int64_t* P, int64_t* Qp, int64_t* pmap,
-                                int64_t qcol_off) {
+                                int64_t qcol_off, uint8_t* cmem = nullptr, int cap = 0) {
     __syncthreads();
     __shared__ uint64_t s_u[64];
     __shared__ uint64_t s_uf[64];
@@ -501,6 +511,11 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
     __shared__ int s_cmd, s_col, s_lim, s_t, s_ob;
     __shared__ int s_nom;
     __shared__ int64_t s_om_pos[64];
+    __shared__ int s_cn, s_cstate, s_bidx;  // compact list: entries, 0 none yet / 1 valid / 2 off
+    uint64_t* const c_w = reinterpret_cast<uint64_t*>(cmem);
+    int* const c_pos = reinterpret_cast<int*>(cmem + 8 * static_cast<size_t>(cap));
+    int* const c_src = c_pos + cap;
+    uint8_t* const c_tt = reinterpret_cast<uint8_t*>(c_src + cap);
 
 #ifdef F2_LEAF_PROFILE
     long long c_start = clock64();
@@ -521,6 +536,9 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
     if (tid == 0) {
         s_nom = 0;
         if (first_in_panel) st->nmoved = 0;
+        s_cn = 0;
+        s_cstate = cmem && cap > 0 ? 0 : 2;
+        s_bidx = -1;
     }
     __syncthreads();
 
@@ -681,9 +699,49 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
 
         // ---- block-wide scan of positions [ob, m) for the leftmost column in [col, lim)
         const int64_t ob = base + s_ob;
-        {
+        if (s_cstate == 1) {  // the leaf's nonzero rows past the first scan's window, in SMEM
+            const int c0 = s_col, tt = s_t, lim = s_lim, cn = s_cn;
+            if (tid == 0) s_best = KEY_NONE;
+            __syncthreads();
+            for (int i0 = 0; i0 < cn; i0 += blockDim.x) {
+                const int i = i0 + tid;
+                unsigned long long key = KEY_NONE;
+                uint64_t v = 0;
+                if (i < cn) {
+                    const int64_t pp = base + c_pos[i];
+                    if (pp >= ob) {
+                        v = c_w[i];
+                        for (int l = c_tt[i]; l < tt; ++l)
+                            if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
+                        c_w[i] = v;
+                        c_tt[i] = static_cast<uint8_t>(tt);
+                        uint64_t z = v & (~0ull << c0);
+                        if (lim < 64) z &= (1ull << lim) - 1;
+                        if (z)
+                            key = (static_cast<unsigned long long>(__ffsll(static_cast<long long>(z)) - 1) << 48) |
+                                  static_cast<unsigned long long>(pp - ob);
+                    }
+                }
+                unsigned long long k = warp_min64(key);
+                if (lane == 0) s_red[warp] = k;
+                __syncthreads();
+                if (warp == 0) {
+                    unsigned long long kk = lane < nwarps ? s_red[lane] : KEY_NONE;
+                    kk = warp_min64(kk);
+                    if (lane == 0 && kk < s_best) s_best = kk;
+                }
+                __syncthreads();
+                if (key != KEY_NONE && key == s_best) {
+                    s_bword = v;
+                    s_bsrc = base + c_src[i];
+                    s_bidx = i;
+                }
+            }
+            __syncthreads();
+        } else {
             const int c0 = s_col, tt = s_t;
             int lim = s_lim;
+            const bool build = s_cstate == 0;  // first scan: every position, listing the nonzero rows
             if (tid == 0) s_best = KEY_NONE;
             __syncthreads();
             for (int64_t b = ob; b < m; b += blockDim.x) {
@@ -702,6 +760,16 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
                         key = (static_cast<unsigned long long>(__ffsll(static_cast<long long>(z)) - 1) << 48) |
                               static_cast<unsigned long long>(pp - ob);
                 }
+                int myidx = -1;
+                if (build && v != 0) {
+                    myidx = atomicAdd(&s_cn, 1);
+                    if (myidx < cap) {
+                        c_w[myidx] = v;
+                        c_pos[myidx] = static_cast<int>(pp - base);
+                        c_src[myidx] = static_cast<int>(sp - base);
+                        c_tt[myidx] = static_cast<uint8_t>(tt);
+                    }
+                }
                 unsigned long long k = warp_min64(key);
                 if (lane == 0) s_red[warp] = k;
                 __syncthreads();
@@ -715,13 +783,16 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
                 if (key != KEY_NONE && key == bk) {
                     s_bword = v;
                     s_bsrc = sp;
+                    s_bidx = myidx;
                 }
                 if (bk != KEY_NONE) {
                     const int bc = static_cast<int>(bk >> 48);
-                    if (bc == c0) break;
+                    if (bc == c0 && !build) break;
                     lim = bc;
                 }
             }
+            __syncthreads();
+            if (build && tid == 0) s_cstate = s_cn <= cap ? 1 : 2;
             __syncthreads();
         }
 
@@ -735,9 +806,16 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
                 const int64_t pstar = ob + static_cast<int64_t>(bk & ((1ull << 48) - 1));
                 const uint64_t u = s_bword;
                 const int psrc = __shfl_sync(FULL, src, pr);
+                const uint64_t wpr = __shfl_sync(FULL, w, pr);
                 if (lane == pr) {
                     w = u;
                     src = static_cast<int>(s_bsrc - base);
+                }
+                if (lane == 0 && s_cstate == 1) {  // pstar's list entry now holds p's row (t pivots applied)
+                    const int bi = s_bidx;
+                    c_w[bi] = wpr;
+                    c_src[bi] = psrc;
+                    c_tt[bi] = static_cast<uint8_t>(t);
                 }
                 if (lane == 0) {
                     omap_put(s_om, pstar, base + psrc);
@@ -786,22 +864,33 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
     F2_MARK(3);
     if (warp == 0) {
         record_moves(bb + lane < span && src != bb + lane, bb + lane, src);
-        if (lane == 0) {
-            for (int i = 0; i < s_nom; ++i) {
-                const int64_t pp = s_om_pos[i];
-                if (pp < base + bb + 32) continue;  // absorbed by the window: recorded above
-                bool dup = false;
-                for (int j = 0; j < i; ++j) dup |= (s_om_pos[j] == pp);
-                if (dup) continue;
-                const int64_t v = omap_get(s_om, pp);
-                if (v != pp) {
-                    s_mv_dst[nmv] = pp;
-                    s_mv_phys[nmv] = pmap[v];
-                    ++nmv;
+        // the outside positions that received another row (first occurrence of each; the ones
+        // the window absorbed were recorded above), across the warp in list order
+        const int nom = s_nom;
+        for (int i0 = 0; i0 < nom; i0 += 32) {
+            const int i = i0 + lane;
+            bool keep = false;
+            int64_t pp = 0, v = 0;
+            if (i < nom) {
+                pp = s_om_pos[i];
+                if (pp >= base + bb + 32) {
+                    bool dup = false;
+                    for (int j = 0; j < i; ++j) dup |= (s_om_pos[j] == pp);
+                    if (!dup) {
+                        v = omap_get(s_om, pp);
+                        keep = v != pp;
+                    }
                 }
             }
-            s_nmv = nmv;
+            const unsigned bm = __ballot_sync(FULL, keep);
+            if (keep) {
+                const int idx = nmv + __popc(bm & ((1u << lane) - 1));
+                s_mv_dst[idx] = pp;
+                s_mv_phys[idx] = pmap[v];
+            }
+            nmv += __popc(bm);
         }
+        if (lane == 0) s_nmv = nmv;
     }
     __syncthreads();
     const int nmv_all = s_nmv;

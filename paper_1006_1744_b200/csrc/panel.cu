@@ -851,7 +851,9 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 }
             } else if (state == S_GENERAL) {
                 const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
-                leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off);
+                // (the window is written back: its SMEM holds the search's compact row list)
+                leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off,
+                                reinterpret_cast<uint8_t*>(dsm), static_cast<int>(kPipeSmem / 17) & ~63);
                 __syncthreads();
                 load_leaf(st, L);
                 if (threadIdx.x < 64) st->fbasis[threadIdx.x] = L.fb[threadIdx.x];

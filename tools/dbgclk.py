@@ -10,4 +10,4 @@ for m, n in [(65536, 2048), (16384, 2048)]:
     for rep in range(3):
         b = a.clone(); f2.pls_recursive(b, f2.EliminationConfig(cutoff_bytes=1 << 10))
     cl = (C.c_longlong * 32)(); L.f2_debug_clocks(cl, 32)
-    print(m, n, {k: cl[k] for k in range(20, 32)})
+    print(m, n, {k: cl[k] for k in list(range(8, 18)) + list(range(20, 32))})
