@@ -221,7 +221,7 @@ int ensure_init() {
     setup_misc_kernels();
     setup_rref_kernels();
     setup_panel_kernels();
-    CK(cudaMalloc(&g.bar, sizeof(unsigned)));
+    CK(cudaMalloc(&g.bar, 4 * sizeof(unsigned)));  // barrier, fresh-window scans (panel.cu)
     {
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));

@@ -39,7 +39,8 @@ struct PlsState {
     int64_t panel_r;   // r at the start of the current panel
     int64_t panel_kb;  // pivots found so far in the current panel
     int32_t nmoved;    // positions whose pmap entry changed during the panel
-    int32_t pad0;
+    int32_t hint;      // a leaf needed the general search (this run): fresh windows ask the
+                       // workers whether any row past them is nonzero (panel.cu, past_zero)
     int64_t pmap_hi;   // pmap[x] == x for every position x >= pmap_hi (this panel)
     uint64_t leaf_mask;                 // pivot columns within the leaf word
     uint64_t ustrict[64];               // leaf pivot words, bits <= pivot cleared

@@ -557,7 +557,7 @@ __device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSm
 // and the carry tables, and returns kb; -1 when the window cannot decide a column.
 __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int lw, PlsState* st, int64_t* P,
                               int64_t* Qp, int64_t* pmap, int64_t qcol_off, PipeSmem& S, PipeStatic& Z, int pb,
-                              PlsState::Packet* pk, int nleaves, bool carried) {
+                              PlsState::Packet* pk, int nleaves, bool carried, bool past_zero) {
     __shared__ FastSmem F;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = A.m, stride = A.stride;
@@ -577,7 +577,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
 #ifdef F2_ONE_WARP_PIVOTS
     if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
 #else
-    if (warp < 3) two_warp_pivots(F, lw, base + kPW < m, false);
+    if (warp < 3) two_warp_pivots(F, lw, base + kPW < m && !past_zero, false);
 #endif
     // meanwhile the other warps finish the carried window: the previous leaf's update of
     // the words right of this leaf's (pipe_build_window did this leaf's word)
@@ -794,6 +794,15 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
     if (threadIdx.x == 0) atomicMin(&st->tl[0][(pw0 / 16) & 127], gtimer());
 #endif
     int kbprev = 0, pkc = 0;  // CTA 0's carry state (uniform across its threads)
+    // Rank-deficient / sparse panels: after a leaf needed the general search (st->hint), each
+    // fresh window has the idle workers check whether any row past it is nonzero in the
+    // panel's remaining words (bar[1]: scans done, bar[2]: last nonzero scan + 1).  All zero:
+    // those rows can never hold a candidate nor be touched by a pivot for the rest of the
+    // panel, so the window decides every column (past_zero, sticky) -- a zero column no
+    // longer sends the leaf to the general search.
+    bool past_zero = false;
+    unsigned nscan = 0;
+    __shared__ int s_pz;
     int64_t state = S_FRESH, leaf = 0, wpk = -1, wleaf = 0;
     for (int it = 0;; ++it) {
         if (it > 0) {
@@ -811,10 +820,27 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
         __syncthreads();
 #endif
         F2_STAMP(st, 0);
+        const bool scan = state == S_FRESH && __ldcg(&st->hint) != 0;  // (the same in every CTA)
+        if (scan) ++nscan;
         if (blockIdx.x == 0) {
             int64_t nstate = S_DONE, nleaf = leaf, nwpk = -1, nwleaf = 0;
             const int j = static_cast<int>(leaf);
             const int pb = j & 1;
+            if (scan) {
+                if (!past_zero) {
+                    if (threadIdx.x == 0) {
+                        const unsigned want = nscan * (gridDim.x - 1);
+                        unsigned v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar + 1) : "memory");
+                        } while (v < want);
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar + 2) : "memory");
+                        s_pz = v < nscan;
+                    }
+                    __syncthreads();
+                    past_zero = s_pz != 0;
+                }
+            }
             if (state == S_FRESH || state == S_CARRY || state == S_FINAL) {
                 F2_CLK(const long long cb = clock64();)
                 pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
@@ -828,7 +854,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                     const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
                     PlsState::Packet* pk = &st->pk[pkc & 1];
                     const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves,
-                                                  state == S_CARRY);
+                                                  state == S_CARRY, past_zero);
                     F2_STAMP(st, 2);
                     if (kb >= 0) {
                         kbprev = kb;
@@ -851,6 +877,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 }
             } else if (state == S_GENERAL) {
                 const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
+                if (threadIdx.x == 0) st->hint = 1;
                 // (the window is written back: its SMEM holds the search's compact row list)
                 leaf_pivot_body(A, pw0 + j, lw, j == 0, j, nleaves * 64, st, P, Qp, pmap, qcol_off,
                                 reinterpret_cast<uint8_t*>(dsm), static_cast<int>(kPipeSmem / 17) & ~63);
@@ -877,6 +904,16 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 c[2] = nwpk;
                 c[3] = nwleaf;
             }
+        } else if (scan) {  // a fresh window: is any row past it nonzero in the remaining words?
+            const int j = static_cast<int>(leaf);
+            const int64_t lo = ldi(&st->r) + kPW;
+            const int nwr = nwp - j, k = threadIdx.x & 15;
+            uint64_t acc = 0;
+            for (int64_t pos = lo + (blockIdx.x - 1) * (kPT / 16) + (threadIdx.x >> 4); pos < A.m;
+                 pos += static_cast<int64_t>(gridDim.x - 1) * (kPT / 16))
+                if (k < nwr) acc |= ldw(A.w + ldi(pmap + pos) * A.stride + pw0 + j + k);
+            if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicMax(bar + 2, nscan);
+            if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar + 1) : "memory");
         } else if (wpk >= 0) {
             const PlsState::Packet* pk = &st->pk[wpk];
             if (blockIdx.x == 1 && s_ctl[0] != S_IDLE) pipe_worker_lmap(st, pk, X);
@@ -908,7 +945,7 @@ void launch_panel_pipe(cudaStream_t s, const Mat& A, int64_t pw0, int width, int
     // update) rely on every CTA becoming resident eventually: the only other work on
     // the device is the Schur kernel, whose CTAs never wait, and the grid (<= SMs)
     // fits one CTA per SM.
-    cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
+    cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nsm));
     cfg.blockDim = dim3(kPT);
