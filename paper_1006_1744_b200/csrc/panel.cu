@@ -47,9 +47,28 @@ constexpr int kTab = 256 * kW;             // one 8-bit group table (CTA 0's fal
 constexpr size_t kSmem = sizeof(uint64_t) * (kTab + 64 * kW + 8 * 256);
 static_assert(kSmem >= sizeof(uint64_t) * (128 + 256) * 15, "CTA 0's fast path scratch");
 
+// CTA 0 waits for the other CTAs' arrivals at the barrier after `target` (the next one).
+__device__ __forceinline__ void await_workers(const unsigned* bar, unsigned target) {
+    unsigned v;
+    do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target + gridDim.x - 1);
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
     __syncthreads();
     target += gridDim.x;
+    if (blockIdx.x == 0) {
+        // CTA 0 (the critical path, nearly always the last to arrive) waits for the others'
+        // arrivals only, then arrives without waiting for its own to land: no CTA's next
+        // round can begin before it, so target - 1 arrivals are this round's
+        if (threadIdx.x == 0) {
+            await_workers(bar, target - gridDim.x);
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+        }
+        __syncthreads();
+        return;
+    }
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
         unsigned v;
