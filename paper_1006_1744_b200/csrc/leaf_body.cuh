@@ -700,42 +700,49 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
         // ---- block-wide scan of positions [ob, m) for the leftmost column in [col, lim)
         const int64_t ob = base + s_ob;
         if (s_cstate == 1) {  // the leaf's nonzero rows past the first scan's window, in SMEM
+            // keys as 32 bits (column << 24 | position - ob: the list exists only while the span
+            // fits 24 bits), one hardware min-reduction per warp and one across the warps
             const int c0 = s_col, tt = s_t, lim = s_lim, cn = s_cn;
-            if (tid == 0) s_best = KEY_NONE;
-            __syncthreads();
-            for (int i0 = 0; i0 < cn; i0 += blockDim.x) {
-                const int i = i0 + tid;
-                unsigned long long key = KEY_NONE;
-                uint64_t v = 0;
-                if (i < cn) {
-                    const int64_t pp = base + c_pos[i];
-                    if (pp >= ob) {
-                        v = c_w[i];
-                        for (int l = c_tt[i]; l < tt; ++l)
-                            if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
-                        c_w[i] = v;
-                        c_tt[i] = static_cast<uint8_t>(tt);
-                        uint64_t z = v & (~0ull << c0);
-                        if (lim < 64) z &= (1ull << lim) - 1;
-                        if (z)
-                            key = (static_cast<unsigned long long>(__ffsll(static_cast<long long>(z)) - 1) << 48) |
-                                  static_cast<unsigned long long>(pp - ob);
+            unsigned key = ~0u;  // this thread's best entry
+            uint64_t bv = 0;
+            int bi = -1;
+            for (int i = tid; i < cn; i += blockDim.x) {
+                const int64_t pp = base + c_pos[i];
+                if (pp < ob) continue;
+                uint64_t v = c_w[i];
+                const int ti = c_tt[i];
+                if (ti < tt) {
+                    for (int l = ti; l < tt; ++l)
+                        if ((v >> s_q[l]) & 1ull) v ^= s_u[l];
+                    c_w[i] = v;
+                    c_tt[i] = static_cast<uint8_t>(tt);
+                }
+                uint64_t z = v & (~0ull << c0);
+                if (lim < 64) z &= (1ull << lim) - 1;
+                if (z) {
+                    const unsigned kk = (static_cast<unsigned>(__ffsll(static_cast<long long>(z)) - 1) << 24) |
+                                        static_cast<unsigned>(pp - ob);
+                    if (kk < key) {
+                        key = kk;
+                        bv = v;
+                        bi = i;
                     }
                 }
-                unsigned long long k = warp_min64(key);
-                if (lane == 0) s_red[warp] = k;
-                __syncthreads();
-                if (warp == 0) {
-                    unsigned long long kk = lane < nwarps ? s_red[lane] : KEY_NONE;
-                    kk = warp_min64(kk);
-                    if (lane == 0 && kk < s_best) s_best = kk;
-                }
-                __syncthreads();
-                if (key != KEY_NONE && key == s_best) {
-                    s_bword = v;
-                    s_bsrc = base + c_src[i];
-                    s_bidx = i;
-                }
+            }
+            const unsigned k = __reduce_min_sync(FULL, key);
+            if (lane == 0) s_red[warp] = k;
+            __syncthreads();
+            if (warp == 0) {
+                const unsigned kk = __reduce_min_sync(FULL, lane < nwarps ? static_cast<unsigned>(s_red[lane]) : ~0u);
+                if (lane == 0)
+                    s_best = kk == ~0u ? KEY_NONE
+                                       : (static_cast<unsigned long long>(kk >> 24) << 48) | (kk & 0xFFFFFFu);
+            }
+            __syncthreads();
+            if (key != ~0u && key == k && key == static_cast<unsigned>(((s_best >> 48) << 24) | (s_best & 0xFFFFFFu))) {
+                s_bword = bv;
+                s_bsrc = base + c_src[bi];
+                s_bidx = bi;
             }
             __syncthreads();
         } else {
@@ -792,7 +799,7 @@ static __device__ __noinline__ void leaf_pivot_body(const Mat& A, int64_t wl, in
                 }
             }
             __syncthreads();
-            if (build && tid == 0) s_cstate = s_cn <= cap ? 1 : 2;
+            if (build && tid == 0) s_cstate = s_cn <= cap && m - ob < (1 << 24) ? 1 : 2;
             __syncthreads();
         }
 
