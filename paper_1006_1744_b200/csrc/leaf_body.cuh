@@ -19,13 +19,13 @@ __device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
+// 64-bit minimum as two hardware 32-bit reductions: the high words, then the low words of
+// the lanes holding the smallest high word
 __device__ __forceinline__ unsigned long long warp_min64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long u = __shfl_xor_sync(FULL, v, o);
-        v = u < v ? u : v;
-    }
-    return v;
+    const unsigned hi = static_cast<unsigned>(v >> 32);
+    const unsigned mh = __reduce_min_sync(FULL, hi);
+    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? static_cast<unsigned>(v) : ~0u);
+    return (static_cast<unsigned long long>(mh) << 32) | ml;
 }
 
 // mask of bits strictly above bit c (c in 0..63)
