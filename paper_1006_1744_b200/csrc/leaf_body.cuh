@@ -73,6 +73,20 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&v)[S], int s) {
 }
 
 template <int S>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&v)[S], int s) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int i = 1; i < S; ++i)
+        if (s == i) r = v[i];
+    return r;
+}
+
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+
+template <int S>
 __device__ __forceinline__ int32_t pick(const int32_t (&v)[S], int s) {
     int32_t r = v[0];
 #pragma unroll
@@ -85,28 +99,14 @@ __device__ __forceinline__ int32_t pick(const int32_t (&v)[S], int s) {
 
 
 // ---- dense fast path ---------------------------------------------------------------
-// The first 128 positions of the current order ("the window") are transposed into
-// column form: column c of the leaf is a 128-bit mask over the window's slots.
-// Warp 0 runs the Gaussian pivot rule on the masks, lane l owning columns l and l+32:
-// per column, candidates = its bits at slots >= t; the lowest is the pivot (the first
-// row in the current order, exactly gauss.cpp:33-40, because the window is a prefix
-// of that order); its slot swaps with slot t (a two-bit swap in every mask, :44);
-// rows below with a 1 receive the pivot row from the next column on (one masked XOR
-// per column, :47-49).  A column without candidates is decided only when no rows lie
-// past the window; otherwise the leaf falls back to the general search below
-// (rank-deficient / sparse inputs).
+// The first 128 positions of the current order ("the window", a prefix of that order) decide
+// a leaf whenever every column finds its pivot among them: row_pivots below applies the
+// Gaussian pivot rule (gauss.cpp:33-49) to the window's leaf words in registers.  A column
+// without candidates is decided only when no rows lie past the window; otherwise the leaf
+// falls back to the general search further down (rank-deficient / sparse inputs).
 //
-// The panel kernel (panel.cu, pipe_fast_leaf) drives these warps on its carried
-// 128-row window and then solves the pivot rows over the rest of the panel.
-struct U128 {
-    uint64_t lo, hi;
-};
-
-// (nlo, nhi) = -(lo, hi) as one 128-bit two's complement (one carry chain)
-__device__ __forceinline__ void neg128(uint64_t lo, uint64_t hi, uint64_t& nlo, uint64_t& nhi) {
-    asm("sub.cc.u64 %0, 0, %2;\n\tsubc.u64 %1, 0, %3;\n" : "=l"(nlo), "=l"(nhi) : "l"(lo), "l"(hi));
-}
-
+// The panel kernel (panel.cu, pipe_fast_leaf) drives this on its carried 128-row window and
+// then solves the pivot rows over the rest of the panel.
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
     // lane i holds bits (i, 0..31) -> lane j holds bits (0..31, j)
     uint32_t m = 0x0000FFFFu;
@@ -122,153 +122,184 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
 }
 
 struct FastSmem {
-    uint32_t colw[64 * 4];       // leaf columns: 4 x 32 slots each
+    uint4 stp[64];               // pivot steps as the search stores them: word lo, hi, source slot | column << 8 |
+                                 // position << 16, -
     uint64_t linv[64];           // rows of L11^{-1} over pivot indices
-    uint64_t rraw[64];           // the same rows in raw leaf-column coordinates
     int posc[64];                // leaf column -> pivot index, -1
-    int64_t phys[128];           // pre-leaf physical row of each slot
-    int step_p[64], step_c[64];  // pivot steps
+    int step_p[64], step_c[64];  // pivot steps: position in the order at the step, column
     int src[128];                // slot s now holds the pre-leaf content of slot src[s]
     uint64_t uf[64];             // pivot rows' final leaf words
     int wcount[4];
     int final_kb;                // -1: fell back
-    // two-warp search: published steps (the selecting warp writes, the other replays)
-    ulonglong2 step_m[64];       // step t's candidate mask: the pivot column's bits at slots >= t
-    uint32_t ufl[64], ufh[64];   // pivot rows' leaf words, columns 0-31 / 32-63
+    int used4;                   // the 96-slot pass could not decide, all 128 slots searched
     uint64_t fbas[64];           // finalize basis
-    uint64_t cfin[64];           // post-search column masks, slots 0..63 (bit l = row l's bit in column c)
+    uint64_t cfin[64];           // pivot rows' leaf words transposed (bit l = row l's bit in column c)
     uint32_t ainv[32], brows[32];
-    volatile int q_n;            // published progress: (columns processed << 8) | steps
 #ifdef F2_LEAF_CLOCKS
-    long long clk[2][2];         // selecting loop start / end per phase
+    long long clk[2];            // search loop start / end
 #endif
 };
 
-// Warp 0: the column-form pivot rule on F.colw (leaf columns as 128-slot masks).
-// Fills step_p/step_c, final_kb (-1: a column needs rows past the window), the pivot
-// rows' final leaf words uf and, with want_linv, the rows of L11^{-1}.
-__device__ __forceinline__ void warp0_pivots(FastSmem& F, int lw, bool more, bool want_linv, PlsState* st) {
+// Warp 0: the same pivot rule in ROW form.  Lane l keeps the leaf words of window slots
+// l, l+32, l+64, l+96 in registers (two 32-bit halves each) together with each row's
+// current position in the order.  Per column: every row with a 1 there offers the key
+// (position, row id); one hardware min-reduction picks the first row in the current order
+// (gauss.cpp:33-40), two shuffles fetch its word, the other offering rows add it from the
+// next column on (gauss.cpp:47-49), the row that sat at position t takes the pivot's old
+// position (the transposition, :44) and the pivot row retires (its word is final: it
+// holds the L bits left of each pivot column and U from the column on).  The dependent
+// chain per pivot is one reduction and one shuffle round, one warp, no cross-warp protocol
+// (the column-form search it replaces -- 128-bit slot masks per column, a lowest-bit carry
+// chain, a second warp replaying every published step and a third tracking the slot
+// permutation -- took 14.4K cycles per 64-column leaf; this one 10.7K).
+// wsrc = the leaf word of slot 0, slots 16 words apart.
+// Fills step_c/step_p, posc, uf, src (every slot) and final_kb (-1: a column without candidates
+// in the window while rows lie past it).  NR = 3 searches the first 96 slots only (a quarter
+// less work per column; the caller repeats the search on all 128 when that cannot decide).
+template <int NR>
+__device__ __forceinline__ int row_pivots(FastSmem& F, const uint64_t* wsrc, int lw, bool more) {
     const int lane = threadIdx.x & 31;
-        U128 C0, C1;
-        C0.lo = F.colw[lane * 4] | (static_cast<uint64_t>(F.colw[lane * 4 + 1]) << 32);
-        C0.hi = F.colw[lane * 4 + 2] | (static_cast<uint64_t>(F.colw[lane * 4 + 3]) << 32);
-        C1.lo = F.colw[(lane + 32) * 4] | (static_cast<uint64_t>(F.colw[(lane + 32) * 4 + 1]) << 32);
-        C1.hi = F.colw[(lane + 32) * 4 + 2] | (static_cast<uint64_t>(F.colw[(lane + 32) * 4 + 3]) << 32);
-                int t = 0;
-        bool ok = true;
-        for (int c = 0; c < lw; ++c) {
-            const uint64_t srclo = c < 32 ? C0.lo : C1.lo, srchi = c < 32 ? C0.hi : C1.hi;
-            const uint64_t mlo = __shfl_sync(FULL, srclo, c & 31);
-            const uint64_t mhi = __shfl_sync(FULL, srchi, c & 31);
-            const uint64_t clo = mlo & (~0ull << t);  // t <= 63 here
-            if ((clo | mhi) == 0) {
-                if (more) {
-                    ok = false;
-                    break;
-                }
-                continue;  // zero column among all remaining rows: no pivot (gauss.cpp:36-41)
-            }
-            const int p = clo ? __ffsll(static_cast<long long>(clo)) - 1 : 63 + __ffsll(static_cast<long long>(mhi));
-            const uint64_t tb = 1ull << t;
-            const uint64_t plo = p < 64 ? (1ull << p) : 0ull, phi = p < 64 ? 0ull : (1ull << (p - 64));
-            // swap slots t and p in every mask (a no-op when p == t)
-            {
-                const uint64_t d0 = (((C0.lo & tb) != 0) != (((C0.lo & plo) | (C0.hi & phi)) != 0)) ? ~0ull : 0ull;
-                C0.lo ^= d0 & (tb | plo);
-                C0.hi ^= d0 & phi;
-                const uint64_t d1 = (((C1.lo & tb) != 0) != (((C1.lo & plo) | (C1.hi & phi)) != 0)) ? ~0ull : 0ull;
-                C1.lo ^= d1 & (tb | plo);
-                C1.hi ^= d1 & phi;
-            }
-            // column c after the swap: bit t set, bit p cleared; rows below t with a 1
-            const uint64_t elo = (mlo & ~plo) & (t == 63 ? 0ull : (~0ull << (t + 1)));
-            const uint64_t ehi = mhi & ~phi;
-            const bool a0 = lane > c && (C0.lo & tb);
-            const bool a1 = lane + 32 > c && (C1.lo & tb);
-            C0.lo ^= a0 ? elo : 0ull;
-            C0.hi ^= a0 ? ehi : 0ull;
-            C1.lo ^= a1 ? elo : 0ull;
-            C1.hi ^= a1 ? ehi : 0ull;
-            F.step_p[t] = p;  // same value from every lane: one store
-            F.step_c[t] = c;
-            ++t;
+    uint32_t lo[NR], hi[NR], kp[NR];  // kp: position << 7 | row id (j << 5 | lane); ~0 once retired
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        const uint64_t w = wsrc[(32 * j + lane) * 16];
+        lo[j] = static_cast<uint32_t>(w);
+        hi[j] = static_cast<uint32_t>(w >> 32);
+        kp[j] = (static_cast<uint32_t>(32 * j + lane) << 7) | static_cast<uint32_t>(32 * j + lane);
+    }
+    int t = 0;
+    const uint32_t stp_a = static_cast<uint32_t>(__cvta_generic_to_shared(&F.stp[0]));
+    // One column: cb = its bit in the half holding it, am = the bits above it in that half.
+    // Branch-free: a column without candidates is a masked no-op step (after a column the
+    // window cannot decide the later steps still run, and the leaf is discarded).
+    auto column = [&](auto hi_half, int c, uint32_t cb, uint32_t am) {
+        constexpr bool HI = decltype(hi_half)::value;
+        uint32_t key[NR];
+#pragma unroll
+        for (int j = 0; j < NR; ++j) key[j] = ((HI ? hi[j] : lo[j]) & cb) ? kp[j] : ~0u;
+        // this lane's first candidate and its word (selected beside the reduction)
+        const bool s01 = key[1] < key[0];
+        const uint32_t k01 = s01 ? key[1] : key[0];
+        uint32_t k23 = key[2], l23 = lo[2], h23 = hi[2];
+        if constexpr (NR == 4) {
+            const bool s23 = key[3] < key[2];
+            k23 = s23 ? key[3] : key[2];
+            l23 = s23 ? lo[3] : lo[2];
+            h23 = s23 ? hi[3] : hi[2];
         }
-        F2_STAMP(st, 17);
-        if (lane == 0) F.final_kb = ok ? t : -1;
-        if (ok) {
-            // pivot rows' final leaf words: slots 0..63 of the 64 columns back to row form
-            const uint32_t r00 = warp_transpose32(static_cast<uint32_t>(C0.lo), lane);        // slots 0-31, cols 0-31
-            const uint32_t r01 = warp_transpose32(static_cast<uint32_t>(C1.lo), lane);        // slots 0-31, cols 32-63
-            const uint32_t r10 = warp_transpose32(static_cast<uint32_t>(C0.lo >> 32), lane);  // slots 32-63
-            const uint32_t r11 = warp_transpose32(static_cast<uint32_t>(C1.lo >> 32), lane);
-            const uint64_t u0 = r00 | (static_cast<uint64_t>(r01) << 32);
-            const uint64_t u1 = r10 | (static_cast<uint64_t>(r11) << 32);
-            F.uf[lane] = u0;
-            F.uf[lane + 32] = u1;
-            if (want_linv) {
-                // L11^{-1}: row l = e_l + sum over t < l with L bit of l at q_t of row t
-                __syncwarp();
-                uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
-                for (int tt = 0; tt < t; ++tt) {
-                    const int qt = F.step_c[tt];
-                    const uint64_t Rt = __shfl_sync(FULL, tt < 32 ? R0 : R1, tt & 31);
-                    if (lane > tt && ((u0 >> qt) & 1ull)) R0 ^= Rt;
-                    if (lane + 32 > tt && ((u1 >> qt) & 1ull)) R1 ^= Rt;
-                }
-                F.linv[lane] = R0;
-                F.linv[lane + 32] = R1;
-            }
+        const bool sb = k23 < k01;
+        const uint32_t km = __reduce_min_sync(FULL, sb ? k23 : k01);
+        const uint32_t blo = sb ? l23 : (s01 ? lo[1] : lo[0]);
+        const uint32_t bhi = sb ? h23 : (s01 ? hi[1] : hi[0]);
+        const uint32_t plo = __shfl_sync(FULL, blo, km & 31), phi = __shfl_sync(FULL, bhi, km & 31);
+        const bool some = km != ~0u;
+        const uint32_t p7 = km & ~127u;
+        const uint32_t kmx = some ? km : 0xfffffffeu;  // no pivot: nothing equals it
+        const uint32_t tk = some ? static_cast<uint32_t>(t) << 7 : 0xfffffffeu;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const bool cand = key[j] != ~0u, piv = key[j] == kmx;
+            const uint32_t amj = piv ? ~0u : am;  // the pivot row adds itself: cleared, it never offers again
+            if (!HI && cand) lo[j] ^= plo & amj;
+            if (cand) hi[j] ^= HI ? phi & amj : phi;
+            if ((kp[j] & ~127u) == tk) kp[j] = (kp[j] & 127u) | p7;  // slot t's row moves to p
+            if (piv) kp[j] = ~0u;
         }
+        // every lane stores the same 16 bytes (predicated on a pivot, shared-window address
+        // computed once outside the loop)
+        asm volatile(
+            "{\n\t.reg .pred q;\n\t"
+            "setp.ne.u32 q, %0, 0xffffffff;\n\t"
+            "@q st.shared.v4.u32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"(km),
+            "r"(stp_a + 16u * t), "r"(plo), "r"(phi),
+            "r"((km & 127u) | (static_cast<uint32_t>(c) << 8) | (p7 << 9)), "r"(0u)
+            : "memory");
+        t += some ? 1 : 0;
+    };
+    int ncol = 0;
+    F2_CLK(if (lane == 0) F.clk[0] = clock64();)
+    // blocks of 8 columns without a branch inside; between blocks, stop once a column could
+    // not be decided (the pass is discarded anyway)
+    {
+        const int c1 = lw < 32 ? lw : 32;
+        uint32_t cb = 1u, am = ~1u;
+        int c = 0;
+        for (; c + 8 <= c1 && !(more && t < c); c += 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i, cb <<= 1, am <<= 1) column(BoolC<false>{}, c + i, cb, am);
+        }
+        if (c + 8 > c1)
+            for (; c < c1; ++c, cb <<= 1, am <<= 1) column(BoolC<false>{}, c, cb, am);
+        ncol = c1;
     }
-
-
-// One warp: rows of L11^{-1} over pivot indices from the pivot rows' leaf words:
-// row l = e_l + sum over t < l with the L bit of l at column q_t of row t.
-__device__ __forceinline__ void warp_linv(FastSmem& F, int kb) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t u0 = F.uf[lane], u1 = F.uf[lane + 32];
-    // the L bits of rows lane and lane+32 gathered into pivot-index order first, so the
-    // 64-step chain is one shuffle and two masked XORs per step
-    uint64_t c0 = 0, c1 = 0;
-    for (int tt = 0; tt < kb; ++tt) {
-        const int qt = F.step_c[tt];
-        c0 |= ((u0 >> qt) & 1ull) << tt;
-        c1 |= ((u1 >> qt) & 1ull) << tt;
+    {
+        uint32_t cb = 1u, am = ~1u;
+        int c = 32;
+        for (; c + 8 <= lw && !(more && t < c); c += 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i, cb <<= 1, am <<= 1) column(BoolC<true>{}, c + i, cb, am);
+        }
+        if (c + 8 > lw)
+            for (; c < lw; ++c, cb <<= 1, am <<= 1) column(BoolC<true>{}, c, cb, am);
+        if (lw > 32) ncol = lw;
     }
-    c0 &= lane == 0 ? 0ull : (~0ull >> (64 - lane));  // strictly below the row's own index
-    uint64_t R0 = 1ull << lane, R1 = 1ull << (lane + 32);
-#pragma unroll 4
-    for (int tt = 0; tt < 32; ++tt) {
-        const uint64_t Rt = __shfl_sync(FULL, R0, tt);
-        R0 ^= ((c0 >> tt) & 1ull) ? Rt : 0ull;
-        R1 ^= ((c1 >> tt) & 1ull) ? Rt : 0ull;
+    F2_CLK(if (lane == 0) F.clk[1] = clock64();)
+    const bool ok = !(more && t < ncol);
+    F.posc[lane] = -1;
+    F.posc[lane + 32] = -1;
+    __syncwarp();
+    for (int l = lane; l < t; l += 32) {
+        const uint4 e = F.stp[l];
+        const uint32_t pk = e.z;
+        F.uf[l] = e.x | (static_cast<uint64_t>(e.y) << 32);
+        F.src[l] = static_cast<int>(pk & 127u);
+        F.step_c[l] = static_cast<int>((pk >> 8) & 63u);
+        F.step_p[l] = static_cast<int>(pk >> 16);
+        F.posc[(pk >> 8) & 63u] = l;
     }
-    c1 &= lane == 0 ? ~0ull >> 32 : (~0ull >> (32 - lane));  // t < lane + 32
-#pragma unroll 4
-    for (int tt = 32; tt < 64; ++tt) {
-        const uint64_t Rt = __shfl_sync(FULL, R1, tt - 32);
-        R1 ^= ((c1 >> tt) & 1ull) ? Rt : 0ull;
+    if (ok) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+            if (kp[j] != ~0u) F.src[kp[j] >> 7] = static_cast<int>(kp[j] & 127u);  // rows left: positions t..
+        if (NR == 3) F.src[96 + lane] = 96 + lane;  // (not searched: they stay)
     }
-    F.linv[lane] = R0;
-    F.linv[lane + 32] = R1;
+    if (lane == 0) F.final_kb = ok ? t : -1;
+    return ok ? t : -1;  // (uniform)
 }
 
-// Warps 0 and 1: rows of L11^{-1} (pivot-index coordinates) from the post-search
-// column masks.  Column q_t's mask holds, in bit l, row l's bit at that column, so
-// one transpose gives every row's L bits in pivot order; then L11 = [A 0; B C] in
-// 32x32 blocks: A^{-1} (warp 0) and C^{-1} (warp 1) by 32-step shuffle chains in
-// parallel, and the off-diagonal block C^{-1} B A^{-1} by two independent passes.
-__device__ __forceinline__ void pair_linv(FastSmem& F, int kb) {
+// Warps 0 and 1 after row_pivots: rows of L11^{-1} in pivot-index coordinates.  Row l's L
+// bits in pivot order are bits q_0, q_1, ... of its final word: with 64 pivots in a 64-column
+// leaf (q_t = t) the word itself; otherwise the words are transposed into column form
+// (F.cfin: bit l of column c = row l's bit there) and the pivot columns transposed back.
+// Then L11 = [A 0; B C] in 32x32 blocks: A^{-1} (warp 0) and C^{-1} (warp 1) by 32-step
+// shuffle chains in parallel, and the off-diagonal block C^{-1} B A^{-1} by two independent
+// passes.
+__device__ __forceinline__ void pair_linv_rows(FastSmem& F, int kb) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int tt = 32 * w + lane;
-    const uint64_t vt = tt < kb ? F.cfin[F.step_c[tt]] : 0ull;  // bit l: L[l][tt] (for l > tt)
     uint32_t rows, rowsb = 0;
-    if (w == 0) {
-        rows = warp_transpose32(static_cast<uint32_t>(vt), lane) & ((1u << lane) - 1u);  // A rows
-        rowsb = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane);                 // B rows
+    if (kb == 64) {
+        const uint64_t u1 = F.uf[lane + 32];
+        if (w == 0) {
+            rows = static_cast<uint32_t>(F.uf[lane]) & ((1u << lane) - 1u);  // A rows
+            rowsb = static_cast<uint32_t>(u1);                               // B rows
+        } else {
+            rows = static_cast<uint32_t>(u1 >> 32) & ((1u << lane) - 1u);    // C rows
+        }
     } else {
-        (void)warp_transpose32(static_cast<uint32_t>(vt), lane);
-        rows = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane) & ((1u << lane) - 1u);  // C rows
+        const uint32_t r0 = warp_transpose32(static_cast<uint32_t>((lane < kb ? F.uf[lane] : 0ull) >> (32 * w)), lane);
+        const uint32_t r1 =
+            warp_transpose32(static_cast<uint32_t>((lane + 32 < kb ? F.uf[lane + 32] : 0ull) >> (32 * w)), lane);
+        F.cfin[32 * w + lane] = r0 | (static_cast<uint64_t>(r1) << 32);
+        asm volatile("bar.sync 2, 64;\n" ::: "memory");
+        const int tt = 32 * w + lane;
+        const uint64_t vt = tt < kb ? F.cfin[F.step_c[tt]] : 0ull;  // bit l: L[l][tt] (for l > tt)
+        if (w == 0) {
+            rows = warp_transpose32(static_cast<uint32_t>(vt), lane) & ((1u << lane) - 1u);
+            rowsb = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane);
+        } else {
+            (void)warp_transpose32(static_cast<uint32_t>(vt), lane);
+            rows = warp_transpose32(static_cast<uint32_t>(vt >> 32), lane) & ((1u << lane) - 1u);
+        }
     }
     uint32_t R = 1u << lane;
 #pragma unroll 8
@@ -295,177 +326,6 @@ __device__ __forceinline__ void pair_linv(FastSmem& F, int kb) {
             z ^= ((R >> sidx) & 1u) ? ys : 0u;
         }
         F.linv[32 + lane] = static_cast<uint64_t>(z) | (static_cast<uint64_t>(R) << 32);
-    }
-}
-
-// Warps 0 and 1: the same pivot rule with the columns split, lane l of warp w owning
-// column 32w + l.  Warp 0 selects the pivots of columns 0-31 while warp 1 replays each
-// published step (slot swap + masked XOR) on its columns; then warp 1 selects columns
-// 32-63 while warp 0 replays the swaps.  Each selecting step touches one column mask
-// per lane instead of two.  Same outputs as warp0_pivots.
-__device__ __forceinline__ void two_warp_pivots(FastSmem& F, int lw, bool more, bool want_linv) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int col = 32 * w + lane;
-    U128 C;
-    if (w < 2) {
-        C.lo = F.colw[col * 4] | (static_cast<uint64_t>(F.colw[col * 4 + 1]) << 32);
-        C.hi = F.colw[col * 4 + 2] | (static_cast<uint64_t>(F.colw[col * 4 + 3]) << 32);
-    } else {
-        // warp 2 tracks the slot permutation: lane b < 7 holds the mask of slots whose
-        // pre-leaf index has bit b set; it replays every swap, so at the end bit b of
-        // slot s's source index sits in bit s of mask b
-        const uint64_t pat[6] = {0xAAAAAAAAAAAAAAAAull, 0xCCCCCCCCCCCCCCCCull, 0xF0F0F0F0F0F0F0F0ull,
-                                 0xFF00FF00FF00FF00ull, 0xFFFF0000FFFF0000ull, 0xFFFFFFFF00000000ull};
-        C.lo = lane < 6 ? pat[lane] : 0ull;
-        C.hi = lane < 6 ? pat[lane] : (lane == 6 ? ~0ull : 0ull);
-    }
-    if (threadIdx.x == 0) {
-        F.q_n = 0;
-    }
-    asm volatile("bar.sync 1, 96;\n" ::: "memory");
-    // step t from its candidate mask m: the pivot is m's lowest bit, the rows to
-    // eliminate are m's other bits (all below slot t after the swap)
-    auto apply = [&](int t, ulonglong2 m, bool xr) {
-        const uint64_t tb = 1ull << t;
-        const uint64_t plo = m.x & (0ull - m.x), phi = m.x ? 0ull : (m.y & (0ull - m.y));
-        const uint64_t elo = m.x ^ plo, ehi = m.y ^ phi;
-        const uint64_t d = (((C.lo & tb) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
-        C.lo ^= d & (tb | plo);
-        C.hi ^= d & phi;
-        const bool a = xr && (C.lo & tb);
-        C.lo ^= a ? elo : 0ull;
-        C.hi ^= a ? ehi : 0ull;
-    };
-    // The selecting warp releases (columns processed << 8) | steps after every column; a
-    // replaying warp applies the steps it sees and knows the phase is over when the column
-    // count reaches the phase's end (and whether it was decidable from the step count).
-    auto progress = [&]() {
-        unsigned v;
-        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))) : "memory");
-        return v;
-    };
-    int t = 0;
-    bool ok = true;
-    if (w == 2) {
-        for (int phase = 0; phase < 2 && ok; ++phase) {
-            if (32 * phase >= lw) break;
-            const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32, t0 = t;
-            while (true) {
-                const unsigned v = progress();
-                for (; t < static_cast<int>(v & 255u); ++t) apply(t, F.step_m[t], false);
-                if (static_cast<int>(v >> 8) >= c1) {
-                    ok = ok && !(more && t - t0 < c1 - c0);
-                    break;
-                }
-            }
-        }
-        // Written whatever this warp's own `ok` says: the tracker may read the progress word
-        // only after the other warp has started publishing phase 1, apply some of those steps
-        // before leaving phase 0, and then undercount phase 1 -- its `ok` is not authoritative
-        // (warp 0's final_kb is), while its masks, having applied every step in order, are.
-        // (Gating this store on the tracker's `ok` once left stale slot sources behind, so a
-        // leaf's pivot rows went to the wrong physical rows in rare runs.)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint64_t m = k < 2 ? C.lo : C.hi;
-            const uint32_t piece = static_cast<uint32_t>(m >> (32 * (k & 1)));
-            F.src[32 * k + lane] = static_cast<int>(warp_transpose32(piece, lane) & 127u);
-        }
-    } else
-    for (int phase = 0; phase < 2; ++phase) {
-        const int c0 = 32 * phase, c1 = lw < c0 + 32 ? lw : c0 + 32;
-        if (w == phase) {
-            // select the pivots of columns c0 .. c1-1.  Branch-free: a column without a
-            // pivot is a masked no-op step, so the chain from one shuffle to the next has
-            // no convergence points (after a column the window cannot decide the later
-            // steps still run, and the leaf is discarded)
-            const int t0 = t;
-            F2_CLK(if (lane == 0) F.clk[phase][0] = clock64();)
-            uint64_t tb = 1ull << t, tm = ~0ull << t;  // slot t, slots >= t
-#pragma unroll 2
-            for (int c = c0; c < c1; ++c) {
-                const uint64_t mlo = __shfl_sync(FULL, C.lo, c & 31);
-                const uint64_t mhi = __shfl_sync(FULL, C.hi, c & 31);
-                // candidates: slots >= t; the pivot is the lowest (as a bit: x & -x over
-                // the 128-bit mask), the rows to eliminate the others.  Every quantity is
-                // masked, none branched on, and the pivot's index is left to the readers of
-                // the candidate mask.
-                const uint64_t clo = mlo & tm;
-                uint64_t plo, phi;
-                neg128(clo, mhi, plo, phi);
-                plo &= clo;
-                phi &= mhi;
-                const bool zero = (plo | phi) == 0;
-                const uint64_t elo = clo ^ plo, ehi = mhi ^ phi;
-                const uint64_t tz = zero ? 0ull : tb;
-                {  // apply step t to this lane's column (a no-op when zero)
-                    const uint64_t d = (((C.lo & tz) != 0) != (((C.lo & plo) | (C.hi & phi)) != 0)) ? ~0ull : 0ull;
-                    C.lo ^= d & (tz | plo);
-                    C.hi ^= d & phi;
-                    const bool a = col > c && (C.lo & tz);
-                    C.lo ^= a ? elo : 0ull;
-                    C.hi ^= a ? ehi : 0ull;
-                }
-                // only real steps are stored (predicated, not branched): every lane then
-                // writes identical values, so a reader acquiring the count from any lane's
-                // release sees the step whichever lane's store it observes
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\t"
-                    "setp.ne.u32 p, %0, 0;\n\t"
-                    "@p st.shared.v2.u64 [%1], {%2, %3};\n\t"
-                    "@p st.shared.u32 [%4], %5;\n\t}"
-                    ::"r"(static_cast<unsigned>(!zero)),
-                    "r"(static_cast<unsigned>(__cvta_generic_to_shared(&F.step_m[t]))), "l"(clo), "l"(mhi),
-                    "r"(static_cast<unsigned>(__cvta_generic_to_shared(&F.step_c[t]))), "r"(c)
-                    : "memory");
-                t += zero ? 0 : 1;
-                tb = zero ? tb : tb << 1;
-                tm = zero ? tm : tm << 1;
-                // every lane stored the same step and releases the same word: no branch
-                asm volatile("st.release.cta.shared.u32 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(const_cast<int*>(&F.q_n)))), "r"(static_cast<unsigned>(((c + 1) << 8) | t)) : "memory");
-            }
-            // a column without candidates is undecidable when rows past the window could hold them
-            ok = ok && !(more && t - t0 < c1 - c0);  // (c1 < c0 for narrow leaves)
-            F2_CLK(if (lane == 0) F.clk[phase][1] = clock64();)
-        } else if (c0 < lw) {
-            // replay the other warp's steps as they are published
-            const int t0 = t;
-            while (true) {
-                const unsigned v = progress();
-                for (; t < static_cast<int>(v & 255u); ++t) apply(t, F.step_m[t], w > phase);
-                if (static_cast<int>(v >> 8) >= c1) {
-                    ok = ok && !(more && t - t0 < c1 - c0);
-                    break;
-                }
-            }
-        }
-        if (!ok) break;
-    }
-    if (lane == 0 && w == 0) F.final_kb = ok ? t : -1;
-    if (w < 2) F.cfin[col] = C.lo;
-    if (ok && w < 2 && col < t) {  // pivot slot of every step, from its candidate mask
-        const ulonglong2 m = F.step_m[col];
-        F.step_p[col] = m.x ? __ffsll(static_cast<long long>(m.x)) - 1 : 63 + __ffsll(static_cast<long long>(m.y));
-    }
-    if (ok && w < 2) {
-        // pivot rows' final leaf words (slots 0..63), this warp's 32 columns
-        const uint32_t r0 = warp_transpose32(static_cast<uint32_t>(C.lo), lane);
-        const uint32_t r1 = warp_transpose32(static_cast<uint32_t>(C.lo >> 32), lane);
-        if (w == 0) {
-            F.ufl[lane] = r0;
-            F.ufl[lane + 32] = r1;
-        } else {
-            F.ufh[lane] = r0;
-            F.ufh[lane + 32] = r1;
-        }
-    }
-    asm volatile("bar.sync 1, 96;\n" ::: "memory");
-    if (ok && w == 0) {
-        const uint64_t u0 = F.ufl[lane] | (static_cast<uint64_t>(F.ufh[lane]) << 32);
-        const uint64_t u1 = F.ufl[lane + 32] | (static_cast<uint64_t>(F.ufh[lane + 32]) << 32);
-        F.uf[lane] = u0;
-        F.uf[lane + 32] = u1;
-        if (want_linv) warp_linv(F, t);
     }
 }
 

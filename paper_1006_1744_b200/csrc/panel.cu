@@ -34,11 +34,6 @@ namespace f2g {
 namespace {
 
 constexpr int kPT = 1024;                  // threads per CTA
-#ifdef F2_ONE_WARP_PIVOTS
-constexpr bool kSrcFromSearch = false;
-#else
-constexpr bool kSrcFromSearch = true;      // the two-warp search's tracker warp leaves the slot sources
-#endif
 constexpr int kRows = (kPT / 32) * 4 * 4;  // rows per update tile (512): 4 lane groups x 4 rows per warp
 constexpr int kW = 16;                     // words of the panel remainder a tile covers (W <= 1024)
 constexpr int kTab = 256 * kW;             // one 8-bit group table (CTA 0's fallback solve), words
@@ -576,7 +571,7 @@ __device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSm
 // and the carry tables, and returns kb; -1 when the window cannot decide a column.
 __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int lw, PlsState* st, int64_t* P,
                               int64_t* Qp, int64_t* pmap, int64_t qcol_off, PipeSmem& S, PipeStatic& Z, int pb,
-                              PlsState::Packet* pk, int nleaves, bool carried, bool past_zero) {
+                              PlsState::Packet* pk, int nleaves, bool carried, bool past_zero, bool& search4) {
     __shared__ FastSmem F;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = A.m, stride = A.stride;
@@ -585,68 +580,51 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     const int nrest = nwp - leaf - 1;  // rest words right of the leaf
     const bool first = leaf == 0;
     const int64_t wl = pw0 + leaf;
-    if (warp < 8) {  // leaf word -> column form
-        const int rb = warp & 3, h = warp >> 2;
-        const uint64_t w = S.win[pb][rb * 32 + lane][leaf];
-        F.colw[(32 * h + lane) * 4 + rb] = warp_transpose32(static_cast<uint32_t>(w >> (32 * h)), lane);
-    }
-    __syncthreads();
     F2_STAMP(st, 16);
     F2_CLK(const bool clk = pw0 == 0 && leaf == 2 && tid == 0; long long c0 = clock64();)
-#ifdef F2_ONE_WARP_PIVOTS
-    if (warp == 0) warp0_pivots(F, lw, base + kPW < m, true, st);
-#else
-    if (warp < 3) two_warp_pivots(F, lw, base + kPW < m && !past_zero, false);
-#endif
+    if (warp == 0) {
+        // the first 96 slots decide a dense leaf; all 128 when they cannot (rank-deficient / sparse)
+        // (search4, sticky for the panel: a leaf needed all 128, so will the next ones)
+        if (lane == 0) F.used4 = 0;
+        if (search4 || row_pivots<3>(F, &S.win[pb][0][leaf], lw, base + 96 < m) < 0) {
+            __syncwarp();
+            row_pivots<4>(F, &S.win[pb][0][leaf], lw, base + kPW < m && !past_zero);
+            if (lane == 0) F.used4 = 1;
+        }
+    }
     // meanwhile the other warps finish the carried window: the previous leaf's update of
     // the words right of this leaf's (pipe_build_window did this leaf's word)
-    // (warps 3, 7, ..., 31 only: the fourth scheduler, away from the selecting warps 0 and 1)
+    // (warps 3, 7, ..., 31 only: the fourth scheduler, away from the searching warp 0)
     if ((warp & 3) == 3 && carried) pipe_phase2(S, pb, leaf - 1, leaf + 1, nwp, (warp >> 2) * 32 + (tid & 31), kPT / 4);
     __syncthreads();
-    F2_CLK(if (clk) { st->dbg[20] = clock64() - c0; st->dbg[29] = F.clk[0][1] - F.clk[0][0]; st->dbg[31] = F.clk[1][1] - F.clk[1][0]; })
+    F2_CLK(if (clk) { st->dbg[20] = clock64() - c0; st->dbg[29] = F.clk[1] - F.clk[0]; })
     F2_STAMP(st, 18);
     const int kb = F.final_kb;
+    if (F.used4) search4 = true;
     if (kb < 0) return -1;
 
-    // warp 0: L11^-1 while the others derive everything that does not need it
-#ifndef F2_ONE_WARP_PIVOTS
-    if (warp < 2) pair_linv(F, kb);
-    F2_CLK(if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;)
-    if (false) {  // slot sources come from the search's tracker warp
-#else
-    if (tid >= 32 && tid < 32 + kPW) {  // slot sources (transpositions backwards, perm.cpp:8-16)
-#endif
-        const int sl = tid - 32;
-        int x = sl;
-        for (int u0 = (kb - 1) & ~7; u0 >= 0; u0 -= 8) {
-            int pv[8];
+    // warps 0-1: L11^-1, while the others derive everything that does not need it (the slot
+    // sources and the column -> pivot map came with the search)
+    if (warp < 2) {
+        pair_linv_rows(F, kb);
+        F2_CLK(if (pw0 == 0 && leaf == 2 && tid == 0) st->dbg[28] = clock64() - c0;)
+    } else if (tid < 128) {
+        // finalize basis: what the unit word e (bit e of the leaf word) receives from the pivots
+        // of its own byte group, applied in column order (x has bit q: x ^= U above q)
+        const int e = tid - 64, g = e >> 3;
+        uint64_t uw[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) pv[i] = F.step_p[u0 + i];
+        for (int b = 0; b < 8; ++b) {
+            const int l = F.posc[8 * g + b];
+            uw[b] = l >= 0 ? F.uf[l] & above(8 * g + b) : 0ull;
+        }
+        uint64_t x = 1ull << e, corr = 0;
 #pragma unroll
-            for (int i = 7; i >= 0; --i) {
-                const int u = u0 + i;
-                if (u < kb) x = x == u ? pv[i] : (x == pv[i] ? u : x);
+        for (int b = 0; b < 8; ++b)
+            if ((x >> (8 * g + b)) & 1ull) {
+                x ^= uw[b];
+                corr ^= uw[b];
             }
-        }
-        F.src[sl] = x;
-        F2_CLK(if (pw0 == 0 && leaf == 2 && tid == 32) st->dbg[29] = clock64() - c0;)
-    } else if (tid >= 32 + kPW && tid < 32 + kPW + 64) {  // finalize basis
-        const int e = tid - 32 - kPW, g = e >> 3, b = e & 7;
-        int lo = 0, hi = kb;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (F.step_c[mid] < 8 * g) lo = mid + 1;
-            else hi = mid;
-        }
-        uint64_t x = 1ull << (8 * g + b), corr = 0;
-        for (int l = lo; l < kb && F.step_c[l] < 8 * g + 8; ++l) {
-            const int q = F.step_c[l];
-            if ((x >> q) & 1ull) {
-                const uint64_t ul = F.uf[l] & above(q);
-                x ^= ul;
-                corr ^= ul;
-            }
-        }
         pk->fb[e] = corr;
         F.fbas[e] = corr;
         F2_CLK(if (pw0 == 0 && leaf == 2 && e == 63) st->dbg[30] = clock64() - c0;)
@@ -658,8 +636,7 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->ufull[l] = in ? F.uf[l] : 0ull;
         st->q[l] = q;
         pk->q[l] = q;
-        F.posc[l] = -1;
-    } else if (tid >= 320 && kSrcFromSearch) {
+    } else if (tid >= 320) {
         // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order): they need
         // only the slot sources, so they are built here, beside L11^-1, by the idle threads
         for (int i = tid - 320; i < 16 * 16 * nrest; i += kPT - 320) {
@@ -685,19 +662,8 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
             if ((v >> b) & 1) f ^= F.fbas[8 * g + b];
         S.F[i] = f;
     }
-    if (tid < kb) F.posc[F.step_c[tid]] = tid;
     if (tid >= 960) pk->linv[tid - 960] = F.linv[tid - 960];  // the lmap is a worker's job
     if (tid == 0) pk->leaf = leaf;
-    if (!kSrcFromSearch) {  // (one-warp search: the slot sources were derived above)
-        for (int i = tid; i < 16 * 16 * nrest; i += kPT) {
-            const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
-            uint64_t v = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
-            S.t16[ge * 15 + k] = v;
-        }
-    }
     __syncthreads();
     F2_CLK(if (clk) st->dbg[26] = clock64() - c0;)
     F2_STAMP(st, 21);
@@ -820,6 +786,9 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
     // panel, so the window decides every column (past_zero, sticky) -- a zero column no
     // longer sends the leaf to the general search.
     bool past_zero = false;
+    // (CTA 0) the 96-slot pivot search could not decide a leaf of this panel, or an earlier
+    // panel needed the general search (rank-deficient / sparse input): search all 128 slots
+    bool search4 = __ldcg(&st->hint) != 0;
     unsigned nscan = 0;
     __shared__ int s_pz;
     int64_t state = S_FRESH, leaf = 0, wpk = -1, wleaf = 0;
@@ -873,7 +842,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                     const int lw = width - 64 * j < 64 ? width - 64 * j : 64;
                     PlsState::Packet* pk = &st->pk[pkc & 1];
                     const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves,
-                                                  state == S_CARRY, past_zero);
+                                                  state == S_CARRY, past_zero, search4);
                     F2_STAMP(st, 2);
                     if (kb >= 0) {
                         kbprev = kb;
