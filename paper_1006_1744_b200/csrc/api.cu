@@ -64,6 +64,8 @@ struct Tuning {
     int side_ctas = 24;           // F2_SIDE_CTAS: CTAs of the look-ahead panel kernel, early panels
     int side_ctas_late = 48;      // F2_SIDE_CTAS_LATE: late panels (0: as early)
     int late_pct = 38;            // F2_LATE_PCT: first late panel, % of the panels
+    int wide_early_pct = 62;      // F2_WIDE_EARLY_PCT: panels (%) whose wide TRSM runs early on aux (-1: late_pct)
+    bool tw_join_at_fork = false; // F2_TW_JOIN=1: the next panel's kernel waits for the early wide TRSM
     // panel width of the mmpf_pls entry point: its output is the Gaussian one whatever the
     // blocking, and 1024-column panels are 3-6x faster on dense inputs than the paper's
     // 64-column MMPF schedule (F2_MMPF_PANEL_BITS=64: panel kernel + HBM-streaming table-apply)
@@ -100,6 +102,8 @@ struct Tuning {
         const int sl = num("F2_SIDE_CTAS_LATE", side_ctas_late);
         if (sl == 0 || (sl >= 2 && sl <= nsm)) side_ctas_late = sl;
         late_pct = num("F2_LATE_PCT", late_pct);
+        wide_early_pct = num("F2_WIDE_EARLY_PCT", wide_early_pct);
+        tw_join_at_fork = flag("F2_TW_JOIN");
         const int mb = num("F2_MMPF_PANEL_BITS", static_cast<int>(mmpf_bits));
         if (mb >= 64 && mb <= 1024 && mb % 64 == 0) mmpf_bits = static_cast<unsigned>(mb);
         stream_upload = !flag("F2_NO_STREAM_UPLOAD");
@@ -567,7 +571,10 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
                                       : (tune.side_ctas_late > 0 && late ? tune.side_ctas_late : tune.side_ctas);
     const int64_t nx = ps.lookahead ? ps.nx : t0;
     const bool split = ps.lookahead && !late && tune.split_early && f4 && nx < nw;
-    const bool wide_early = ps.lookahead && !late && tune.early_wide_trsm && nx < nw;
+    const bool late_we = tune.wide_early_pct < 0
+                             ? late
+                             : 100 * (ps.p + 1) >= tune.wide_early_pct * std::max<int64_t>(ps.npanels, 1);
+    const bool wide_early = ps.lookahead && !late_we && tune.early_wide_trsm && nx < nw;
     auto schur = [&](cudaStream_t st, int64_t c0, int64_t c1, int region, int grid) -> int {
         if (c1 <= c0) return F2_OK;
         SchurTimed tm{ps.p, c0, c1, nullptr, nullptr};
@@ -637,10 +644,10 @@ int enqueue_panel_step(const PanelStep& ps, cudaStream_t s, cudaStream_t sd, Fac
         if (f4) CK(cudaStreamWaitEvent(s, g.ax_join, 0));
         if ((rc = schur(s, t0, nx, 0, g.nsm))) return rc;
         evmark(s, "schur_narrow", ps.p);
-        // the next panel's kernel never runs beside the wide TRSM: with the two overlapping,
-        // panel p+1's pivoting was seen to diverge (a few runs in 20 at 64K^2, early panels
-        // only); the TRSM is nearly always done by now, so the wait costs ~nothing
-        if (wide_early) CK(cudaStreamWaitEvent(s, g.tw_join, 0));
+        // (F2_TW_JOIN: the next panel's kernel waits for the early wide TRSM.  A divergence
+        // once attributed to the two overlapping was a race inside the old column-form pivot
+        // search; they touch disjoint columns)
+        if (wide_early && tune.tw_join_at_fork) CK(cudaStreamWaitEvent(s, g.tw_join, 0));
         CK(cudaEventRecord(g.la_fork, s));
         CK(cudaStreamWaitEvent(sd, g.la_fork, 0));
         factor_next(sd, side);

@@ -51,6 +51,8 @@ SCRIPT = textwrap.dedent("""
     {"F2_NO_GRAPH": "1"},
     {"F2_NO_PDL": "1"},
     {"F2_NO_EARLY_WIDE_TRSM": "1"},
+    {"F2_WIDE_EARLY_PCT": "-1", "F2_TW_JOIN": "1"},
+    {"F2_WIDE_EARLY_PCT": "100"},
     {"F2_SPLIT_EARLY": "1"},
     {"F2_SPLIT_EARLY": "1", "F2_NO_EARLY_WIDE_TRSM": "1"},
     {"F2_SIDE_CTAS": "8", "F2_SIDE_CTAS_LATE": "0"},
