@@ -1464,9 +1464,10 @@ int f2_debug_prof(long long* out, int n) {
 
 int f2_debug_clocks(long long* out, int n) {
     if (!g.init || !out || n <= 0) return F2_INVALID_ARGUMENT;
-    long long tmp[32];
+    long long tmp[96];  // dbg[32] then prof[64] (contiguous in PlsState)
+    static_assert(offsetof(PlsState, prof) == offsetof(PlsState, dbg) + 32 * sizeof(long long), "dbg/prof layout");
     CK(cudaMemcpy(tmp, &g.st->dbg[0], sizeof(tmp), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n && i < 32; ++i) out[i] = tmp[i];
+    for (int i = 0; i < n && i < 96; ++i) out[i] = tmp[i];
     return F2_OK;
 }
 

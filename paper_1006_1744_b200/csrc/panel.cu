@@ -802,6 +802,8 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
             wleaf = s_ctl[3];
             __syncthreads();
         }
+        // (clocks build) CTA 0's iteration starts of a late panel (panel 56 of a 64-panel run)
+        F2_CLK(if (pw0 == 16 * 56 && blockIdx.x == 0 && threadIdx.x == 0 && it < 24) st->prof[32 + it] = clock64();)
         if (state == S_DONE) break;
 #ifdef F2_PANEL_PROFILE
         if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = (pw0 == 0 && leaf == 2 && state == S_CARRY);
