@@ -804,6 +804,8 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
         }
         // (clocks build) CTA 0's iteration starts of a late panel (panel 56 of a 64-panel run)
         F2_CLK(if (pw0 == 16 * 56 && blockIdx.x == 0 && threadIdx.x == 0 && it < 24) st->prof[32 + it] = clock64();)
+        F2_CLK(const bool lclk = pw0 == 16 * 56 && blockIdx.x == 0 && threadIdx.x == 0 && it == 5;)
+        F2_CLK(if (lclk) st->dbg[1] = clock64();)  // control word read
         if (state == S_DONE) break;
 #ifdef F2_PANEL_PROFILE
         if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = (pw0 == 0 && leaf == 2 && state == S_CARRY);
@@ -836,6 +838,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                 pipe_build_window(A, pw0, nwp, pmap, st, S, Z, pb, state != S_FRESH, kbprev, j - 1,
                                   j == 0 ? 0 : st->pmap_hi, state == S_FINAL);
                 F2_CLK(if (pw0 == 0 && j == 2 && threadIdx.x == 0) st->dbg[22] = clock64() - cb;)
+                F2_CLK(if (lclk) st->dbg[2] = clock64();)  // window built
                 F2_STAMP(st, 1);
                 if (state == S_FINAL) {
                     pipe_write_back(A, pw0, nwp, S, Z, pb);
@@ -845,6 +848,7 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                     PlsState::Packet* pk = &st->pk[pkc & 1];
                     const int kb = pipe_fast_leaf(A, pw0, nwp, j, lw, st, P, Qp, pmap, qcol_off, S, Z, pb, pk, nleaves,
                                                   state == S_CARRY, past_zero, search4);
+                    F2_CLK(if (lclk) st->dbg[3] = clock64();)  // leaf done
                     F2_STAMP(st, 2);
                     if (kb >= 0) {
                         kbprev = kb;
@@ -920,7 +924,9 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
         if (threadIdx.x == 0 && blockIdx.x == 0) g_prof_on = 0;
 #endif
         F2_CLK(const long long cbar = clock64();)
+        F2_CLK(if (lclk) st->dbg[4] = cbar;)  // at the grid barrier
         grid_barrier(bar, target);
+        F2_CLK(if (lclk) st->dbg[5] = clock64();)  // barrier passed
         F2_CLK(if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 0) st->dbg[23] = clock64() - cbar;)
         F2_CLK(if (pw0 == 0 && leaf == 2 && threadIdx.x == 0 && blockIdx.x == 1) st->dbg[24] = clock64() - cbar;)
     }

@@ -241,3 +241,34 @@ def test_host_streamed_upload(f2, oracle, m, n, kind):
             assert res.rank == r and (res.P == p).all(), (m, n, kind, recursive, rep)
             assert (res.Q == (qr if recursive else q)).all(), (m, n, kind, recursive, rep, "Q")
             assert (h == w).all(), (m, n, kind, recursive, rep, "packed")
+
+
+def test_pivot_search_window_tiers(f2, oracle):
+    """The fast pivot search looks at the first 96 window slots, then all 128, then falls back
+    to the general search (csrc/leaf_body.cuh row_pivots, panel.cu): inputs whose pivots sit
+    only in slots 96-127, only past the window, or alternate between the tiers from leaf to
+    leaf, with zero columns in between (gauss.cpp:33-49 is the rule in every tier)."""
+    rng = np.random.default_rng(96128)
+    cases = []
+    for m, n, zero_rows in [(200, 64, 96), (200, 200, 100), (300, 130, 127), (300, 200, 128), (400, 256, 200),
+                            (130, 64, 97), (97, 97, 96), (129, 300, 128), (1000, 192, 96)]:
+        a = oracle.randomize(m, n, 0.5, int(rng.integers(1, 2 ** 62)))
+        a[:zero_rows, :] = 0
+        cases.append((a, n))
+    # per 64-column leaf a different band of rows is nonzero: 0-95, 96-127, past 128, none
+    m, n = 520, 512
+    a = np.zeros((m, words(n)), dtype=np.uint64)
+    full = oracle.randomize(m, n, 0.5, 7)
+    bands = [(0, 96), (96, 128), (128, 520), (0, 0), (100, 120), (300, 310), (0, 520), (127, 129)]
+    for j, (r0, r1) in enumerate(bands):
+        a[r0:r1, j] = full[r0:r1, j]
+    cases.append((a, n))
+    # sparse columns: few candidates, most of them deep in the order
+    a = np.zeros((700, words(256)), dtype=np.uint64)
+    for c in range(256):
+        for r in rng.integers(0, 700, size=2):
+            a[r, c // 64] |= np.uint64(1) << np.uint64(c % 64)
+    cases.append((a, 256))
+    for a, n in cases:
+        check_against_oracle(f2, oracle, a, n, recursive_cutoff=4096)
+        check_against_oracle(f2, oracle, a, n)

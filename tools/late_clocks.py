@@ -18,3 +18,6 @@ L.f2_debug_clocks(out, 96)
 v = list(out)[64:88]
 print("iteration starts (cycles from the first):", [x - v[0] for x in v if x])
 print("per iteration:", [v[i + 1] - v[i] for i in range(len(v) - 1) if v[i + 1] and v[i]])
+d = list(out)[:8]
+print(f"iteration 5 of panel 56 (cycles): window build {d[2]-d[1]}, leaf {d[3]-d[2]}, to the barrier {d[4]-d[3]}, "
+      f"barrier {d[5]-d[4]}, control word of the next iteration {out[64+6]-d[5]}")
