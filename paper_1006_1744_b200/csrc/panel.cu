@@ -636,16 +636,21 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         st->ufull[l] = in ? F.uf[l] : 0ull;
         st->q[l] = q;
         pk->q[l] = q;
-    } else if (tid >= 320) {
+    } else if (tid >= 320 && tid < 576) {
         // 4-bit tables over A12 (the pivot rows' pre-leaf rest words, pivot order): they need
-        // only the slot sources, so they are built here, beside L11^-1, by the idle threads
-        for (int i = tid - 320; i < 16 * 16 * nrest; i += kPT - 320) {
-            const int ge = i / nrest, k = i - ge * nrest, g = ge >> 4, e = ge & 15;
-            uint64_t v = 0;
+        // only the slot sources, so they are built here, beside L11^-1.  Thread = (group g of
+        // four pivots, rest word k): four loads, then the sixteen subset sums in Gray order
+        const int g = (tid - 320) >> 4, k = (tid - 320) & 15;
+        if (k < nrest) {
+            uint64_t v[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (((e >> b) & 1) && 4 * g + b < kb) v ^= S.win[pb][F.src[4 * g + b]][leaf + 1 + k];
-            S.t16[ge * 15 + k] = v;
+            for (int b = 0; b < 4; ++b) v[b] = 4 * g + b < kb ? S.win[pb][F.src[4 * g + b]][leaf + 1 + k] : 0ull;
+            uint64_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (i) x ^= v[(i & 1) ? 0 : ((i & 2) ? 1 : ((i & 4) ? 2 : 3))];  // the bit that flips in i ^ (i >> 1)
+                S.t16[((g << 4) | (i ^ (i >> 1))) * 15 + k] = x;
+            }
         }
     }
     if (first)
@@ -653,20 +658,6 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
     __syncthreads();
     F2_CLK(if (clk) st->dbg[25] = clock64() - c0;)
     F2_STAMP(st, 19);
-    // carry finalize tables from the basis; posc; L11^-1 rows in raw columns (for lmap)
-    for (int i = tid; i < 8 * 256; i += kPT) {
-        const int g = i >> 8, v = i & 255;
-        uint64_t f = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-            if ((v >> b) & 1) f ^= F.fbas[8 * g + b];
-        S.F[i] = f;
-    }
-    if (tid >= 960) pk->linv[tid - 960] = F.linv[tid - 960];  // the lmap is a worker's job
-    if (tid == 0) pk->leaf = leaf;
-    __syncthreads();
-    F2_CLK(if (clk) st->dbg[26] = clock64() - c0;)
-    F2_STAMP(st, 21);
     // solved rest words U_l = sum over t of Linv[l][t] A12_t
     for (int i = tid; i < 64 * 16; i += kPT) {
         const int l = i >> 4, k = i & 15;
@@ -679,6 +670,20 @@ __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int 
         S.U[i] = acc;
         if (k >= 1) pk->u[l][k - 1] = acc;
     }
+    // in the same phase (nothing here feeds the solve): the carry finalize tables from the
+    // basis and the packet's L11^-1 rows (the lmap is a worker's job)
+    for (int i = tid; i < 8 * 256; i += kPT) {
+        const int g = i >> 8, v = i & 255;
+        uint64_t f = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if ((v >> b) & 1) f ^= F.fbas[8 * g + b];
+        S.F[i] = f;
+    }
+    if (tid >= 960) pk->linv[tid - 960] = F.linv[tid - 960];
+    if (tid == 0) pk->leaf = leaf;
+    F2_CLK(if (clk) st->dbg[26] = clock64() - c0;)
+    F2_STAMP(st, 21);
     const int mv0 = first ? 0 : static_cast<int>(st->nmoved);
     const int64_t pkb = first ? 0 : st->panel_kb;
     int moved = 0, off = 0;
