@@ -428,7 +428,7 @@ __device__ void publish_from_state(const PlsState* st, PlsState::Packet* pk) {
 // kb rows of the order, and CTA 0 itself applies leaf j's update to all 128.  So the
 // search for leaf j+1 needs nothing from the other CTAs, which meanwhile apply leaf
 // j to every row past the next window.  One grid barrier per leaf, and the row
-// updates run concurrently with the next pivot search.  A leaf the column-form search
+// updates run concurrently with the next pivot search.  A leaf the window search
 // cannot decide inside the window (rank-deficient / sparse inputs) falls back to the
 // general search on the global matrix: CTA 0 writes its window back, waits for the
 // workers, searches, then the workers update everything before a fresh window.
@@ -566,7 +566,7 @@ __device__ void pipe_write_back(const Mat& A, int64_t pw0, int nwp, const PipeSm
     }
 }
 
-// Column-form search of leaf `leaf` on window buffer pb; on success publishes every
+// Row-form search (leaf_body.cuh, row_pivots) of leaf `leaf` on window buffer pb; on success publishes every
 // output (P, Q, pmap moves, pivot rows' slices, state, panel-TRSM map, worker packet)
 // and the carry tables, and returns kb; -1 when the window cannot decide a column.
 __device__ int pipe_fast_leaf(const Mat& A, int64_t pw0, int nwp, int leaf, int lw, PlsState* st, int64_t* P,
