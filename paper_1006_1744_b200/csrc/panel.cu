@@ -868,6 +868,18 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
                         // its TRSM map there), so the empty panels after full row rank cost
                         // one leaf instead of sixteen
                         if (st->r >= A.m) nstate = S_FINAL;
+                        // a leaf without pivots while no row past the window is nonzero in the
+                        // panel's remaining words (past_zero): if the window's remaining words
+                        // are zero too, no column of this panel can hold another pivot -- the
+                        // rank-deficient panels past the rank cost one or two leaves, not sixteen
+                        if (nstate == S_CARRY && kb == 0 && past_zero) {
+                            uint64_t acc = 0;
+                            for (int i = threadIdx.x; i < kPW * 16; i += kPT) {
+                                const int k = i & 15;
+                                if (k > j && k < nwp) acc |= S.win[pb][i >> 4][k];
+                            }
+                            if (!__syncthreads_or(acc != 0)) nstate = S_FINAL;
+                        }
                     } else {  // undecidable in the window: hand the window back, search globally
                         pipe_write_back(A, pw0, nwp, S, Z, pb);
                         nstate = S_GENERAL;
