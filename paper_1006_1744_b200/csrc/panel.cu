@@ -783,6 +783,25 @@ k_panel_pipe(Mat A, int64_t pw0, int width, int64_t pw1, PlsState* st, int64_t* 
 #ifdef F2_TIMELINE
     if (threadIdx.x == 0) atomicMin(&st->tl[0][(pw0 / 16) & 127], gtimer());
 #endif
+    // Every row is a pivot already (a wide matrix past its row rank): the panel has nothing to
+    // pivot or update.  Every CTA sees the same r (final since the previous panel's kernel) and
+    // leaves at once; CTA 0 publishes the empty panel for the gather / TRSM / Schur launches.
+    if (ldi(&st->r) >= A.m) {
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i < nleaves * 64; i += kPT) st->brow[i] = -1;
+            if (threadIdx.x == 0) {
+                const int64_t r = ldi(&st->r);
+                st->leaf_mask = 0;
+                st->nmoved = 0;
+                st->pmap_hi = 0;
+                st->leaf_r = r;
+                st->leaf_kb = 0;
+                st->panel_r = r;
+                st->panel_kb = 0;
+            }
+        }
+        return;
+    }
     int kbprev = 0, pkc = 0;  // CTA 0's carry state (uniform across its threads)
     // Rank-deficient / sparse panels: after a leaf needed the general search (st->hint), each
     // fresh window has the idle workers check whether any row past it is nonzero in the

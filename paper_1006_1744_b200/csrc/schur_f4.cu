@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(256) k_f4_expand_a(F4Job jb, uint8_t* __restri
 __global__ void __launch_bounds__(256) k_f4_expand_b(F4Job jb, uint8_t* __restrict__ Bx, int nst, unsigned* claim) {
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *claim = 0u;
+    if (jb.rows_end - f4_row_shift(jb) <= 0) return;  // no rows below the pivots: the product is empty
     const int lane = threadIdx.x & 31;
     const int64_t nhw = 2 * (jb.cw1 - jb.cw0);
     const int64_t nct = (nhw + kFHW - 1) / kFHW;
