@@ -877,6 +877,9 @@ int enqueue_engine(const Mat& A, unsigned W, cudaStream_t s, bool poll) {
 // Graph cache: the launch sequence depends only on (matrix, m, n, stride, W) and the
 // workspace buffers, so square-ish factorisations replay one captured CUDA graph
 // (per-launch overhead of ~3300 small launches at 64K^2 drops to graph-node cost).
+// A few graphs are kept (round-robin eviction): a caller alternating between matrix
+// buffers, or between shapes, pays the capture + instantiation (~19 ms at 64K^2) once per
+// buffer instead of on every call.
 struct GraphCache {
     uint64_t* w = nullptr;
     uint64_t* dl_host = nullptr;
@@ -886,9 +889,12 @@ struct GraphCache {
     int64_t m = 0, n = 0, stride = 0;
     unsigned W = 0;
     uint64_t gen = 0;
+    uint64_t launches = 0, kernels = 0;  // enqueued launches / kernel nodes per replay
     cudaGraphExec_t exec = nullptr;
 };
-GraphCache g_graph;
+constexpr int kGraphSlots = 4;
+GraphCache g_graphs[kGraphSlots];
+int g_graph_next = 0;
 uint64_t g_ws_gen = 1;  // bumped whenever a workspace buffer is reallocated
 
 int run_engine(const Mat& A, unsigned W, EngineOut& out) {
@@ -911,13 +917,16 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
     const bool use_graph = !g.stats && nw >= 32 && n <= 2 * m && tune.graph;
     g_evtl = !use_graph && tune.evtl;
     if (use_graph) {
-        const bool hit = g_graph.exec && g_graph.w == A.w && g_graph.m == m && g_graph.n == n &&
-                         g_graph.stride == A.stride && g_graph.W == W && g_graph.gen == g_ws_gen &&
-                         g_graph.dl_host == g.dl_host && g_graph.dl_pitch == g.dl_pitch &&
-                         g_graph.ul_host == g.ul_host && g_graph.ul_pitch == g.ul_pitch;
-        if (!hit) {
-            if (g_graph.exec) cudaGraphExecDestroy(g_graph.exec);
-            g_graph.exec = nullptr;
+        GraphCache* gc = nullptr;
+        for (auto& c : g_graphs)
+            if (c.exec && c.w == A.w && c.m == m && c.n == n && c.stride == A.stride && c.W == W && c.gen == g_ws_gen &&
+                c.dl_host == g.dl_host && c.dl_pitch == g.dl_pitch && c.ul_host == g.ul_host && c.ul_pitch == g.ul_pitch)
+                gc = &c;
+        if (!gc) {
+            gc = &g_graphs[g_graph_next];
+            g_graph_next = (g_graph_next + 1) % kGraphSlots;
+            if (gc->exec) cudaGraphExecDestroy(gc->exec);
+            gc->exec = nullptr;
             cudaGraph_t graph;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             const uint64_t l0 = g.launches;
@@ -926,37 +935,41 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
             cudaError_t e = cudaStreamEndCapture(s, &graph);
             if (rc) return rc;
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+            uint64_t nk = 0;
             {  // kernel launches per call = the graph's kernel nodes
                 size_t nn = 0;
                 cudaGraphGetNodes(graph, nullptr, &nn);
                 std::vector<cudaGraphNode_t> nodes(nn);
                 if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
-                uint64_t nk = 0;
                 for (auto nd : nodes) {
                     cudaGraphNodeType ty;
                     if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++nk;
                 }
-                g.graph_kernels = nk;
             }
-            e = cudaGraphInstantiate(&g_graph.exec, graph, 0);
+            e = cudaGraphInstantiate(&gc->exec, graph, 0);
             cudaGraphDestroy(graph);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-            g_graph.w = A.w;
-            g_graph.dl_host = g.dl_host;
-            g_graph.dl_pitch = g.dl_pitch;
-            g_graph.ul_host = g.ul_host;
-            g_graph.ul_pitch = g.ul_pitch;
-            g_graph.m = m;
-            g_graph.n = n;
-            g_graph.stride = A.stride;
-            g_graph.W = W;
-            g_graph.gen = g_ws_gen;
-            g.graph_launches = per_call;
+            if (e != cudaSuccess) {
+                gc->exec = nullptr;
+                return cuda_fail(e, "cudaGraphInstantiate");
+            }
+            gc->w = A.w;
+            gc->dl_host = g.dl_host;
+            gc->dl_pitch = g.dl_pitch;
+            gc->ul_host = g.ul_host;
+            gc->ul_pitch = g.ul_pitch;
+            gc->m = m;
+            gc->n = n;
+            gc->stride = A.stride;
+            gc->W = W;
+            gc->gen = g_ws_gen;
+            gc->launches = per_call;
+            gc->kernels = nk;
         } else {
-            g.launches += g.graph_launches;
+            g.launches += gc->launches;
         }
-        g.last_kernels = g.graph_kernels;
-        CK(cudaGraphLaunch(g_graph.exec, s));
+        g.graph_launches = gc->launches;
+        g.graph_kernels = g.last_kernels = gc->kernels;
+        CK(cudaGraphLaunch(gc->exec, s));
     } else {
         rc = enqueue_engine(A, W, s, true);
         if (rc) return rc;
