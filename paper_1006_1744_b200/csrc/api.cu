@@ -925,8 +925,15 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
         if (!gc) {
             gc = &g_graphs[g_graph_next];
             g_graph_next = (g_graph_next + 1) % kGraphSlots;
-            if (gc->exec) cudaGraphExecDestroy(gc->exec);
-            gc->exec = nullptr;
+            // the evicted graph has this one's topology when only the matrix buffer differs:
+            // then its executable is updated in place (cheaper than a new instantiation)
+            const bool same_shape = gc->exec && gc->m == m && gc->n == n && gc->stride == A.stride && gc->W == W &&
+                                    gc->gen == g_ws_gen && gc->dl_host == g.dl_host && gc->dl_pitch == g.dl_pitch &&
+                                    gc->ul_host == g.ul_host && gc->ul_pitch == g.ul_pitch;
+            if (gc->exec && !same_shape) {
+                cudaGraphExecDestroy(gc->exec);
+                gc->exec = nullptr;
+            }
             cudaGraph_t graph;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             const uint64_t l0 = g.launches;
@@ -946,7 +953,17 @@ int run_engine(const Mat& A, unsigned W, EngineOut& out) {
                     if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++nk;
                 }
             }
-            e = cudaGraphInstantiate(&gc->exec, graph, 0);
+            e = cudaErrorUnknown;
+            if (gc->exec) {
+                cudaGraphExecUpdateResultInfo info;
+                e = cudaGraphExecUpdate(gc->exec, graph, &info);
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    cudaGraphExecDestroy(gc->exec);
+                    gc->exec = nullptr;
+                }
+            }
+            if (e != cudaSuccess) e = cudaGraphInstantiate(&gc->exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) {
                 gc->exec = nullptr;
