@@ -272,3 +272,25 @@ def test_pivot_search_window_tiers(f2, oracle):
     for a, n in cases:
         check_against_oracle(f2, oracle, a, n, recursive_cutoff=4096)
         check_against_oracle(f2, oracle, a, n)
+
+
+def test_graph_cache_across_buffers_and_shapes(f2, oracle):
+    """The engine replays cached CUDA graphs keyed by matrix buffer and shape (csrc/api.cu,
+    run_engine): six live buffers over four cache slots, two shapes interleaved, different
+    contents per buffer -- every call must factor its own matrix (a stale buffer pointer in a
+    replayed or in-place updated graph would factor another one)."""
+    shapes = [(2048, 2048), (2304, 2176)]
+    mats = []
+    for i in range(6):
+        m, n = shapes[i % 2]
+        a = oracle.randomize(m, n, 0.5, 9000 + i)
+        mats.append((a, m, n, oracle.gauss_pls(a, n)))
+    bufs = [f2.DeviceMatrix(m, n) for (_, m, n, _) in mats]
+    for rnd in range(3):
+        for i in ([0, 1, 2, 3, 4, 5] if rnd != 1 else [5, 3, 1, 4, 2, 0]):
+            a, m, n, (w, p, q, r) = mats[i]
+            bufs[i].copy_from(upload(f2, a, n))
+            res = f2.pls_recursive(bufs[i], f2.EliminationConfig(cutoff_bytes=1 << 16))
+            assert res.rank == r and (res.P == p).all(), (rnd, i)
+            assert (bufs[i].download() == w).all(), (rnd, i)
+            assert (res.Q == oracle.recursive_q(m, n, 1 << 16, q[:r])).all(), (rnd, i)
